@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""Benchmark of the exact-GP BBMM hot path on B200 (BASELINE.json metric).
+
+A *step* is one mBCG iteration at n = 10^6 (houseelectric-shaped synthetic,
+d = 11, Matern-3/2 ARD, rank-100 pivoted-Cholesky preconditioner, t = 11
+right-hand sides = [y | 10 probes]): the fused on-the-fly K̂·P over all n^2
+kernel entries + the alpha/U/R update + Woodbury preconditioner + beta/P
+update, with the per-iteration convergence status read back to the host, as
+in the real solver. `value` = mBCG iterations/s of the whole job; the fused
+K·V kernel's TFLOP/s (n^2 (2d + 2t) per launch) and its SFU roofline are
+reported beside it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun (one process per GPU, NCCL): rows are sharded,
+P all-gathered and CG scalars all-reduced each iteration (strong scaling:
+total n fixed). `--impl reference` times the CPU reference path (the oracle
+port of blockgp's partitioned K̂·V + CG vector ops) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "fused K(X,X)·V TFLOP/s + mBCG iters/s at n=10^6 on 1/2/4/8 B200"
+UNIT = "mBCG iters/s"
+T_RHS = 11
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", default="M1e6")
+    ap.add_argument("--n", type=int, default=0, help="override n (testing only)")
+    ap.add_argument("--algo", type=int, default=0, help="0 auto, 1 SIMT, 2 tcgen05")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons through NVML during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x1: "gpu_idle", 0x2: "applications_clocks_setting",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index=0, period=0.1):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period = period
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"})}
+
+
+def workload_inputs(wkey, n_override=0):
+    import numpy as np
+    from paper_1903_08114_b200 import synthetic as syn
+    w = syn.WORKLOADS[wkey]
+    n = n_override or w.n
+    X = syn.whitened_inputs(n, w.d, seed=0)
+    y = syn.rff_target(X, features=256, seed=1)
+    return w, n, X, y
+
+
+# --------------------------------------------------------------------------
+# CPU reference path (oracle port of blockgp; test infrastructure) — timed on
+# a bounded row sample and extrapolated linearly (cost is exactly ∝ rows,
+# partition.py:224-241).
+# --------------------------------------------------------------------------
+
+def cpu_iteration_sample(X, ls, family, noise, rank_k, rows_target_s=4.0, state=None):
+    import numpy as np
+    import oracle as O
+    hp = O.make_hp(family, 1.0, ls, noise)
+    n = X.shape[0]
+    threads = O.host_threads()
+    # the reference materialises ~0.4 GB of temporaries per worker at n=1e6
+    # (it rescales all of X per block, kernels.py:301-302); cap the pool so
+    # the host never runs out of memory, and report the workers used
+    workers = max(1, min(threads, 64))
+    rpp = 8
+    if state is None:
+        state = {"rows": rpp * workers}
+    rows = min(n, max(rpp, int(state["rows"]) // rpp * rpp))
+    V = np.random.default_rng(2).standard_normal((n, T_RHS))
+    Xs = X[:rows]
+    ranges = O.partition_ranges(rows, rpp)
+
+    def block(Xa, s, e):  # rows [s, e) of K̂ against ALL n columns
+        return O.kernel_block(hp, Xa[s:e], X, add_noise=False)
+
+    t0 = time.perf_counter()
+    O.partitioned_kernel_mvm(block, Xs, V, ranges, workers=workers)
+    t_rows = time.perf_counter() - t0
+    per_row = t_rows / rows
+    # CG vector work of one iteration on the full n (numpy, all BLAS threads):
+    # two Woodbury passes over L (n x k) and the block axpys / dots
+    L = np.random.default_rng(3).standard_normal((n, rank_k)) * 0.01
+    R = np.random.default_rng(4).standard_normal((n, T_RHS))
+    t0 = time.perf_counter()
+    c = L.T @ R
+    Zc = (R - L @ c) / noise
+    g = np.einsum("ij,ij->j", R, Zc)
+    P = Zc + 0.5 * R
+    U = R + 0.1 * P
+    _ = np.einsum("ij,ij->j", P, U) + g
+    t_vec = time.perf_counter() - t0
+    iter_s = per_row * n + t_vec
+    state["rows"] = max(rpp, int(rows * rows_target_s / max(t_rows, 1e-3)))
+    return {"iters_per_s": 1.0 / iter_s, "rows": rows, "t_rows": t_rows, "t_vec": t_vec,
+            "threads": threads, "workers": workers, "state": state}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np
+    w, n, X, y = workload_inputs(args.workload, args.n)
+    ls = w.lengthscales()
+    state = None
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_iteration_sample(X, ls, w.family, 0.1, w.rank, state=state)
+        state = r["state"]
+        if i >= args.warmup:
+            vals.append(r)
+    v = statistics.median([r["iters_per_s"] for r in vals])
+    rows = vals[-1]["rows"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded whitened U[0,1]^d inputs, RFF target)",
+        "config": {"workload": f"{w.name}: n={n} d={w.d} {w.family} ARD, t={T_RHS}, k={w.rank}",
+                   "cpu_path": "oracle port of blockgp partitioned K̂·V (numpy float64, "
+                               "thread pool, BLAS 1 thread/worker) + CG vector ops"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": vals[-1]["workers"], "kind": "port",
+                         "sample": f"{rows} rows x {n} cols of K̂·V per step (+ full-n CG vector "
+                                   f"ops), extrapolated linearly to n rows"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# --------------------------------------------------------------------------
+# GPU path
+# --------------------------------------------------------------------------
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_1903_08114_b200 as gp
+    from paper_1903_08114_b200 import _device as D, _lib, _ops
+    from paper_1903_08114_b200.cg import FusedOperator, MbcgRun
+    from paper_1903_08114_b200.distributed import TorchComm
+    from paper_1903_08114_b200.likelihood import build_kernel_preconditioner, draw_probes_device
+
+    lib = _lib.lib()
+    peaks, peak_kind = load_peaks()
+    w, n, X, y = workload_inputs(args.workload, args.n)
+    ls = w.lengthscales()
+    model = gp.KernelModel(w.family, 1.0, ls, 0.1)
+    comm = TorchComm(n) if world > 1 else None
+    r0, r1 = (comm.row0, comm.row1) if comm else (0, n)
+
+    ps = D.points(X)
+    Xs32, _ = ps.scaled(ls)
+    precond = build_kernel_preconditioner(model, ps, w.rank)  # redundant per rank
+    Z = draw_probes_device(n, T_RHS - 1, 0, precond)
+    B = torch.cat([D.to_device(y)[:, None], Z], dim=1)[r0:r1].contiguous()
+    kv = _ops.FusedKernelOperator(model.family_code, w.d, Xs32[r0:r1], Xs32, 1.0, 0.0, -1,
+                                  algo=args.algo)
+    op = FusedOperator(kv, model.noise, n)
+    total_steps = args.warmup + args.steps
+    run = MbcgRun(op, B, 1e-300, total_steps, precond, comm, row_offset=r0)
+    ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    run.kv_events = ev
+    for _ in range(args.warmup):
+        run.step()
+    torch.cuda.synchronize()
+    if comm:
+        dist.barrier()
+    kv_ms = []
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = lib.gp_launch_count()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        start.record()
+        for _ in range(args.steps):
+            run.step()  # ends with a stream sync on the status word
+            kv_ms.append(ev[0].elapsed_time(ev[1]))
+        end.record()
+        torch.cuda.synchronize()
+    launches = lib.gp_launch_count() - launches0
+    if comm:
+        dist.barrier()
+    ms = start.elapsed_time(end)
+    t = torch.tensor([ms, statistics.mean(kv_ms)], dtype=torch.float64, device="cuda")
+    if comm:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, kv_ms_max = float(t[0]), float(t[1])
+    iters_per_s = args.steps / (ms_max / 1000.0)
+
+    # fused K·V kernel: algorithmic flops per launch = rows x n x (2d + 2t)
+    flops_launch = (r1 - r0) * n * (2 * w.d + 2 * T_RHS)
+    kv_ms_mean = statistics.mean(kv_ms)
+    tflops = flops_launch / (kv_ms_mean / 1e3) / 1e12
+    entries_per_s = (r1 - r0) * n / (kv_ms_mean / 1e3)
+    mufu_per_entry = 2 if w.family == "matern32" else 1
+    sm_mhz_max = clk.summary().get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    sfu_peak_entries = 148 * 16 * sm_mhz_max * 1e6 / mufu_per_entry
+    job_tflops = n * n * (2 * w.d + 2 * T_RHS) / (kv_ms_max / 1e3) / 1e12
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_run(args, w, n, X, y, model, comm, r0, r1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cs = None
+        vals = []
+        for _ in range(3):
+            r = cpu_iteration_sample(X, ls, w.family, 0.1, w.rank, rows_target_s=4.0, state=cs)
+            cs = r["state"]
+            vals.append(r)
+        cpu = {"value": statistics.median([r["iters_per_s"] for r in vals[1:]]), "unit": UNIT,
+               "cores": vals[-1]["workers"], "kind": "port",
+               "sample": f"{vals[-1]['rows']} rows x {n} cols of K̂·V (+ full-n CG vector ops) "
+                         "per sample, oracle port on all host threads, extrapolated to n rows; "
+                         "median of 2 after 1 sizing run"}
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": iters_per_s, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f32 K·V (fp32 accumulate) / f64 CG state",
+            "data": "synthetic: seeded whitened U[0,1]^11 inputs, RFF target, probes ~ N(0, P)",
+            "config": {"workload": f"{w.name}: n={n} d={w.d} {w.family} ARD mBCG iteration, "
+                                   f"t={T_RHS} RHS, rank-{w.rank} pivoted-Cholesky preconditioner",
+                       "parallelism": f"row-shard x{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (per-step working set: L 800 MB + CG blocks "
+                             "+ X/P fp32 > 126 MB L2)"},
+            "kv_tflops": job_tflops,
+            "kv_ms_per_launch": kv_ms_max,
+            "roofline": {"bound": "tensor", "achieved": tflops, "peak": peaks["bf16_tflops"],
+                         "unit": "TFLOP/s", "frac": tflops / peaks["bf16_tflops"], "traffic": None,
+                         "peak_source": f"{peak_kind} bf16 dense (MEASURED_PEAKS.json)",
+                         "binding_unit": {
+                             "bound": "sfu", "achieved": entries_per_s / 1e9,
+                             "peak": sfu_peak_entries / 1e9, "unit": "Gentries/s",
+                             "frac": entries_per_s / sfu_peak_entries,
+                             "note": f"{mufu_per_entry} MUFU op(s)/entry, 148 SM x 16/clk at "
+                                     f"{sm_mhz_max} MHz"}},
+            "clocks": clocks,
+            "gpu_launches": int(launches),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if comm:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e_run(args, w, n, X, y, model, comm, r0, r1):
+    """Same metric through the public API with HOST inputs: X and [y | Z]
+    copied host->device and the solutions device->host inside the timed
+    region (pinned staging)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1903_08114_b200 import _device as D, _ops
+    from paper_1903_08114_b200.cg import FusedOperator, MbcgRun
+    from paper_1903_08114_b200.likelihood import build_kernel_preconditioner, draw_probes
+
+    precond = build_kernel_preconditioner(model, X, w.rank)
+    Bh = np.hstack([y[:, None], draw_probes(n, T_RHS - 1, 0, precond)])[r0:r1].copy()
+    Xh = X.copy()  # a fresh host array: nothing cached on the device
+    steps = args.steps
+    torch.cuda.synchronize()
+    if comm:
+        dist.barrier()
+    t0 = time.perf_counter()
+    ps = D.PointSet(Xh)
+    Xs32, _ = ps.scaled(model.lengthscales)
+    kv = _ops.FusedKernelOperator(model.family_code, w.d, Xs32[r0:r1], Xs32, 1.0, 0.0, -1,
+                                  algo=args.algo)
+    run = MbcgRun(FusedOperator(kv, model.noise, n), D.to_device(Bh), 1e-300, steps, precond,
+                  comm, row_offset=r0)
+    for _ in range(steps):
+        run.step()
+    U = D.to_host(run.U)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    if comm:
+        t = torch.tensor([el], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t[0])
+    return {"value": steps / el, "unit": UNIT,
+            "h2d_bytes_per_step": int((Xh.nbytes + Bh.nbytes) / steps),
+            "d2h_bytes_per_step": int(U.nbytes / steps),
+            "api": "PointSet upload + prescale + MbcgRun(FusedOperator) steps + solutions readback"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

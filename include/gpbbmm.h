@@ -1,0 +1,212 @@
+/*
+ * gpbbmm.h — C ABI of the B200-native exact-GP BBMM hot path.
+ *
+ * Drop-in boundary for the reference package blockgp 0.1.0
+ * (/root/reference/pkg/src/blockgp). The reference is pure Python, so it has
+ * no FFI of its own; each entry point below replaces one operator seam of the
+ * reference (cited file:line) and is bound from the Python host mirror
+ * (paper_1903_08114_b200/_lib.py) through ctypes. INTEGRATION.md shows the
+ * binding a blockgp maintainer would add.
+ *
+ * Conventions
+ *   - All pointers are DEVICE pointers unless the name ends in _host.
+ *   - Matrices are row-major with an explicit leading dimension (elements).
+ *   - `stream` is a cudaStream_t passed as void*; every call is stream-ordered
+ *     and asynchronous unless documented otherwise.
+ *   - The library allocates nothing that outlives a call: callers own every
+ *     buffer, including workspaces sized by the *_workspace_bytes queries.
+ *   - Every entry point returns a status (GP_OK = 0). gp_last_error() returns
+ *     a thread-local message for the last failure on the calling thread.
+ */
+#ifndef GPBBMM_H
+#define GPBBMM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mapped to ValueError / NumericError / ConvergenceError
+ *      by the host mirror; errors.py:4-15 of the reference) ---------------- */
+#define GP_OK 0
+#define GP_EINVAL 1      /* invalid argument            -> ValueError        */
+#define GP_ENONFINITE 2  /* non-finite kernel entry     -> NumericError      */
+#define GP_ENOTPD 3      /* p^T A p <= 0 / failed chol  -> NumericError      */
+#define GP_ECUDA 4       /* CUDA runtime failure        -> RuntimeError      */
+#define GP_EUNSUPPORTED 5 /* shape outside compiled kernels -> ValueError    */
+
+#define GP_FAMILY_RBF 0
+#define GP_FAMILY_MATERN32 1
+
+const char* gp_last_error(void);
+int gp_version(void);
+/* number of kernels this library has launched since it was loaded */
+uint64_t gp_launch_count(void);
+/* 1 if the tcgen05 (sm_100a tensor-core) K·V kernel is compiled in. */
+int gp_has_tcgen05(void);
+
+/* ---- point preparation -------------------------------------------------
+ * Xs = X / lengthscale (per column when n_ls == d, shared when n_ls == 1),
+ * written as fp32 (ld32 >= d, zero padded) and/or fp64 (ld64 >= d).
+ * Replaces the per-call rescaling of kernels.py:266 and :301-302.
+ * Either output may be NULL. norms32 (optional) = ||Xs_i||^2 in fp32. */
+int gp_prescale(const double* X, int64_t n, int d, int64_t ldx,
+                const double* lengthscales, int n_ls,
+                float* Xs32, int64_t ld32, double* Xs64, int64_t ld64,
+                float* norms32, void* stream);
+
+/* ---- fused on-the-fly kernel-matrix multiply ---------------------------
+ * out[i, :] = s2 * sum_j kappa(||xr_i - xc_j||^2) V[j, :]
+ *             (+ noise * V[i + diag_offset, :] when diag_offset >= 0)
+ * for i < n_rows, j < n_cols, t right-hand sides. The n_rows x n_cols kernel
+ * block is never materialised (tiles live in registers / SMEM / TMEM).
+ * Replaces kernels.training_mvm_oracle + partition.partitioned_mvm
+ * (kernels.py:293-316, partition.py:186-241) and, with diag_offset = -1,
+ * kernels.cross_mvm_oracle (kernels.py:319-325, predictor.py:130-131).
+ * Xr/Xc are prescaled fp32 points (gp_prescale). Per-row reduction order is
+ * fixed by n_cols alone, so results are bitwise independent of how rows are
+ * sharded across devices (test_partition.py:92-102).
+ * `algo`: 0 = auto, 1 = SIMT FFMA kernel, 2 = tcgen05 kernel. */
+typedef struct gp_kv_desc {
+  int32_t family;        /* GP_FAMILY_* */
+  int32_t d;             /* input dimension */
+  const float* Xr; int64_t ldr; int64_t n_rows;
+  const float* Xc; int64_t ldc; int64_t n_cols;
+  double outputscale;    /* s^2 */
+  double noise;          /* sigma^2 */
+  int64_t diag_offset;   /* global column of row 0 for the noise term, -1 = none */
+  int32_t algo;
+  int32_t reserved;
+} gp_kv_desc;
+
+size_t gp_kv_workspace_bytes(const gp_kv_desc* desc, int t);
+int gp_kv(const gp_kv_desc* desc, const float* V, int64_t ldv, int t,
+          float* out, int64_t ldo, void* workspace, size_t workspace_bytes,
+          void* stream);
+
+/* Dense fp64 kernel block (kernels.py:247-270 kernel_block, :293-308
+ * kernel_rows): out[i,j] = s2 kappa(xr_i, xc_j) (+ noise where
+ * j == i + diag_offset, diag_offset >= 0). Xr/Xc are prescaled fp64. */
+int gp_kernel_block(int family, int d, const double* Xr, int64_t ldr, int64_t n_rows,
+                    const double* Xc, int64_t ldc, int64_t n_cols, double outputscale,
+                    double noise, int64_t diag_offset, double* out, int64_t ldo,
+                    void* stream);
+
+/* Row-block product for arbitrary (materialised) row blocks — the path of
+ * partitioned_mvm with a user row oracle (partition.py:224-237):
+ * out = block @ V (fp64); *first_bad_row_dev receives the first row holding a
+ * non-finite entry, or n_rows if all are finite. */
+int gp_block_mvm(const double* block, int64_t n_rows, int64_t n_cols, int64_t ldb,
+                 const double* V, int64_t ldv, int t, double* out, int64_t ldo,
+                 int32_t* first_bad_row_dev, void* stream);
+
+/* ---- mBCG (cg.py:84-164) ------------------------------------------------
+ * Device-resident batched PCG. The host drives iterations phase by phase so
+ * a sharded (multi-GPU) caller can all-reduce the `red` payload between
+ * phases:  red = [pv : t | rn2 : t | LtR : k*t | gam : t]  (fp64).
+ * Per iteration:
+ *   gp_kv(P32 gathered)            Q32 = K P      (rows of this shard)
+ *   gp_mbcg_pv(Q)                  red.pv        -> all-reduce
+ *   gp_mbcg_update(Q, it)          alpha, U, R, red.rn2, red.LtR -> all-reduce
+ *   gp_mbcg_precond(it, tol)       rel, freeze, Z, red.gam        -> all-reduce
+ *   gp_mbcg_direction(it)          beta, P, P32
+ * status[0] = active columns after the freeze, status[1] = first column
+ * with p^T A p <= 0 or non-finite (INT32_MAX if none), status[2] = the
+ * iteration at which it happened. */
+typedef struct gp_mbcg {
+  int64_t n;             /* rows on this shard */
+  int32_t t;             /* right-hand sides */
+  int32_t k;             /* preconditioner rank (0 = none) */
+  int64_t ld;            /* leading dim of U, R, P, Z (>= t) */
+  int64_t ld32;          /* leading dim of P32 (>= t) */
+  double* U; double* R; double* P; double* Z;
+  float* P32;            /* fp32 copy of P: the K·V operand */
+  double noise;          /* operator K + noise I */
+  const double* L; int64_t ldl;   /* this shard's rows of the n x k factor */
+  const double* Binv;    /* k x k, (pc_noise I + L^T L)^{-1}, row-major */
+  double pc_noise;       /* preconditioner diagonal */
+  double* bnorm;         /* [t] */
+  double* gamma;         /* [t] */
+  double* red;           /* [3t + k t] reduction payload */
+  double* cbuf;          /* [k t] B^{-1} L^T R */
+  double* alpha_hist;    /* [max_iters t] */
+  double* beta_hist;     /* [max_iters t] */
+  double* rel;           /* [t] */
+  double* rel_hist;      /* [max_iters t] */
+  int32_t* active;       /* [t] */
+  int32_t* converged;    /* [t] */
+  int32_t* status;       /* [4] */
+  double* partials;      /* block partial sums */
+  int64_t partials_len;  /* doubles available in `partials` */
+  int32_t max_iters;
+  int32_t nblocks;       /* 0 = library default */
+} gp_mbcg;
+
+int64_t gp_mbcg_partials_len(int64_t n, int t, int k);
+/* init: R = B, U = 0, red.rn2 = ||B_j||^2, red.LtR = L^T B (local) */
+int gp_mbcg_init_a(gp_mbcg* s, const double* B, int64_t ldb, void* stream);
+/* after all-reduce of red: bnorm, Z = P^{-1} R, P = Z, P32, red.gam = r^T z */
+int gp_mbcg_init_b(gp_mbcg* s, void* stream);
+/* after all-reduce of red.gam: gamma = gam, active = 1 */
+int gp_mbcg_init_c(gp_mbcg* s, void* stream);
+/* Q = K P for this shard's rows: fp32 from gp_kv (q_is_f64 = 0; the
+ * noise * P term is added in fp64 inside the CG kernels) or an fp64 result of
+ * a user operator that already includes any diagonal (q_is_f64 = 1, and the
+ * state's `noise` should then be 0). */
+int gp_mbcg_pv(gp_mbcg* s, const void* Q, int64_t ldq, int q_is_f64, void* stream);
+int gp_mbcg_update(gp_mbcg* s, const void* Q, int64_t ldq, int q_is_f64, int iteration,
+                   void* stream);
+int gp_mbcg_precond(gp_mbcg* s, int iteration, double tolerance, void* stream);
+int gp_mbcg_direction(gp_mbcg* s, int iteration, void* stream);
+
+/* ---- column reductions / low-rank products (fp64) ----------------------- */
+/* out[j] = sum_i A[i,j] * B[i,j], deterministic fixed-order reduction */
+int gp_coldot(int64_t n, int t, const double* A, int64_t lda, const double* B,
+              int64_t ldb, double* out, double* partials, int64_t partials_len,
+              void* stream);
+/* out (k x t) = L^T V */
+int gp_lt_mul(int64_t n, int k, const double* L, int64_t ldl, const double* V,
+              int64_t ldv, int t, double* out, double* partials, int64_t partials_len,
+              void* stream);
+/* Y = beta * Y + alpha * L M,  L n x k, M k x t (row-major, ldm) */
+int gp_lowrank_mul(int64_t n, int k, const double* L, int64_t ldl, const double* M,
+                   int64_t ldm, int t, double alpha, double beta, double* Y,
+                   int64_t ldy, void* stream);
+
+/* ---- preconditioner (precond.py:58-174, likelihood.py:74-91) ------------
+ * Greedy rank-k pivoted Cholesky of the NOISELESS kernel matrix with
+ * constant diagonal s2: argmax pivot (lowest index on ties), early stop when
+ * the residual diagonal is <= 0, clamp at 0. fp64 throughout.
+ * Xs64 are prescaled fp64 points. Outputs: L (n x ldl), pivots_dev (k),
+ * resid_diag (n), info_dev[0] = achieved rank. */
+size_t gp_pivchol_workspace_bytes(int64_t n, int k);
+int gp_pivchol(int family, int d, const double* Xs64, int64_t ldx, int64_t n,
+               double outputscale, int k, double* L, int64_t ldl,
+               int64_t* pivots_dev, double* resid_diag, int32_t* info_dev,
+               void* workspace, size_t workspace_bytes, void* stream);
+/* B = noise I + L^T L; chol (lower) ; Binv = B^{-1}; logdet_tr_dev[0] =
+ * 2 sum log diag(chol), [1] = tr(B^{-1}); info_dev[0] != 0 on failure. */
+int gp_precond_factor(int64_t n, int k, const double* L, int64_t ldl, double noise,
+                      double* chol, double* Binv, double* logdet_tr_dev,
+                      int32_t* info_dev, double* partials, int64_t partials_len,
+                      void* stream);
+
+/* ---- gradient forms (likelihood.py:166-216, kernels.py:332-410) ---------
+ * For every geometric hyperparameter p returns sum_ij (dK/dtheta_p)_ij H_ij
+ * with H = Y R^T (Y, R: n x w fp32), using prescaled fp32 points:
+ *   out[0]     : p = outputscale   (dK/ds2 = kappa)
+ *   out[1]     : shared lengthscale, times l  (env * D)
+ *   out[1 + i] : ARD lengthscale i, times l_i (env * (xs_i - xs'_i)^2)
+ * env = s2 e^{-D/2} (RBF) or 3 s2 e^{-sqrt3 r} (Matern). fp64 output. */
+size_t gp_grad_forms_workspace_bytes(int64_t n_rows, int d, int ard);
+int gp_grad_forms(int family, int d, int ard, const float* Xr, int64_t ldr, int64_t n_rows,
+                  const float* Xc, int64_t ldc, int64_t n_cols, double outputscale,
+                  const float* Y, int64_t ldy, const float* R, int64_t ldrr, int w,
+                  double* out, void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPBBMM_H */

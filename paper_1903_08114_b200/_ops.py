@@ -1,0 +1,135 @@
+"""Thin tensor-level wrappers over the C-ABI (all work runs in libgpbbmm)."""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _device as D
+from . import _lib
+
+
+def _T():
+    return D.torch()
+
+
+def _st():
+    return _lib.stream_handle()
+
+
+class Workspace:
+    """Grow-only scratch buffers (caller-owned workspace for the C-ABI)."""
+
+    def __init__(self):
+        self._bufs = {}
+
+    def bytes(self, name: str, nbytes: int):
+        T = _T()
+        nbytes = max(int(nbytes), 8)
+        b = self._bufs.get(name)
+        if b is None or b.numel() < nbytes:
+            b = T.empty(nbytes, dtype=T.uint8, device=D.device())
+            self._bufs[name] = b
+        return b
+
+    def f64(self, name: str, count: int):
+        return self.bytes(name, 8 * max(int(count), 1)).view(_T().float64)
+
+
+_ws = Workspace()
+
+
+def workspace() -> Workspace:
+    return _ws
+
+
+class FusedKernelOperator:
+    """Rows [r0, r1) of s2*kappa(Xr, Xc) (+ noise I) applied on the fly by
+    gp_kv. Xr/Xc are prescaled fp32 point tensors (n x ld32)."""
+
+    def __init__(self, family_code: int, d: int, Xr32, Xc32, outputscale: float, noise: float,
+                 diag_offset: int, algo: int = 0):
+        self.desc = _lib.KvDesc(family=family_code, d=d, Xr=_lib.ptr(Xr32), ldr=Xr32.shape[1],
+                                n_rows=Xr32.shape[0], Xc=_lib.ptr(Xc32), ldc=Xc32.shape[1],
+                                n_cols=Xc32.shape[0], outputscale=float(outputscale),
+                                noise=float(noise), diag_offset=int(diag_offset), algo=int(algo))
+        self._keep = (Xr32, Xc32)
+        self.n_rows = Xr32.shape[0]
+        self.n_cols = Xc32.shape[0]
+
+    def apply32(self, V32, t: int, out32=None):
+        """out32[:, :t] = K V32[:, :t] (fp32 in, fp32 out)."""
+        T = _T()
+        if out32 is None:
+            out32 = T.empty((self.n_rows, t), dtype=T.float32, device=D.device())
+        L = _lib.lib()
+        nbytes = L.gp_kv_workspace_bytes(self.desc, t)
+        ws = _ws.bytes("kv", nbytes) if nbytes else None
+        _lib.check(L.gp_kv(self.desc, _lib.ptr(V32), V32.shape[1], t, _lib.ptr(out32),
+                           out32.shape[1], _lib.ptr(ws), int(nbytes), _st()), "gp_kv")
+        return out32
+
+
+def coldot(A, B):
+    """Per-column sum(A * B) of two (n, t) fp64 tensors -> (t,) fp64."""
+    T = _T()
+    n, t = A.shape
+    out = T.empty(t, dtype=T.float64, device=D.device())
+    part = _ws.f64("coldot", (2 * 148 + 8) * t + 1024)
+    _lib.check(_lib.lib().gp_coldot(n, t, _lib.ptr(A), A.stride(0), _lib.ptr(B), B.stride(0),
+                                    _lib.ptr(out), _lib.ptr(part), part.numel(), _st()), "gp_coldot")
+    return out
+
+
+def lt_mul(L, V):
+    """L^T V for L (n, k), V (n, t) fp64 -> (k, t)."""
+    T = _T()
+    n, k = L.shape
+    t = V.shape[1]
+    out = T.empty((k, t), dtype=T.float64, device=D.device())
+    part = _ws.f64("ltmul", (2 * 148 + 8) * k * t + 1024)
+    _lib.check(_lib.lib().gp_lt_mul(n, k, _lib.ptr(L), L.stride(0), _lib.ptr(V), V.stride(0), t,
+                                    _lib.ptr(out), _lib.ptr(part), part.numel(), _st()), "gp_lt_mul")
+    return out
+
+
+def lowrank_mul(L, M, Y=None, alpha=1.0, beta=0.0):
+    """Y = beta Y + alpha L M  (L (n,k), M (k,t))."""
+    T = _T()
+    n, k = L.shape
+    t = M.shape[1]
+    if Y is None:
+        Y = T.empty((n, t), dtype=T.float64, device=D.device())
+        beta = 0.0
+    M = M.contiguous()
+    _lib.check(_lib.lib().gp_lowrank_mul(n, k, _lib.ptr(L), L.stride(0), _lib.ptr(M), M.stride(0), t,
+                                         float(alpha), float(beta), _lib.ptr(Y), Y.stride(0), _st()),
+               "gp_lowrank_mul")
+    return Y
+
+
+def block_mvm(block, V):
+    """(block @ V, first non-finite row or None) for a materialised fp64 block."""
+    T = _T()
+    nr, nc = block.shape
+    t = V.shape[1]
+    out = T.empty((nr, t), dtype=T.float64, device=D.device())
+    bad = T.full((1,), nr, dtype=T.int32, device=D.device())
+    _lib.check(_lib.lib().gp_block_mvm(_lib.ptr(block), nr, nc, block.stride(0), _lib.ptr(V),
+                                       V.stride(0), t, _lib.ptr(out), t, _lib.ptr(bad), _st()),
+               "gp_block_mvm")
+    first = int(bad.item())
+    return out, (None if first >= nr else first)
+
+
+def first_nonfinite_row(A) -> int | None:
+    """Index of the first row of a device tensor holding a non-finite value."""
+    T = _T()
+    bad = ~T.isfinite(A)
+    if A.dim() > 1:
+        bad = bad.any(dim=1)
+    idx = T.nonzero(bad)
+    return int(idx[0, 0]) if idx.numel() else None
+
+
+def np_f64(x) -> np.ndarray:
+    return np.asarray(x, dtype=np.float64)

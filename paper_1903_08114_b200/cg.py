@@ -1,0 +1,362 @@
+"""Batched preconditioned CG with Lanczos coefficients (mirror of blockgp.cg).
+
+The solve runs device-resident through the gp_mbcg_* phases of the C-ABI
+(cg.py:84-164 semantics: per-column freeze on the recurrence residual
+||r||/||b||, alpha/beta recorded for active columns only). The host reads
+one small status word per iteration to decide termination; the alpha/beta
+history stays in HBM until the end. SLQ (cg.py:182-218) runs on the host on
+the t tiny tridiagonals, as in the reference.
+
+Operators (`mvm`):
+  * a fused kernel operator (likelihood/predictor build them): K·P on
+    gp_kv from the fp32 copy of P, noise*P added in fp64 by the CG kernels;
+  * any callable on (n, j) arrays (numpy in/out, or CUDA tensors in/out):
+    applied to the active columns, fp64 end to end.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.linalg
+
+from . import _device as D
+from . import _lib
+from . import _ops
+from .errors import NumericError
+from .precond import PreconditionerCache
+
+
+@dataclass
+class SolveRequest:
+    """rhs columns, relative-residual tolerance, iteration cap, optional
+    preconditioner (cg.py:27-49)."""
+
+    rhs: object
+    tolerance: float
+    max_iters: int = 1000
+    preconditioner: PreconditionerCache | None = None
+
+    def __post_init__(self):
+        if D.is_tensor(self.rhs):
+            r = self.rhs
+            if r.dim() == 1:
+                r = r[:, None]
+            if r.dim() != 2:
+                raise ValueError("rhs must be a vector or a matrix of columns")
+            self.rhs = r
+            norms = D.to_host(D.torch().linalg.norm(r.to(D.torch().float64), dim=0))
+        else:
+            r = np.asarray(self.rhs, dtype=np.float64)
+            if r.ndim == 1:
+                r = r[:, None]
+            if r.ndim != 2:
+                raise ValueError("rhs must be a vector or a matrix of columns")
+            self.rhs = r
+            norms = np.linalg.norm(r, axis=0)
+        if not self.tolerance > 0:
+            raise ValueError(f"tolerance must be positive, got {self.tolerance}")
+        if self.max_iters < 1:
+            raise ValueError(f"max_iters must be >= 1, got {self.max_iters}")
+        if np.any(norms == 0):
+            raise ValueError("every right-hand-side column must be non-zero")
+
+
+@dataclass(frozen=True)
+class Tridiagonal:
+    """Lanczos matrix of one column (cg.py:52-69)."""
+
+    diag: np.ndarray
+    offdiag: np.ndarray
+
+    @property
+    def order(self) -> int:
+        return self.diag.shape[0]
+
+    def dense(self) -> np.ndarray:
+        T = np.diag(self.diag)
+        if self.offdiag.size:
+            i = np.arange(self.offdiag.size)
+            T[i, i + 1] = self.offdiag
+            T[i + 1, i] = self.offdiag
+        return T
+
+
+@dataclass
+class SolveReport:
+    solutions: np.ndarray
+    final_relative_residuals: np.ndarray
+    iterations: int
+    tridiagonals: list
+    converged: np.ndarray
+    residual_history: np.ndarray = field(repr=False)
+    solutions_device: object = field(default=None, repr=False)
+
+
+class FusedOperator:
+    """K̂ = s2 kappa(X, X) + noise I applied by gp_kv on this device's rows.
+    `apply32(P32_full, t, out32)` computes the noiseless K·P; the CG kernels
+    add noise*P in fp64."""
+
+    fused = True
+
+    def __init__(self, kv_op: _ops.FusedKernelOperator, noise: float, n_total: int,
+                 gather=None):
+        self.kv = kv_op
+        self.noise = float(noise)
+        self.n_total = n_total
+        self.gather = gather  # distributed: all-gather of the local P32 rows
+
+    def __call__(self, V):  # reference-style use
+        T = D.torch()
+        Vd = D.to_device(V)
+        out = self.kv.apply32(Vd.to(T.float32).contiguous(), Vd.shape[1]).to(T.float64)
+        out += self.noise * Vd
+        return out if D.is_tensor(V) else D.to_host(out)
+
+
+def _tridiagonal(al, be) -> Tridiagonal:
+    """cg.py:167-179: diag_i = 1/a_i + b_{i-1}/a_{i-1}, off_i = sqrt(b_i)/a_i."""
+    m = len(al)
+    diag = np.empty(m)
+    off = np.empty(max(m - 1, 0))
+    for i in range(m):
+        diag[i] = 1.0 / al[i] + (be[i - 1] / al[i - 1] if i else 0.0)
+        if i < m - 1:
+            off[i] = math.sqrt(be[i]) / al[i]
+    return Tridiagonal(diag=diag, offdiag=off)
+
+
+class _Comm:
+    """No-op communicator (single device)."""
+
+    world = 1
+
+    def allreduce_(self, t):
+        return t
+
+    def allgather_rows(self, local, full):
+        full.copy_(local)
+        return full
+
+
+class DeviceSolve:
+    """Result of a device-resident solve (tensors stay in HBM)."""
+
+    def __init__(self, U, rel, iterations, alphas, betas, converged, history):
+        self.U = U
+        self.rel = rel
+        self.iterations = iterations
+        self.alphas = alphas
+        self.betas = betas
+        self.converged = converged
+        self.history = history
+
+    def tridiagonals(self):
+        return [_tridiagonal(a, b) for a, b in zip(self.alphas, self.betas)]
+
+
+class MbcgRun:
+    """Steppable device-resident mBCG (cg.py:84-164) on this device's rows.
+
+    `step()` runs one iteration (K·P, alpha/U/R update, freeze, Z, beta/P)
+    and returns the number of still-active columns; `finish()` folds the
+    device-side alpha/beta/residual history into a DeviceSolve. With a
+    multi-rank `comm`, the reduction payload is all-reduced between phases
+    and the fp32 search directions are all-gathered before each K·P."""
+
+    def __init__(self, mvm, B, tol: float, max_iters: int = 1000,
+                 precond: PreconditionerCache | None = None, comm=None, row_offset: int = 0):
+        T = D.torch()
+        self.T = T
+        self.comm = comm or _Comm()
+        self.lib = _lib.lib()
+        self.st = _lib.stream_handle()
+        dev = D.device()
+        B = B.to(T.float64).contiguous()
+        n, t = B.shape
+        self.n, self.t, self.tol, self.max_iters = n, t, float(tol), int(max_iters)
+        self.mvm = mvm
+        self.precond = precond
+        k = precond.rank if precond is not None else 0
+        self.k = k
+        ld32 = (t + 3) // 4 * 4
+        self.ld32 = ld32
+        f64 = dict(dtype=T.float64, device=dev)
+        self.U, self.R, self.P, self.Z = (T.empty((n, t), **f64) for _ in range(4))
+        rows32 = getattr(self.comm, "rows_per_rank", n) if self.comm.world > 1 else n
+        self.P32 = T.zeros((max(rows32, n), ld32), dtype=T.float32, device=dev)
+        self.red = T.zeros(3 * t + k * t, **f64)
+        self.cbuf = T.zeros(max(k * t, 1), **f64)
+        self.hist = T.zeros((3, max_iters, t), **f64)  # alpha, beta, rel
+        self.vec = T.zeros((3, t), **f64)  # bnorm, gamma, rel
+        self.ints = T.zeros(2 * t + 4, dtype=T.int32, device=dev)
+        plen = int(self.lib.gp_mbcg_partials_len(n, t, k))
+        self.partials = _ops.workspace().f64("mbcg_partials", plen)
+        L = precond.factor_device if precond is not None else None
+        if L is not None and L.shape[0] != n:
+            L = L[row_offset:row_offset + n]
+        self.L = L
+        self.fused = bool(getattr(mvm, "fused", False))
+        self.state = _lib.MbcgState(
+            n=n, t=t, k=k, ld=t, ld32=ld32, U=_lib.ptr(self.U), R=_lib.ptr(self.R),
+            P=_lib.ptr(self.P), Z=_lib.ptr(self.Z), P32=_lib.ptr(self.P32),
+            noise=float(mvm.noise) if self.fused else 0.0,
+            L=_lib.ptr(L) if k else 0, ldl=L.stride(0) if k else 0,
+            Binv=_lib.ptr(precond.binv_device) if k else 0,
+            pc_noise=float(precond.noise) if precond is not None else 0.0,
+            bnorm=_lib.ptr(self.vec[0]), gamma=_lib.ptr(self.vec[1]), red=_lib.ptr(self.red),
+            cbuf=_lib.ptr(self.cbuf), alpha_hist=_lib.ptr(self.hist[0]),
+            beta_hist=_lib.ptr(self.hist[1]), rel=_lib.ptr(self.vec[2]),
+            rel_hist=_lib.ptr(self.hist[2]), active=_lib.ptr(self.ints[:t]),
+            converged=_lib.ptr(self.ints[t:2 * t]), status=_lib.ptr(self.ints[2 * t:]),
+            partials=_lib.ptr(self.partials), partials_len=plen, max_iters=max_iters, nblocks=0)
+        self.sp = _lib.C.byref(self.state)
+        if self.fused:
+            self.Q = T.empty((n, t), dtype=T.float32, device=dev)
+            total = mvm.n_total if self.comm.world == 1 else rows32 * self.comm.world
+            self.P32_full = self.P32 if self.comm.world == 1 else \
+                T.zeros((total, ld32), dtype=T.float32, device=dev)
+        self.status_host = T.zeros(4, dtype=T.int32).pin_memory()
+        self.iterations = 0
+        self.kv_events = None  # optional (start, end) CUDA events around K·P
+        lib, sp, st = self.lib, self.sp, self.st
+        _lib.check(lib.gp_mbcg_init_a(sp, _lib.ptr(B), t, st), "gp_mbcg_init_a")
+        self._allreduce(t, 2 * t + k * t)
+        _lib.check(lib.gp_mbcg_init_b(sp, st), "gp_mbcg_init_b")
+        self._allreduce(2 * t + k * t, 3 * t + k * t)
+        _lib.check(lib.gp_mbcg_init_c(sp, st), "gp_mbcg_init_c")
+
+    def _allreduce(self, a, b):
+        if self.comm.world > 1 and b > a:
+            self.comm.allreduce_(self.red[a:b])
+
+    def step(self) -> int:
+        """One mBCG iteration; returns the active-column count after the freeze."""
+        it = self.iterations + 1
+        if it > self.max_iters:
+            raise RuntimeError("mBCG iteration cap exceeded")
+        lib, sp, st, t, k = self.lib, self.sp, self.st, self.t, self.k
+        if self.fused:
+            if self.comm.world > 1:
+                self.comm.allgather_rows(self.P32, self.P32_full)
+            if self.kv_events is not None:
+                self.kv_events[0].record()
+            self.mvm.kv.apply32(self.P32_full, t, self.Q)
+            if self.kv_events is not None:
+                self.kv_events[1].record()
+            qptr, qf64 = _lib.ptr(self.Q), 0
+        else:
+            Qd = _apply_user_operator(self.mvm, self.P, self.ints[:t])
+            qptr, qf64 = _lib.ptr(Qd), 1
+        _lib.check(lib.gp_mbcg_pv(sp, qptr, t, qf64, st), "gp_mbcg_pv")
+        self._allreduce(0, t)
+        _lib.check(lib.gp_mbcg_update(sp, qptr, t, qf64, it, st), "gp_mbcg_update")
+        self._allreduce(t, 2 * t + (k * t if self.precond is not None else 0))
+        _lib.check(lib.gp_mbcg_precond(sp, it, self.tol, st), "gp_mbcg_precond")
+        self._allreduce(2 * t + k * t, 3 * t + k * t)
+        self.iterations = it
+        self.status_host.copy_(self.ints[2 * t:], non_blocking=True)
+        self.T.cuda.current_stream().synchronize()
+        n_active, bad_col = int(self.status_host[0]), int(self.status_host[1])
+        if bad_col < t:
+            raise NumericError(f"operator is not positive definite: p^T A p <= 0 for column "
+                               f"{bad_col} at iteration {int(self.status_host[2])}")
+        if n_active:
+            _lib.check(lib.gp_mbcg_direction(sp, it, st), "gp_mbcg_direction")
+        return n_active
+
+    def run(self) -> "DeviceSolve":
+        while self.iterations < self.max_iters:
+            if self.step() == 0:
+                break
+        return self.finish()
+
+    def finish(self) -> "DeviceSolve":
+        t, its, tol = self.t, self.iterations, self.tol
+        H = D.to_host(self.hist[:, :its])
+        rel = D.to_host(self.vec[2])
+        conv = D.to_host(self.ints[t:2 * t]).astype(bool)
+        alphas, betas = [], []
+        for j in range(t):
+            hit = np.flatnonzero(H[2, :, j] <= tol)
+            m = int(hit[0]) + 1 if conv[j] and hit.size else its
+            alphas.append([float(x) for x in H[0, :m, j]])
+            betas.append([float(x) for x in H[1, :(m - 1 if conv[j] else its), j]])
+        return DeviceSolve(self.U, rel, its, alphas, betas, conv, H[2].copy())
+
+
+def mbcg_device(mvm, B, tol: float, max_iters: int = 1000,
+                precond: PreconditionerCache | None = None, comm=None,
+                row_offset: int = 0) -> DeviceSolve:
+    """Device-resident mBCG on this device's rows of B (n_local x t, fp64)."""
+    return MbcgRun(mvm, B, tol, max_iters, precond, comm, row_offset).run()
+
+
+def _apply_user_operator(mvm, P, active_dev):
+    """Apply a user callable to the active columns of P (fp64)."""
+    T = D.torch()
+    active = D.to_host(active_dev).astype(bool)
+    cols = np.flatnonzero(active)
+    Q = T.zeros_like(P)
+    if cols.size == 0:
+        return Q
+    idx = T.from_numpy(cols).to(P.device)
+    Pa = P.index_select(1, idx)
+    try:
+        res = mvm(Pa)
+    except TypeError:
+        res = None
+    if res is None or not D.is_tensor(res):
+        res = mvm(D.to_host(Pa)) if res is None else res
+        res = D.to_device(np.asarray(res, dtype=np.float64))
+    res = res.to(T.float64)
+    if res.dim() == 1:
+        res = res[:, None]
+    Q.index_copy_(1, idx, res)
+    return Q
+
+
+def mbcg_solve(mvm, request: SolveRequest) -> SolveReport:
+    """Run batched PCG until every column meets the tolerance or the cap
+    (cg.py:84-164)."""
+    B = D.to_device(request.rhs)
+    if B.dim() == 1:
+        B = B[:, None]
+    sol = mbcg_device(mvm, B, request.tolerance, request.max_iters, request.preconditioner)
+    U = sol.U
+    return SolveReport(solutions=D.to_host(U), final_relative_residuals=sol.rel,
+                       iterations=sol.iterations, tridiagonals=sol.tridiagonals(),
+                       converged=sol.converged,
+                       residual_history=sol.history if sol.iterations else np.zeros((0, U.shape[1])),
+                       solutions_device=U)
+
+
+def slq_logdet(report, preconditioner: PreconditionerCache | None = None, columns=None) -> float:
+    """n * mean_j sum_m (V_0m)^2 log(lambda_m) (+ logdet P) over probe
+    columns (cg.py:182-218; the weight is n, as in the reference code)."""
+    tris = report.tridiagonals if not isinstance(report, DeviceSolve) else report.tridiagonals()
+    cols = list(range(len(tris)) if columns is None else columns)
+    if not cols:
+        raise ValueError("at least one probe column is required")
+    n = (report.solutions.shape[0] if isinstance(report, SolveReport) else report.U.shape[0])
+    total = 0.0
+    for j in cols:
+        Tj = tris[j]
+        if Tj.order == 0:
+            raise NumericError(f"column {j} has an empty recurrence")
+        if Tj.order == 1:
+            lam, w = Tj.diag.copy(), np.ones(1)
+        else:
+            lam, vecs = scipy.linalg.eigh_tridiagonal(Tj.diag, Tj.offdiag)
+            w = vecs[0, :] ** 2
+        if np.any(lam <= 0):
+            raise NumericError(f"tridiagonal for column {j} has a non-positive eigenvalue; "
+                               "the operator is not positive definite or the recurrence broke down")
+        total += float(w @ np.log(lam))
+    est = n * total / len(cols)
+    if preconditioner is not None:
+        est += preconditioner.logdet
+    return est

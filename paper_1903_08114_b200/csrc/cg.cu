@@ -1,0 +1,704 @@
+// mBCG phases, deterministic column reductions, low-rank products, and the
+// preconditioner's inner factorisation.
+//
+// Reference semantics: cg.py:84-164 (mbcg_solve: per-column freeze on the
+// recurrence residual ||r||/||b||, alpha/beta recorded per active column),
+// precond.py:101-139 (Woodbury apply), :165-174 (tr P^{-1}).
+//
+// All reductions are fixed-order: every block reduces a contiguous row range
+// in a fixed thread order into partials[block][slot]; a finalize kernel sums
+// the blocks in index order. Results are therefore run-to-run deterministic.
+#include "gp_common.cuh"
+
+#include <algorithm>
+
+namespace gp {
+
+constexpr int kRT = 256;  // threads per row-block kernel
+
+__device__ __forceinline__ void row_range(int64_t n, int64_t& r0, int64_t& r1) {
+  int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  r0 = (int64_t)blockIdx.x * per;
+  r1 = min(n, r0 + per);
+}
+
+// Per-column sums over this block's rows of f(row, col); writes
+// out[c] for c < t. Thread layout: consecutive threads = consecutive columns
+// of a row (coalesced on row-major blocks).
+template <class F>
+__device__ void block_colsum(int64_t r0, int64_t r1, int t, F f, double* out, double* sred) {
+  for (int c0 = 0; c0 < t; c0 += kRT) {
+    int tw = min(kRT, t - c0);
+    int rpp = kRT / tw;
+    int tc = threadIdx.x % tw, tr = threadIdx.x / tw;
+    double acc = 0.0;
+    if (tr < rpp)
+      for (int64_t r = r0 + tr; r < r1; r += rpp) acc += f(r, c0 + tc);
+    sred[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x < tw) {
+      double s = 0.0;
+      for (int q = 0; q < rpp; ++q) s += sred[threadIdx.x + q * tw];
+      out[c0 + threadIdx.x] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// out[kk*t + c] (per block) = sum_{rows} L[r,kk] * A[r,c]
+__device__ void block_ltmul(int64_t r0, int64_t r1, int k, int t, const double* __restrict__ L,
+                            int64_t ldl, const double* __restrict__ A, int64_t lda, double* out,
+                            double* sL, double* sA, const int* colmask) {
+  constexpr int CR = 16, PPT = 8;
+  const int KT = k * t;
+  for (int p0 = 0; p0 < KT; p0 += kRT * PPT) {
+    double acc[PPT];
+#pragma unroll
+    for (int m = 0; m < PPT; ++m) acc[m] = 0.0;
+    for (int64_t rc = r0; rc < r1; rc += CR) {
+      int nr = (int)min((int64_t)CR, r1 - rc);
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < nr * k; idx += kRT) {
+        int r = idx / k, kk = idx - r * k;
+        sL[r * k + kk] = L[(rc + r) * ldl + kk];
+      }
+      for (int idx = threadIdx.x; idx < nr * t; idx += kRT) {
+        int r = idx / t, c = idx - r * t;
+        sA[r * t + c] = A[(rc + r) * lda + c];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int m = 0; m < PPT; ++m) {
+        int p = p0 + threadIdx.x + m * kRT;
+        if (p < KT) {
+          int kk = p / t, c = p - kk * t;
+          double s = acc[m];
+          for (int r = 0; r < nr; ++r) s = fma(sL[r * k + kk], sA[r * t + c], s);
+          acc[m] = s;
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < PPT; ++m) {
+      int p = p0 + threadIdx.x + m * kRT;
+      if (p < KT) out[p] = (colmask && !colmask[p % t]) ? 0.0 : acc[m];
+    }
+    __syncthreads();
+  }
+}
+
+// out[s] = sum_b partials[b*W + s] for s in [s0, s1), blocks in index order
+__global__ void finalize_partials(const double* __restrict__ partials, int nblocks, int W,
+                                  int s0, int s1, double* out) {
+  int s = s0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= s1) return;
+  double acc = 0.0;
+  for (int b = 0; b < nblocks; ++b) acc += partials[(int64_t)b * W + s];
+  out[s] = acc;
+}
+
+static int finalize(const double* partials, int nb, int W, int s0, int s1, double* out,
+                    cudaStream_t st) {
+  if (s1 <= s0) return GP_OK;
+  finalize_partials<<<(s1 - s0 + 255) / 256, 256, 0, st>>>(partials, nb, W, s0, s1, out);
+  GP_LAUNCH_CHECK();
+  return GP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// mBCG kernels
+// ---------------------------------------------------------------------------
+struct CgK {  // by-value kernel view of gp_mbcg
+  int64_t n; int t; int k; int64_t ld; int64_t ld32;
+  double* U; double* R; double* P; double* Z; float* P32;
+  double noise;
+  const double* L; int64_t ldl; const double* Binv; double pc_noise;
+  double* bnorm; double* gamma; double* red; double* cbuf;
+  double* alpha_hist; double* beta_hist; double* rel; double* rel_hist;
+  int* active; int* converged; int* status; double* partials;
+};
+
+static CgK view(const gp_mbcg* s) {
+  CgK v;
+  v.n = s->n; v.t = s->t; v.k = s->k; v.ld = s->ld; v.ld32 = s->ld32;
+  v.U = s->U; v.R = s->R; v.P = s->P; v.Z = s->Z; v.P32 = s->P32; v.noise = s->noise;
+  v.L = s->L; v.ldl = s->ldl; v.Binv = s->Binv; v.pc_noise = s->pc_noise;
+  v.bnorm = s->bnorm; v.gamma = s->gamma; v.red = s->red; v.cbuf = s->cbuf;
+  v.alpha_hist = s->alpha_hist; v.beta_hist = s->beta_hist; v.rel = s->rel;
+  v.rel_hist = s->rel_hist; v.active = s->active; v.converged = s->converged;
+  v.status = s->status; v.partials = s->partials;
+  return v;
+}
+
+// red layout offsets
+__host__ __device__ inline int off_pv(int) { return 0; }
+__host__ __device__ inline int off_rn2(int t) { return t; }
+__host__ __device__ inline int off_ltr(int t) { return 2 * t; }
+__host__ __device__ inline int off_gam(int t, int k) { return 2 * t + k * t; }
+
+// init_a: R = B, U = 0; partial rn2 = ||B_j||^2 and L^T B
+__global__ void __launch_bounds__(kRT) cg_init_a(CgK s, const double* __restrict__ B, int64_t ldb) {
+  extern __shared__ double dsm[];
+  double* sred = dsm;
+  double* sL = sred + kRT;
+  double* sA = sL + 16 * max(s.k, 1);
+  int64_t r0, r1;
+  row_range(s.n, r0, r1);
+  const int t = s.t;
+  const int W = 3 * t + s.k * t;
+  double* part = s.partials + (int64_t)blockIdx.x * W;
+  block_colsum(r0, r1, t, [&](int64_t r, int c) {
+    double b = B[r * ldb + c];
+    s.R[r * s.ld + c] = b;
+    s.U[r * s.ld + c] = 0.0;
+    return b * b;
+  }, part + t, sred);
+  if (s.k > 0) {
+    __syncthreads();
+    block_ltmul(r0, r1, s.k, t, s.L, s.ldl, s.R, s.ld, part + 2 * t, sL, sA, nullptr);
+  }
+}
+
+// c = B^{-1} (L^T R) for the given columns; single block
+__global__ void cg_cvec(CgK s, int use_active) {
+  const int t = s.t, k = s.k;
+  const double* ltr = s.red + off_ltr(t);
+  for (int p = threadIdx.x; p < k * t; p += blockDim.x) {
+    int kk = p / t, c = p - kk * t;
+    double acc = 0.0;
+    if (!use_active || s.active[c])
+      for (int l = 0; l < k; ++l) acc = fma(s.Binv[kk * k + l], ltr[l * t + c], acc);
+    s.cbuf[p] = acc;
+  }
+}
+
+// Z = P^{-1} R on (active) columns; partial gam = sum R o Z.
+// pc_noise <= 0: no preconditioner (Z = R, cg.py:360, :401);
+// k == 0: Z = R / pc_noise (precond.py:131-132).
+template <bool INIT>
+__global__ void __launch_bounds__(kRT) cg_precond_z(CgK s) {
+  extern __shared__ double dsm[];
+  double* sred = dsm;
+  double* sc = sred + kRT;  // k * t
+  const int t = s.t, k = s.k;
+  for (int p = threadIdx.x; p < k * t; p += kRT) sc[p] = s.cbuf[p];
+  __syncthreads();
+  int64_t r0, r1;
+  row_range(s.n, r0, r1);
+  const int W = 3 * t + k * t;
+  double* part = s.partials + (int64_t)blockIdx.x * W;
+  block_colsum(r0, r1, t, [&](int64_t r, int c) {
+    if (!INIT && !s.active[c]) return 0.0;
+    double rv = s.R[r * s.ld + c];
+    double z;
+    if (s.pc_noise <= 0.0) {
+      z = rv;
+    } else {
+      double lc = 0.0;
+      const double* lr = s.L + r * s.ldl;
+      for (int kk = 0; kk < k; ++kk) lc = fma(lr[kk], sc[kk * t + c], lc);
+      z = (rv - lc) / s.pc_noise;
+    }
+    s.Z[r * s.ld + c] = z;
+    if (INIT) {
+      s.P[r * s.ld + c] = z;
+      s.P32[r * s.ld32 + c] = (float)z;
+    }
+    return rv * z;
+  }, part + off_gam(t, k), sred);
+}
+
+__global__ void cg_init_c(CgK s) {
+  for (int c = threadIdx.x; c < s.t; c += blockDim.x) {
+    s.gamma[c] = s.red[off_gam(s.t, s.k) + c];
+    s.active[c] = 1;
+    s.converged[c] = 0;
+    s.rel[c] = 1.0;
+  }
+  if (threadIdx.x == 0) {
+    s.status[0] = s.t;
+    s.status[1] = 0x7fffffff;  // no non-PD column seen
+    s.status[2] = 0;
+  }
+}
+
+__global__ void cg_bnorm(CgK s) {
+  for (int c = threadIdx.x; c < s.t; c += blockDim.x) s.bnorm[c] = sqrt(s.red[off_rn2(s.t) + c]);
+}
+
+// pv partial = sum P o (Q + noise P) over active columns
+template <typename QT>
+__global__ void __launch_bounds__(kRT) cg_pv(CgK s, const QT* __restrict__ Q, int64_t ldq) {
+  __shared__ double sred[kRT];
+  int64_t r0, r1;
+  row_range(s.n, r0, r1);
+  const int t = s.t;
+  double* part = s.partials + (int64_t)blockIdx.x * (3 * t + s.k * t);
+  block_colsum(r0, r1, t, [&](int64_t r, int c) {
+    if (!s.active[c]) return 0.0;
+    double p = s.P[r * s.ld + c];
+    double q = (double)Q[r * ldq + c] + s.noise * p;
+    return p * q;
+  }, part, sred);
+}
+
+// alpha = gamma / pv on active columns + PD check (cg.py:120-128)
+__global__ void cg_alpha(CgK s, int it) {
+  for (int c = threadIdx.x; c < s.t; c += blockDim.x) {
+    double a = 0.0;
+    if (s.active[c]) {
+      double pv = s.red[off_pv(s.t) + c];
+      if (!(pv > 0.0) || !isfinite(pv)) {
+        atomicMin(&s.status[1], c);  // lowest offending column
+        s.status[2] = it;
+      }
+      a = s.gamma[c] / pv;
+    }
+    s.alpha_hist[(int64_t)(it - 1) * s.t + c] = a;
+  }
+}
+
+// U += alpha P; R -= alpha (Q + noise P); partial rn2; partial L^T R
+template <typename QT>
+__global__ void __launch_bounds__(kRT) cg_update(CgK s, const QT* __restrict__ Q, int64_t ldq, int it) {
+  extern __shared__ double dsm[];
+  double* sred = dsm;
+  double* sal = sred + kRT;               // t
+  double* sL = sal + s.t;
+  double* sA = sL + 16 * max(s.k, 1);
+  const int t = s.t, k = s.k;
+  for (int c = threadIdx.x; c < t; c += kRT)
+    sal[c] = s.active[c] ? s.alpha_hist[(int64_t)(it - 1) * t + c] : 0.0;
+  __syncthreads();
+  int64_t r0, r1;
+  row_range(s.n, r0, r1);
+  const int W = 3 * t + k * t;
+  double* part = s.partials + (int64_t)blockIdx.x * W;
+  block_colsum(r0, r1, t, [&](int64_t r, int c) {
+    double rv = s.R[r * s.ld + c];
+    if (s.active[c]) {
+      double a = sal[c];
+      double p = s.P[r * s.ld + c];
+      double q = (double)Q[r * ldq + c] + s.noise * p;
+      s.U[r * s.ld + c] += a * p;
+      rv -= a * q;
+      s.R[r * s.ld + c] = rv;
+    }
+    return rv * rv;
+  }, part + t, sred);
+  if (k > 0 && s.pc_noise > 0.0) {
+    __syncthreads();
+    block_ltmul(r0, r1, k, t, s.L, s.ldl, s.R, s.ld, part + 2 * t, sL, sA, s.active);
+  }
+}
+
+// rel, freeze (cg.py:133-143); c = B^{-1} L^T R for the columns kept
+__global__ void cg_freeze(CgK s, int it, double tol) {
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  for (int c = threadIdx.x; c < s.t; c += blockDim.x) {
+    if (s.active[c]) {
+      double rel = sqrt(s.red[off_rn2(s.t) + c]) / s.bnorm[c];
+      s.rel[c] = rel;
+      if (rel <= tol) {
+        s.converged[c] = 1;
+        s.active[c] = 0;
+      }
+    }
+    s.rel_hist[(int64_t)(it - 1) * s.t + c] = s.rel[c];
+    if (s.active[c]) atomicAdd(&cnt, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) s.status[0] = cnt;
+}
+
+// beta = gam / gamma on active columns (cg.py:145-152)
+__global__ void cg_beta(CgK s, int it) {
+  const double* gam = s.red + off_gam(s.t, s.k);
+  for (int c = threadIdx.x; c < s.t; c += blockDim.x) {
+    double b = 0.0;
+    if (s.active[c]) {
+      b = gam[c] / s.gamma[c];
+      s.gamma[c] = gam[c];
+    }
+    s.beta_hist[(int64_t)(it - 1) * s.t + c] = b;
+  }
+}
+
+__global__ void cg_direction(CgK s, int it) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t tot = s.n * s.t;
+  for (; idx < tot; idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = idx / s.t;
+    int c = (int)(idx - r * s.t);
+    if (!s.active[c]) continue;
+    double b = s.beta_hist[(int64_t)(it - 1) * s.t + c];
+    double p = s.Z[r * s.ld + c] + b * s.P[r * s.ld + c];
+    s.P[r * s.ld + c] = p;
+    s.P32[r * s.ld32 + c] = (float)p;
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// generic column reductions / low-rank products
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kRT) coldot_kernel(int64_t n, int t, const double* __restrict__ A,
+                                                     int64_t lda, const double* __restrict__ B,
+                                                     int64_t ldb, double* partials) {
+  __shared__ double sred[kRT];
+  int64_t r0, r1;
+  row_range(n, r0, r1);
+  block_colsum(r0, r1, t, [&](int64_t r, int c) { return A[r * lda + c] * B[r * ldb + c]; },
+               partials + (int64_t)blockIdx.x * t, sred);
+}
+
+__global__ void __launch_bounds__(kRT) ltmul_kernel(int64_t n, int k, const double* __restrict__ L,
+                                                    int64_t ldl, const double* __restrict__ V,
+                                                    int64_t ldv, int t, double* partials) {
+  extern __shared__ double dsm[];
+  int64_t r0, r1;
+  row_range(n, r0, r1);
+  block_ltmul(r0, r1, k, t, L, ldl, V, ldv, partials + (int64_t)blockIdx.x * k * t, dsm,
+              dsm + 16 * k, nullptr);
+}
+
+// Y = beta Y + alpha L M
+__global__ void lowrank_kernel(int64_t n, int k, const double* __restrict__ L, int64_t ldl,
+                               const double* __restrict__ M, int64_t ldm, int t, double alpha,
+                               double beta, double* Y, int64_t ldy) {
+  extern __shared__ double sM[];  // k x t
+  for (int p = threadIdx.x; p < k * t; p += blockDim.x) {
+    int kk = p / t, c = p - kk * t;
+    sM[p] = M[kk * ldm + c];
+  }
+  __syncthreads();
+  int64_t tot = n * t;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < tot;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = idx / t;
+    int c = (int)(idx - r * t);
+    const double* lr = L + r * ldl;
+    double acc = 0.0;
+    for (int kk = 0; kk < k; ++kk) acc = fma(lr[kk], sM[kk * t + c], acc);
+    double y = beta == 0.0 ? 0.0 : beta * Y[r * ldy + c];
+    Y[r * ldy + c] = y + alpha * acc;
+  }
+}
+
+// In-place Cholesky of B = noise I + G (G = L^T L, k x k, row-major, lower
+// result), then Binv = B^{-1} = C^{-T} C^{-1}; out[0] = 2 sum log C_jj,
+// out[1] = tr(B^{-1}) (precond.py:114-122, :165-174). Single block.
+__global__ void precond_factor_kernel(int k, double noise, double* C, double* Binv, double* out,
+                                      int* info) {
+  __shared__ int fail;
+  if (threadIdx.x == 0) fail = 0;
+  __syncthreads();
+  // shift the diagonal (only the lower triangle is read afterwards)
+  for (int p = threadIdx.x; p < k * k; p += blockDim.x) {
+    int i = p / k, j = p - i * k;
+    if (i == j) C[p] += noise;
+  }
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
+    if (threadIdx.x == 0) {
+      double djj = C[j * k + j];
+      if (!(djj > 0.0) || !isfinite(djj)) fail = 1;
+      C[j * k + j] = sqrt(fmax(djj, 0.0));
+    }
+    __syncthreads();
+    if (fail) break;
+    double cjj = C[j * k + j];
+    for (int i = j + 1 + threadIdx.x; i < k; i += blockDim.x) C[i * k + j] /= cjj;
+    __syncthreads();
+    int m = k - j - 1;
+    for (int p = threadIdx.x; p < m * m; p += blockDim.x) {
+      int i = j + 1 + p / m, l = j + 1 + p % m;
+      if (l <= i) C[i * k + l] -= C[i * k + j] * C[l * k + j];
+    }
+    __syncthreads();
+  }
+  if (fail) {
+    if (threadIdx.x == 0) info[0] = 1;
+    return;
+  }
+  for (int p = threadIdx.x; p < k * k; p += blockDim.x) {
+    int i = p / k, j = p - i * k;
+    if (j > i) C[p] = 0.0;
+  }
+  __syncthreads();
+  // X = C^{-1} (lower), column-parallel forward substitution into Binv scratch
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    for (int i = 0; i < k; ++i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int l = c; l < i; ++l) s -= C[i * k + l] * Binv[l * k + c];
+      Binv[i * k + c] = (i < c) ? 0.0 : s / C[i * k + i];
+    }
+  }
+  __syncthreads();
+  // tr(B^{-1}) = ||X||_F^2 ; logdet = 2 sum log C_jj
+  __shared__ double sred[1024];
+  double tr = 0.0, ld = 0.0;
+  for (int p = threadIdx.x; p < k * k; p += blockDim.x) tr += Binv[p] * Binv[p];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) ld += log(C[j * k + j]);
+  sred[threadIdx.x] = tr;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int q = 0; q < (int)blockDim.x; ++q) s += sred[q];
+    out[1] = s;
+  }
+  __syncthreads();
+  sred[threadIdx.x] = ld;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int q = 0; q < (int)blockDim.x; ++q) s += sred[q];
+    out[0] = 2.0 * s;
+    info[0] = 0;
+  }
+}
+
+// Binv = X^T X given X (lower) in Xs; separate kernel to avoid aliasing
+__global__ void xtx_kernel(int k, const double* __restrict__ X, double* out) {
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= k * k) return;
+  int i = p / k, j = p - i * k;
+  int l0 = max(i, j);
+  double s = 0.0;
+  for (int l = l0; l < k; ++l) s = fma(X[l * k + i], X[l * k + j], s);
+  out[p] = s;
+}
+
+static int cg_nblocks(const gp_mbcg* s) {
+  if (s->nblocks > 0) return s->nblocks;
+  int64_t nb = std::min<int64_t>(2 * num_sms(), (s->n + 63) / 64);
+  return (int)std::max<int64_t>(nb, 1);
+}
+
+static int check_state(const gp_mbcg* s) {
+  GP_REQUIRE(s && s->n >= 0 && s->t >= 1, "gp_mbcg: bad state");
+  GP_REQUIRE(s->ld >= s->t && s->ld32 >= s->t, "gp_mbcg: leading dimension < t");
+  GP_REQUIRE(s->k >= 0 && s->k <= 1024, "gp_mbcg: k=%d", s->k);
+  GP_REQUIRE(s->k == 0 || (s->L && s->Binv), "gp_mbcg: k>0 needs L and Binv");
+  int64_t need = (int64_t)cg_nblocks(s) * (3 * s->t + s->k * s->t);
+  GP_REQUIRE(s->partials_len >= need, "gp_mbcg: partials workspace %lld < %lld",
+             (long long)s->partials_len, (long long)need);
+  return GP_OK;
+}
+
+static size_t ltmul_smem(int k, int t) { return (size_t)(16 * std::max(k, 1) + 16 * t) * sizeof(double); }
+
+template <class K>
+static int set_smem(K kern, size_t bytes) {
+  if (bytes > 48 * 1024)
+    GP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  return GP_OK;
+}
+
+}  // namespace gp
+
+using namespace gp;
+
+extern "C" {
+
+int64_t gp_mbcg_partials_len(int64_t n, int t, int k) {
+  int64_t nb = std::min<int64_t>(2 * num_sms(), (n + 63) / 64);
+  nb = std::max<int64_t>(nb, 1);
+  return nb * (3 * (int64_t)t + (int64_t)k * t);
+}
+
+int gp_mbcg_init_a(gp_mbcg* s, const double* B, int64_t ldb, void* stream) {
+  if (int rc = check_state(s)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int t = s->t, k = s->k, W = 3 * t + k * t, nb = cg_nblocks(s);
+  if (s->n > 0) {
+    size_t smem = kRT * sizeof(double) + ltmul_smem(k, t);
+    if (int rc = set_smem(cg_init_a, smem)) return rc;
+    cg_init_a<<<nb, kRT, smem, st>>>(view(s), B, ldb);
+    GP_LAUNCH_CHECK();
+    return finalize(s->partials, nb, W, off_rn2(t), off_ltr(t) + (k > 0 ? k * t : 0), s->red, st);
+  }
+  GP_CUDA_TRY(cudaMemsetAsync(s->red + off_rn2(t), 0, sizeof(double) * (t + k * t), st));
+  return GP_OK;
+}
+
+int gp_mbcg_init_b(gp_mbcg* s, void* stream) {
+  if (int rc = check_state(s)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  CgK v = view(s);
+  const int t = s->t, k = s->k, W = 3 * t + k * t, nb = cg_nblocks(s);
+  cg_bnorm<<<1, 256, 0, st>>>(v);
+  GP_LAUNCH_CHECK();
+  if (k > 0 && s->pc_noise > 0.0) {
+    cg_cvec<<<1, 1024, 0, st>>>(v, 0);
+    GP_LAUNCH_CHECK();
+  }
+  if (s->n > 0) {
+    size_t smem = (kRT + (size_t)k * t) * sizeof(double);
+    if (int rc = set_smem(cg_precond_z<true>, smem)) return rc;
+    cg_precond_z<true><<<nb, kRT, smem, st>>>(v);
+    GP_LAUNCH_CHECK();
+    return finalize(s->partials, nb, W, off_gam(t, k), off_gam(t, k) + t, s->red, st);
+  }
+  GP_CUDA_TRY(cudaMemsetAsync(s->red + off_gam(t, k), 0, sizeof(double) * t, st));
+  return GP_OK;
+}
+
+int gp_mbcg_init_c(gp_mbcg* s, void* stream) {
+  if (int rc = check_state(s)) return rc;
+  cg_init_c<<<1, 256, 0, (cudaStream_t)stream>>>(view(s));
+  GP_LAUNCH_CHECK();
+  return GP_OK;
+}
+
+int gp_mbcg_pv(gp_mbcg* s, const void* Q, int64_t ldq, int q_is_f64, void* stream) {
+  if (int rc = check_state(s)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int t = s->t, k = s->k, W = 3 * t + k * t, nb = cg_nblocks(s);
+  if (s->n > 0) {
+    if (q_is_f64)
+      cg_pv<double><<<nb, kRT, 0, st>>>(view(s), static_cast<const double*>(Q), ldq);
+    else
+      cg_pv<float><<<nb, kRT, 0, st>>>(view(s), static_cast<const float*>(Q), ldq);
+    GP_LAUNCH_CHECK();
+    return finalize(s->partials, nb, W, off_pv(t), off_pv(t) + t, s->red, st);
+  }
+  GP_CUDA_TRY(cudaMemsetAsync(s->red, 0, sizeof(double) * t, st));
+  return GP_OK;
+}
+
+int gp_mbcg_update(gp_mbcg* s, const void* Q, int64_t ldq, int q_is_f64, int iteration,
+                   void* stream) {
+  if (int rc = check_state(s)) return rc;
+  GP_REQUIRE(iteration >= 1 && iteration <= s->max_iters, "gp_mbcg_update: iteration %d", iteration);
+  cudaStream_t st = (cudaStream_t)stream;
+  CgK v = view(s);
+  const int t = s->t, k = s->k, W = 3 * t + k * t, nb = cg_nblocks(s);
+  cg_alpha<<<1, 256, 0, st>>>(v, iteration);
+  GP_LAUNCH_CHECK();
+  if (s->n > 0) {
+    size_t smem = (kRT + t) * sizeof(double) + ltmul_smem(k, t);
+    if (q_is_f64) {
+      if (int rc = set_smem(cg_update<double>, smem)) return rc;
+      cg_update<double><<<nb, kRT, smem, st>>>(v, static_cast<const double*>(Q), ldq, iteration);
+    } else {
+      if (int rc = set_smem(cg_update<float>, smem)) return rc;
+      cg_update<float><<<nb, kRT, smem, st>>>(v, static_cast<const float*>(Q), ldq, iteration);
+    }
+    GP_LAUNCH_CHECK();
+    int s1 = (k > 0 && s->pc_noise > 0.0) ? off_ltr(t) + k * t : off_ltr(t);
+    return finalize(s->partials, nb, W, off_rn2(t), s1, s->red, st);
+  }
+  GP_CUDA_TRY(cudaMemsetAsync(s->red + off_rn2(t), 0, sizeof(double) * (t + k * t), st));
+  return GP_OK;
+}
+
+int gp_mbcg_precond(gp_mbcg* s, int iteration, double tolerance, void* stream) {
+  if (int rc = check_state(s)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  CgK v = view(s);
+  const int t = s->t, k = s->k, W = 3 * t + k * t, nb = cg_nblocks(s);
+  cg_freeze<<<1, 256, 0, st>>>(v, iteration, tolerance);
+  GP_LAUNCH_CHECK();
+  if (k > 0 && s->pc_noise > 0.0) {
+    cg_cvec<<<1, 1024, 0, st>>>(v, 1);
+    GP_LAUNCH_CHECK();
+  }
+  if (s->n > 0) {
+    size_t smem = (kRT + (size_t)k * t) * sizeof(double);
+    if (int rc = set_smem(cg_precond_z<false>, smem)) return rc;
+    cg_precond_z<false><<<nb, kRT, smem, st>>>(v);
+    GP_LAUNCH_CHECK();
+    return finalize(s->partials, nb, W, off_gam(t, k), off_gam(t, k) + t, s->red, st);
+  }
+  GP_CUDA_TRY(cudaMemsetAsync(s->red + off_gam(t, k), 0, sizeof(double) * t, st));
+  return GP_OK;
+}
+
+int gp_mbcg_direction(gp_mbcg* s, int iteration, void* stream) {
+  if (int rc = check_state(s)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  CgK v = view(s);
+  cg_beta<<<1, 256, 0, st>>>(v, iteration);
+  GP_LAUNCH_CHECK();
+  if (s->n > 0) {
+    int64_t tot = s->n * s->t;
+    int nb = (int)std::min<int64_t>((tot + 255) / 256, 8LL * num_sms());
+    cg_direction<<<nb, 256, 0, st>>>(v, iteration);
+    GP_LAUNCH_CHECK();
+  }
+  return GP_OK;
+}
+
+
+static int nb_rows(int64_t n) {
+  int64_t nb = std::min<int64_t>(2 * num_sms(), (n + 63) / 64);
+  return (int)std::max<int64_t>(nb, 1);
+}
+
+int gp_coldot(int64_t n, int t, const double* A, int64_t lda, const double* B, int64_t ldb,
+              double* out, double* partials, int64_t partials_len, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  GP_REQUIRE(t >= 1, "gp_coldot: t=%d", t);
+  if (n == 0) {
+    GP_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double) * t, st));
+    return GP_OK;
+  }
+  int nb = nb_rows(n);
+  GP_REQUIRE(partials_len >= (int64_t)nb * t, "gp_coldot: partials %lld < %lld",
+             (long long)partials_len, (long long)nb * t);
+  coldot_kernel<<<nb, kRT, 0, st>>>(n, t, A, lda, B, ldb, partials);
+  GP_LAUNCH_CHECK();
+  return finalize(partials, nb, t, 0, t, out, st);
+}
+
+int gp_lt_mul(int64_t n, int k, const double* L, int64_t ldl, const double* V, int64_t ldv, int t,
+              double* out, double* partials, int64_t partials_len, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  GP_REQUIRE(t >= 1 && k >= 1, "gp_lt_mul: k=%d t=%d", k, t);
+  if (n == 0) {
+    GP_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double) * k * t, st));
+    return GP_OK;
+  }
+  int nb = nb_rows(n);
+  GP_REQUIRE(partials_len >= (int64_t)nb * k * t, "gp_lt_mul: partials too small");
+  size_t smem = ltmul_smem(k, t);
+  if (int rc = set_smem(ltmul_kernel, smem)) return rc;
+  ltmul_kernel<<<nb, kRT, smem, st>>>(n, k, L, ldl, V, ldv, t, partials);
+  GP_LAUNCH_CHECK();
+  return finalize(partials, nb, k * t, 0, k * t, out, st);
+}
+
+int gp_lowrank_mul(int64_t n, int k, const double* L, int64_t ldl, const double* M, int64_t ldm,
+                   int t, double alpha, double beta, double* Y, int64_t ldy, void* stream) {
+  GP_REQUIRE(t >= 1 && k >= 0, "gp_lowrank_mul: k=%d t=%d", k, t);
+  if (n == 0) return GP_OK;
+  size_t smem = (size_t)k * t * sizeof(double);
+  if (int rc = set_smem(lowrank_kernel, smem)) return rc;
+  int64_t tot = n * t;
+  int nb = (int)std::min<int64_t>((tot + 255) / 256, 8LL * num_sms());
+  lowrank_kernel<<<nb, 256, smem, (cudaStream_t)stream>>>(n, k, L, ldl, M, ldm, t, alpha, beta, Y, ldy);
+  GP_LAUNCH_CHECK();
+  return GP_OK;
+}
+
+int gp_precond_factor(int64_t n, int k, const double* L, int64_t ldl, double noise, double* chol,
+                      double* Binv, double* logdet_tr_dev, int32_t* info_dev, double* partials,
+                      int64_t partials_len, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  GP_REQUIRE(k >= 1 && noise > 0.0, "gp_precond_factor: k=%d noise=%g", k, noise);
+  // chol <- L^T L
+  if (int rc = gp_lt_mul(n, k, L, ldl, L, ldl, k, chol, partials, partials_len, stream)) return rc;
+  precond_factor_kernel<<<1, 1024, 0, st>>>(k, noise, chol, Binv, logdet_tr_dev, info_dev);
+  GP_LAUNCH_CHECK();
+  // Binv currently holds X = C^{-1}; form X^T X into partials then copy
+  GP_REQUIRE(partials_len >= (int64_t)k * k, "gp_precond_factor: partials too small");
+  xtx_kernel<<<(k * k + 255) / 256, 256, 0, st>>>(k, Binv, partials);
+  GP_LAUNCH_CHECK();
+  GP_CUDA_TRY(cudaMemcpyAsync(Binv, partials, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, st));
+  return GP_OK;
+}
+
+}  // extern "C"

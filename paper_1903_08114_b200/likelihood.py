@@ -1,0 +1,213 @@
+"""Exact-GP log marginal likelihood and gradients (mirror of blockgp.likelihood).
+
+One device-resident mBCG solve over [y - mu | Z] (probes Z drawn with
+covariance P from the host generator, bit-identical to the reference),
+SLQ on the probe columns for logdet, and ONE fused gradient pass
+(gp_grad_forms) for every geometric hyperparameter:
+
+    g_p = sum_ij (dK/dtheta_p)_ij (Y R^T)_ij - tr(dK/dtheta_p) / (2 noise)
+    Y = [a/2 | -(S-W)/(2t) | L B^{-1}/(2 noise)],   R = [a | W | L]
+
+which is algebraically identical to the reference's per-parameter products
+(likelihood.py:166-216; identity derived in SURVEY §7.3(6)).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _device as D
+from . import _lib
+from . import _ops
+from . import precond as _pc
+from .cg import FusedOperator, mbcg_device, slq_logdet
+from .errors import NumericError
+from .kernels import KernelModel, param_ids
+from .partition import PartitionPlan, WorkerPool
+
+LOG_TWO_PI = math.log(2.0 * math.pi)
+
+
+@dataclass
+class CgConfig:
+    """Training-protocol solver settings (likelihood.py:38-54)."""
+
+    tolerance: float = 1.0
+    max_iters: int = 1000
+    probes: int = 10
+    precond_rank: int = 100
+
+    def __post_init__(self):
+        if self.probes < 1:
+            raise ValueError("at least one probe vector is required")
+
+
+@dataclass
+class MLLDiagnostics:
+    probe_seed: int
+    iterations: int
+    final_residuals: np.ndarray
+    converged: bool
+    logdet_estimate: float
+    quad_term: float
+    precond_rank: int
+
+
+@dataclass
+class MLLResult:
+    value: float
+    gradients: dict
+    diagnostics: MLLDiagnostics = field(repr=False)
+
+
+def build_kernel_preconditioner(model: KernelModel, X, rank: int):
+    """Rank-min(rank, n) pivoted-Cholesky preconditioner of the noiseless
+    kernel (likelihood.py:74-91); None when rank <= 0."""
+    if rank <= 0:
+        return None
+    src = _pc.KernelRowSource(model, X)
+    n = src.points.n
+    k = min(rank, n)
+    factor = _pc.partial_pivoted_cholesky(src, np.full(n, model.outputscale), k)
+    return _pc.build_preconditioner(factor, model.noise)
+
+
+def draw_probes_device(n: int, t: int, seed: int, cache):
+    rng = np.random.default_rng(seed)
+    if cache is None:
+        return D.to_device(rng.standard_normal((n, t)))
+    return _pc.precond_sample_device(cache, rng, t)
+
+
+def draw_probes(n: int, t: int, seed: int, cache) -> np.ndarray:
+    """Seeded probes: N(0, I) or N(0, P) (likelihood.py:94-101)."""
+    return D.to_host(draw_probes_device(n, t, seed, cache))
+
+
+def training_operator(model: KernelModel, ps, algo: int = 0) -> FusedOperator:
+    Xs32, _ = ps.scaled(model.scale_for(ps.d))
+    kv = _ops.FusedKernelOperator(model.family_code, ps.d, Xs32, Xs32, model.outputscale, 0.0,
+                                  -1, algo=algo)
+    return FusedOperator(kv, model.noise, ps.n)
+
+
+def mll_value_and_grad(model: KernelModel, X, y, plan: PartitionPlan, pool: WorkerPool,
+                       cg_config: CgConfig, probe_seed: int) -> MLLResult:
+    """log p(y) and d/dtheta for every trainable hyperparameter
+    (likelihood.py:104-163), computed on the GPU."""
+    T = D.torch()
+    ps = D.points(X)
+    n = ps.n
+    yd = D.to_device(y)
+    if tuple(yd.shape) != (n,):
+        raise ValueError(f"y has shape {tuple(yd.shape)}, expected ({n},)")
+    if plan.n != n:
+        raise ValueError("partition plan does not match the training size")
+    model.scale_for(ps.d)
+    t = cg_config.probes
+    yc = yd - model.mean
+    cache = build_kernel_preconditioner(model, ps, cg_config.precond_rank)
+    Z = draw_probes_device(n, t, probe_seed, cache)
+    op = training_operator(model, ps)
+    B = T.cat([yc[:, None], Z], dim=1).contiguous()
+    sol = mbcg_device(op, B, cg_config.tolerance, cg_config.max_iters, cache)
+    a = sol.U[:, 0].contiguous()
+    S = sol.U[:, 1:].contiguous()
+    logdet = slq_logdet(sol, cache, columns=range(1, t + 1))
+    quad = float(_ops.coldot(yc[:, None], a[:, None])[0].item())
+    value = -0.5 * quad - 0.5 * logdet - 0.5 * n * LOG_TWO_PI
+    W = _pc.precond_apply_device(cache, Z) if cache is not None else Z
+    gradients = _gradients(model, ps, a, S, W, cache)
+    gradients["mean"] = float(a.sum().item())
+    if not np.isfinite(value) or any(not np.isfinite(g) for g in gradients.values()):
+        raise NumericError("non-finite likelihood value or gradient")
+    diag = MLLDiagnostics(probe_seed=probe_seed, iterations=sol.iterations,
+                          final_residuals=sol.rel, converged=bool(sol.converged.all()),
+                          logdet_estimate=logdet, quad_term=quad,
+                          precond_rank=cache.rank if cache is not None else 0)
+    return MLLResult(value=value, gradients=gradients, diagnostics=diag)
+
+
+def gradient_operands(a, S, W, cache):
+    """fp32 (Y, R) of the fused gradient pass, plus the constant
+    tr(dK/ds2)/(2 noise) to subtract from the outputscale form."""
+    T = D.torch()
+    t = W.shape[1]
+    if cache is not None:
+        Yc = [0.5 * a[:, None], -(S - W) / (2.0 * t)]
+        Rc = [a[:, None], W]
+        if cache.rank:
+            LB = _ops.lowrank_mul(cache.factor_device, cache.binv_device)
+            Yc.append(LB / (2.0 * cache.noise))
+            Rc.append(cache.factor_device)
+    else:
+        Yc = [0.5 * a[:, None], -S / (2.0 * t)]
+        Rc = [a[:, None], W]
+    Y = T.cat(Yc, dim=1).to(T.float32).contiguous()
+    R = T.cat(Rc, dim=1).to(T.float32).contiguous()
+    return Y, R
+
+
+def _gradients(model: KernelModel, ps, a, S, W, cache) -> dict:
+    n, t = W.shape
+    Xs32, _ = ps.scaled(model.scale_for(ps.d))
+    Y, R = gradient_operands(a, S, W, cache)
+    raw = _grad_forms_raw(model, ps.d, Xs32, Xs32, Y, R)
+    return assemble_gradients(model, raw, a, S, W, cache, n)
+
+
+def _grad_forms_raw(model, d, Xr32, Xc32, Y, R):
+    T = D.torch()
+    ard = 1 if model.ard else 0
+    npar = 1 + (d if ard else 1)
+    out = T.zeros(npar, dtype=T.float64, device=D.device())
+    lib = _lib.lib()
+    nbytes = lib.gp_grad_forms_workspace_bytes(Xr32.shape[0], d, ard)
+    ws = _ops.workspace().bytes("grad", nbytes)
+    _lib.check(lib.gp_grad_forms(model.family_code, d, ard, _lib.ptr(Xr32), Xr32.stride(0),
+                                 Xr32.shape[0], _lib.ptr(Xc32), Xc32.stride(0), Xc32.shape[0],
+                                 float(model.outputscale), _lib.ptr(Y), Y.stride(0), _lib.ptr(R),
+                                 R.stride(0), Y.shape[1], _lib.ptr(out), _lib.ptr(ws), nbytes,
+                                 _lib.stream_handle()), "gp_grad_forms")
+    return out
+
+
+def assemble_gradients(model, raw_dev, a, S, W, cache, n_total: int, reduce=None) -> dict:
+    """Constant factors + noise gradient (likelihood.py:192-216). `reduce`
+    all-reduces device scalars when rows are sharded."""
+    T = D.torch()
+    t = W.shape[1]
+    # device scalars: [a.a, sum (S-W) o W  (or S o W)]
+    if cache is not None:
+        sw = _ops.coldot((S - W).contiguous(), W).sum()
+    else:
+        sw = _ops.coldot(S, W).sum()
+    aa = _ops.coldot(a[:, None], a[:, None])[0]
+    vec = T.cat([raw_dev, aa[None], sw[None]])
+    if reduce is not None:
+        vec = reduce(vec)
+    v = D.to_host(vec)
+    raw, aa, sw = v[:-2], float(v[-2]), float(v[-1])
+    s2 = model.outputscale
+    g = {}
+    const = 0.5 * n_total / cache.noise if cache is not None else 0.0
+    g["outputscale"] = float(raw[0]) - const
+    if model.ard:
+        for i, l in enumerate(model.lengthscales):
+            g[f"lengthscale_{i}"] = s2 * float(raw[1 + i]) / float(l)
+    else:
+        g["lengthscale"] = s2 * float(raw[1]) / float(model.lengthscales[0])
+    if cache is not None:
+        tr_noise = _pc.precond_inverse_quadratic_trace(cache) if n_total == cache.n else \
+            (n_total - (cache.rank - cache.noise * cache.tr_binv)) / cache.noise
+        g["noise"] = 0.5 * aa - 0.5 * (tr_noise + sw / t)
+    else:
+        g["noise"] = 0.5 * aa - 0.5 * sw / t
+    ordered = {}
+    for pid in param_ids(model):
+        if pid in g:
+            ordered[pid] = g[pid]
+    return ordered
