@@ -236,7 +236,7 @@ def run_ours(args):
     Z = draw_probes_device(n, T_RHS - 1, 0, precond)
     B = torch.cat([D.to_device(y)[:, None], Z], dim=1)[r0:r1].contiguous()
     kv = _ops.FusedKernelOperator(model.family_code, w.d, Xs32[r0:r1], Xs32, 1.0, 0.0, -1,
-                                  algo=args.algo)
+                                  algo=args.algo, self_offset=r0)
     op = FusedOperator(kv, model.noise, n)
     total_steps = args.warmup + args.steps
     run = MbcgRun(op, B, 1e-300, total_steps, precond, comm, row_offset=r0)
@@ -352,7 +352,7 @@ def e2e_run(args, w, n, X, y, model, comm, r0, r1):
     ps = D.PointSet(Xh)
     Xs32, _ = ps.scaled(model.lengthscales)
     kv = _ops.FusedKernelOperator(model.family_code, w.d, Xs32[r0:r1], Xs32, 1.0, 0.0, -1,
-                                  algo=args.algo)
+                                  algo=args.algo, self_offset=r0)
     run = MbcgRun(FusedOperator(kv, model.noise, n), D.to_device(Bh), 1e-300, steps, precond,
                   comm, row_offset=r0)
     for _ in range(steps):

@@ -79,6 +79,9 @@ typedef struct gp_kv_desc {
   int64_t diag_offset;   /* global column of row 0 for the noise term, -1 = none */
   int32_t algo;
   int32_t reserved;
+  int64_t self_offset;   /* row i of Xr IS column i + self_offset of Xc (-1 = unrelated):
+                            that entry is evaluated at r2 = 0 exactly, as the
+                            reference's clamp does (kernels.py:216-222) */
 } gp_kv_desc;
 
 size_t gp_kv_workspace_bytes(const gp_kv_desc* desc, int t);

@@ -27,7 +27,7 @@ class KvDesc(C.Structure):
                 ("Xr", c_p), ("ldr", c_i64), ("n_rows", c_i64),
                 ("Xc", c_p), ("ldc", c_i64), ("n_cols", c_i64),
                 ("outputscale", c_f64), ("noise", c_f64), ("diag_offset", c_i64),
-                ("algo", c_i32), ("reserved", c_i32)]
+                ("algo", c_i32), ("reserved", c_i32), ("self_offset", c_i64)]
 
 
 class MbcgState(C.Structure):

@@ -47,11 +47,16 @@ class FusedKernelOperator:
     gp_kv. Xr/Xc are prescaled fp32 point tensors (n x ld32)."""
 
     def __init__(self, family_code: int, d: int, Xr32, Xc32, outputscale: float, noise: float,
-                 diag_offset: int, algo: int = 0):
-        self.desc = _lib.KvDesc(family=family_code, d=d, Xr=_lib.ptr(Xr32), ldr=Xr32.shape[1],
-                                n_rows=Xr32.shape[0], Xc=_lib.ptr(Xc32), ldc=Xc32.shape[1],
+                 diag_offset: int, algo: int = 0, self_offset: int | None = None):
+        """self_offset: row i of Xr is column i + self_offset of Xc (training
+        operator rows); defaults to diag_offset."""
+        if self_offset is None:
+            self_offset = diag_offset
+        self.desc = _lib.KvDesc(family=family_code, d=d, Xr=_lib.ptr(Xr32), ldr=Xr32.stride(0),
+                                n_rows=Xr32.shape[0], Xc=_lib.ptr(Xc32), ldc=Xc32.stride(0),
                                 n_cols=Xc32.shape[0], outputscale=float(outputscale),
-                                noise=float(noise), diag_offset=int(diag_offset), algo=int(algo))
+                                noise=float(noise), diag_offset=int(diag_offset), algo=int(algo),
+                                self_offset=int(self_offset))
         self._keep = (Xr32, Xc32)
         self.n_rows = Xr32.shape[0]
         self.n_cols = Xc32.shape[0]

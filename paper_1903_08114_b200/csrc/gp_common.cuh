@@ -82,4 +82,9 @@ inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 int num_sms();
 
+// out[row, c] = s2 * sum_s ws[s, row, c] (+ noise V[row + diag_offset, c])
+int launch_split_reduce(const float* ws, int S, int64_t stride, int64_t nr, int t, float* out,
+                        int64_t ldo, float s2, float noise, const float* V, int64_t ldv,
+                        int64_t diag_offset, cudaStream_t st);
+
 }  // namespace gp

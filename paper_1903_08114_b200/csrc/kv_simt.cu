@@ -216,6 +216,16 @@ __global__ void kv_split_reduce(const float* __restrict__ ws, int S, int64_t str
   out[row * ldo + col] = r;
 }
 
+int launch_split_reduce(const float* ws, int S, int64_t stride, int64_t nr, int t, float* out,
+                        int64_t ldo, float s2, float noise, const float* V, int64_t ldv,
+                        int64_t diag_offset, cudaStream_t st) {
+  int64_t tot = nr * (int64_t)t;
+  kv_split_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(ws, S, stride, nr, t, out, ldo, s2,
+                                                                 noise, V, ldv, diag_offset);
+  GP_LAUNCH_CHECK();
+  return GP_OK;
+}
+
 // number of column splits: a function of the COLUMN count only (so the per
 // row summation order does not depend on how rows are sharded) unless the
 // caller is a cross block where determinism across shards is moot.

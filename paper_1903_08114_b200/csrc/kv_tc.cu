@@ -1,13 +1,669 @@
-// tcgen05 (5th-gen tensor core) fused K·V kernel for sm_100a — see DESIGN.md.
-// Placeholder until the tensor-core path lands: reports "not compiled".
+// tcgen05 (5th-generation tensor core) fused K·V kernel for sm_100a.
+//
+// out[i, :] = s2 * sum_j kappa(r2_ij) V[j, :]  for 128-row tiles, streaming
+// 64-column tiles; the n x n kernel matrix never leaves TMEM.
+//
+// Per column tile j of a row tile (one CTA per SM, persistent over items):
+//   1. TMA warp   : cp.async.bulk the pre-tiled column image (X_c hi/lo, with
+//                   the squared norm folded in as an extra K column) and the
+//                   V image (hi/lo) into a 4-stage SMEM ring.
+//   2. MMA thread : S = A . B^T on tcgen05 (kind::tf32, M=128, N=64), where
+//                   a_i = [c x_i, -c|x_i|^2/2, -c/2], b_j = [x_j, 1, |x_j|^2]
+//                   so S = -(c/2) r2 exactly in the expansion of
+//                   kernels.py:216-222; 3xTF32 (hi.hi + hi.lo + lo.hi) keeps
+//                   fp32 accuracy. S lands in TMEM (double buffered).
+//   3. 8 epilogue warps: tcgen05.ld S, kappa on the SFU (RBF: 1 ex2;
+//                   Matern: sqrt + ex2), split K = K_hi + K_lo (tf32), and
+//                   tcgen05.st both back into TMEM as the A operand.
+//   4. MMA thread : O += K_hi.V_hi + K_hi.V_lo + K_lo.V_hi (A from TMEM,
+//                   M=128, N=16, K=64) into a TMEM accumulator that is
+//                   flushed to fp32 registers every 64 tiles (4096 columns).
+// Reference semantics: kernels.py:225-244 (kappa), :293-316 (rows of K̂),
+// partition.py:224-241 (row-block product). Per-row column order is fixed by
+// the column count, so row sharding across GPUs is bitwise neutral.
 #include "gp_common.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace gp {
-bool kv_tc_supported(const gp_kv_desc*, int) { return false; }
-size_t kv_tc_workspace(const gp_kv_desc*, int) { return 0; }
-int kv_tc(const gp_kv_desc*, const float*, int64_t, int, float*, int64_t, void*, size_t, cudaStream_t) {
-  return set_error(GP_EUNSUPPORTED, "tcgen05 K·V kernel not compiled in");
+namespace tc {
+
+constexpr int BM = 128;   // rows per tile (UMMA M)
+constexpr int BN = 64;    // columns per tile (distance N, contraction K)
+constexpr int TN = 16;    // right-hand sides (contraction N)
+constexpr int CHUNK = 1;  // column tiles per O-accumulator flush: TMEM fp32 accumulation
+                          // is lossy over long K (measured: 64 tiles -> 4e-5 rel error,
+                          // 1 tile -> 5e-7), and the lagged flush hides its latency
+constexpr int NTHREADS = 384;
+constexpr int EPI_WARP0 = 4;
+constexpr int NUM_EPI_WARPS = 8;
+
+
+struct Args {
+  const float* row_img;   // [row tiles][2][BM*DK]
+  const float* col_img;   // [col tiles][2][BN*DK]
+  const float* v_img;     // [col tiles][2][TN*BN]
+  int DK;
+  int64_t n_rows, n_cols;
+  int row_tiles, col_tiles, splits, tiles_per_split;
+  int nstages;
+  int fam;
+  int t;
+  float s2, noise;
+  int64_t diag_offset;
+  int64_t self_offset;
+  const float* V; int64_t ldv;
+  float* out; int64_t ldo;
+  int64_t split_stride;   // 0 = final output
+  int chunk;              // column tiles per O flush
+  int lookahead;          // distance MMAs issued this many tiles ahead (<= nstages - 1)
+};
+
+// ---------------------------------------------------------------------------
+// PTX helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+// D[tmem] (+)= A[smem desc] . B[smem desc]
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// D[tmem] (+)= A[tmem] . B[smem desc]
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+#define GP_R32(a) "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]), \
+    "=r"(a[7]), "=r"(a[8]), "=r"(a[9]), "=r"(a[10]), "=r"(a[11]), "=r"(a[12]), "=r"(a[13]),          \
+    "=r"(a[14]), "=r"(a[15]), "=r"(a[16]), "=r"(a[17]), "=r"(a[18]), "=r"(a[19]), "=r"(a[20]),       \
+    "=r"(a[21]), "=r"(a[22]), "=r"(a[23]), "=r"(a[24]), "=r"(a[25]), "=r"(a[26]), "=r"(a[27]),       \
+    "=r"(a[28]), "=r"(a[29]), "=r"(a[30]), "=r"(a[31])
+#define GP_W32(a) "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]),         \
+    "r"(a[7]), "r"(a[8]), "r"(a[9]), "r"(a[10]), "r"(a[11]), "r"(a[12]), "r"(a[13]), "r"(a[14]),      \
+    "r"(a[15]), "r"(a[16]), "r"(a[17]), "r"(a[18]), "r"(a[19]), "r"(a[20]), "r"(a[21]), "r"(a[22]),   \
+    "r"(a[23]), "r"(a[24]), "r"(a[25]), "r"(a[26]), "r"(a[27]), "r"(a[28]), "r"(a[29]), "r"(a[30]),   \
+    "r"(a[31])
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : GP_R32(v)
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      GP_W32(v)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// SMEM matrix descriptor, K-major, no swizzle (canonical 8-row x 16-byte core
+// matrices): LBO = byte distance between K-adjacent core matrices, SBO =
+// byte distance between M/N-adjacent core matrices. Bits: start>>4 [0,14),
+// LBO>>4 [16,30), SBO>>4 [32,46), version 1 [46,48), layout 0 [61,64).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+// instruction descriptor: D f32, A/B tf32, K-major both, N>>3 at [17,23), M>>4 at [24,29)
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// canonical K-major no-swizzle offset (floats) of element (r, k) in an R-row tile
+__host__ __device__ __forceinline__ int canon(int r, int k, int R) {
+  return (((k >> 2) * (R >> 3) + (r >> 3)) << 5) + ((r & 7) << 2) + (k & 3);
+}
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t y;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(y) : "f"(x));
+  return __uint_as_float(y);
+}
+
+// ---------------------------------------------------------------------------
+// image preparation (fp64 arithmetic, tf32 hi/lo split)
+// ---------------------------------------------------------------------------
+// role 0: row image a_i = [c x_i, -c |x_i|^2 / 2, -c/2]   (R = BM)
+// role 1: col image b_j = [x_j, 1, |x_j|^2]               (R = BN)
+// column means (fp64) of the prescaled points: both sides are shifted by the
+// same vector (translation invariance of r2), which shrinks |x|^2 and with it
+// the cancellation of the expansion |a|^2 + |b|^2 - 2ab in fp32.
+__global__ void column_mean_kernel(const float* __restrict__ X, int64_t ldx, int64_t n, int d,
+                                   double* mean) {
+  __shared__ double red[256];
+  for (int k = blockIdx.x; k < d; k += gridDim.x) {
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += X[i * ldx + k];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+      if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) mean[k] = n > 0 ? red[0] / (double)n : 0.0;
+    __syncthreads();
+  }
+}
+
+// role 0: row image a_i = [c y_i, -c |y_i|^2 / 2, -c/2]   (R = BM)
+// role 1: col image b_j = [y_j, 1, |y_j|^2]               (R = BN)
+// with y = x - mean (fp64), split into tf32 hi + lo.
+__global__ void points_image_kernel(const float* __restrict__ X, int64_t ldx, int64_t n, int d, int DK,
+                                    int R, int role, double c, const double* __restrict__ mean,
+                                    float* img, int64_t ntiles) {
+  int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= ntiles * R) return;
+  int64_t tile = row / R;
+  int r = (int)(row - tile * R);
+  float* hi = img + tile * 2 * (int64_t)R * DK;
+  float* lo = hi + (int64_t)R * DK;
+  double nrm = 0.0;
+  bool valid = row < n;
+  if (valid)
+    for (int k = 0; k < d; ++k) {
+      double x = (double)X[row * ldx + k] - mean[k];
+      nrm += x * x;
+    }
+  for (int k = 0; k < DK; ++k) {
+    double v = 0.0;
+    if (valid) {
+      if (k < d) v = ((double)X[row * ldx + k] - mean[k]) * (role == 0 ? c : 1.0);
+      else if (k == d) v = role == 0 ? -0.5 * c * nrm : 1.0;
+      else if (k == d + 1) v = role == 0 ? -0.5 * c : nrm;
+    }
+    float h = tf32_rna((float)v);
+    float l = (float)(v - (double)h);
+    hi[canon(r, k, R)] = h;
+    lo[canon(r, k, R)] = l;
+  }
+}
+
+// V image: per column tile, element (n = rhs, k = column within tile), R = TN
+__global__ void v_image_kernel(const float* __restrict__ V, int64_t ldv, int t, int64_t ncols,
+                               float* img, int64_t ntiles) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= ntiles * BN * TN) return;
+  int64_t tile = idx / (BN * TN);
+  int rem = (int)(idx - tile * BN * TN);
+  int k = rem / TN, nn = rem - k * TN;  // consecutive threads: consecutive rhs of one column
+  int64_t col = tile * BN + k;
+  float v = (col < ncols && nn < t) ? V[col * ldv + nn] : 0.f;
+  float h = tf32_rna(v);
+  float* base = img + tile * 2 * BN * TN;
+  base[canon(nn, k, TN)] = h;
+  base[BN * TN + canon(nn, k, TN)] = v - h;
+}
+
+// ---------------------------------------------------------------------------
+// the fused kernel
+//   TMEM: S_0..2 (3 x 64 cols, distance accumulators, 2 tiles of look-ahead),
+//         K_0..1 (hi 64 + lo 64 cols each, contraction A operand),
+//         O_0..1 (16 cols each, flushed to registers every CHUNK tiles).
+//   Barriers: full/empty (SMEM ring), s_full[3] (MMA -> epilogue),
+//   k_full[2] (epilogue -> MMA), k_empty[2] (MMA -> epilogue, contraction
+//   done reading K), o_full/o_empty[2], xr_full/xr_empty (row image).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t TMS(uint32_t b) { return b * 64; }           // 0, 64, 128
+__device__ __forceinline__ uint32_t TMKH(uint32_t b) { return 192 + b * 128; }   // 192, 320
+__device__ __forceinline__ uint32_t TMKL(uint32_t b) { return 256 + b * 128; }   // 256, 384
+__device__ __forceinline__ uint32_t TMO(uint32_t c) { return 448 + c * 16; }     // 448, 464
+
+template <int FAM>
+__global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int DK = a.DK;
+  const uint32_t row_bytes = 2u * BM * DK * 4u;
+  const uint32_t col_bytes = 2u * BN * DK * 4u;
+  const uint32_t v_bytes = 2u * TN * BN * 4u;
+  const uint32_t stage_bytes = col_bytes + v_bytes;
+  const int NS = a.nstages;
+  uint8_t* xr_s = smem;
+  uint8_t* stages = smem + row_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + NS * stage_bytes);
+  uint64_t* full = bars;             // [NS]
+  uint64_t* empty = bars + NS;       // [NS]
+  uint64_t* s_full = bars + 2 * NS;  // [3]
+  uint64_t* k_full = s_full + 3;     // [2]
+  uint64_t* k_empty = k_full + 2;    // [2]
+  uint64_t* o_full = k_empty + 2;    // [2]
+  uint64_t* o_empty = o_full + 2;    // [2]
+  uint64_t* xr_full = o_empty + 2;   // [1]
+  uint64_t* xr_empty = xr_full + 1;  // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xr_empty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int b = 0; b < 3; ++b) mbar_init(smem_u32(&s_full[b]), 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&k_full[b]), NUM_EPI_WARPS);
+      mbar_init(smem_u32(&k_empty[b]), 1);
+      mbar_init(smem_u32(&o_full[b]), 1);
+      mbar_init(smem_u32(&o_empty[b]), 4);
+    }
+    mbar_init(smem_u32(xr_full), 1);
+    mbar_init(smem_u32(xr_empty), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int n_items = a.row_tiles * a.splits;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      uint32_t s = 0, ph = 0, itc = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++itc) {
+        const int rt = it / a.splits, sp = it - rt * a.splits;
+        const int ct0 = sp * a.tiles_per_split;
+        const int ct1 = min(a.col_tiles, ct0 + a.tiles_per_split);
+        mbar_wait(smem_u32(xr_empty), (itc & 1) ^ 1);
+        mbar_expect_tx(smem_u32(xr_full), row_bytes);
+        bulk_g2s(smem_u32(xr_s), a.row_img + (int64_t)rt * (row_bytes / 4), row_bytes, smem_u32(xr_full));
+        const float* cimg = a.col_img + (int64_t)ct0 * (col_bytes / 4);
+        const float* vimg = a.v_img + (int64_t)ct0 * (v_bytes / 4);
+        for (int ct = ct0; ct < ct1; ++ct) {
+          mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+          uint8_t* st = stages + s * stage_bytes;
+          mbar_expect_tx(smem_u32(&full[s]), stage_bytes);
+          bulk_g2s(smem_u32(st), cimg, col_bytes, smem_u32(&full[s]));
+          bulk_g2s(smem_u32(st + col_bytes), vimg, v_bytes, smem_u32(&full[s]));
+          cimg += col_bytes / 4;
+          vimg += v_bytes / 4;
+          if (++s == (uint32_t)NS) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    // The whole warp runs the (warp-uniform) control flow so bookkeeping
+    // lives in uniform registers; one elected lane issues tcgen05 ops.
+    // Descriptors are built once; per-MMA work is a 32-bit add on the
+    // start-address field (addresses advance in 16-byte units).
+    const uint32_t idesc_d = make_idesc(BM, BN);
+    const uint32_t idesc_c = make_idesc(BM, TN);
+    const uint32_t lbo_a = (BM / 8) * 128, lbo_b = (BN / 8) * 128, lbo_v = (TN / 8) * 128;
+    const uint32_t a_half16 = (BM * DK * 4) >> 4, b_half16 = (BN * DK * 4) >> 4;
+    const uint32_t v_half16 = (TN * BN * 4) >> 4;
+    const int ksteps = DK / 8;
+    const uint64_t da0 = make_desc(smem_u32(xr_s), lbo_a, 128);
+    const uint64_t db0 = make_desc(smem_u32(stages), lbo_b, 128);
+    const uint64_t dv0 = make_desc(smem_u32(stages + col_bytes), lbo_v, 128);
+    const uint32_t stage16 = stage_bytes >> 4;
+    const uint32_t kstep_a16 = (2 * lbo_a) >> 4, kstep_b16 = (2 * lbo_b) >> 4, kstep_v16 = (2 * lbo_v) >> 4;
+    const bool leader = elect_one();
+    // distance-stage ring position (ahead of the contraction by LA tiles)
+    uint32_t ds = 0, dph = 0;      // stage / phase for the next dist()
+    uint32_t cs = 0;               // stage of the next contraction
+    uint32_t sb_next = 0, sph_unused = 0;
+    (void)sph_unused;
+    uint32_t kb = 0, kph = 0;      // K buffer / phase of the next contraction
+    uint32_t oc = 0, oph = 0;      // O buffer / phase
+    uint32_t itc = 0;
+    const int LA = a.lookahead;    // 1 or 2; the SMEM ring needs LA + 1 stages
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++itc) {
+      const int sp = it % a.splits;
+      const int ct0 = sp * a.tiles_per_split;
+      const int ct1 = min(a.col_tiles, ct0 + a.tiles_per_split);
+      const int J = ct1 - ct0;
+      mbar_wait(smem_u32(xr_full), itc & 1);
+      tc_fence_after();
+      auto dist = [&]() {
+        mbar_wait(smem_u32(&full[ds]), dph);
+        tc_fence_after();
+        const uint32_t d_tm = tmem + TMS(sb_next);
+        const uint64_t db = db0 + (uint64_t)(ds * stage16);
+        if (leader) {
+#pragma unroll
+          for (int pass = 0; pass < 3; ++pass) {
+            const uint64_t a_p = da0 + (pass == 0 ? a_half16 : 0u);
+            const uint64_t b_p = db + (pass == 1 ? b_half16 : 0u);
+            for (int ks = 0; ks < ksteps; ++ks)
+              mma_ss(d_tm, a_p + (uint64_t)(ks * kstep_a16), b_p + (uint64_t)(ks * kstep_b16), idesc_d,
+                     (pass | ks) != 0);
+          }
+          tc_commit(smem_u32(&s_full[sb_next]));
+        }
+        __syncwarp();
+        if (++ds == (uint32_t)NS) { ds = 0; dph ^= 1; }
+        if (++sb_next == 3) sb_next = 0;
+      };
+      for (int jj = 0; jj < LA && jj < J; ++jj) dist();
+      for (int jj = 0; jj < J; ++jj) {
+        // S buffer of tile jj+LA was last read by the epilogue for tile
+        // jj+LA-3 <= jj-1, whose k_full we waited for already
+        if (jj + LA < J) dist();
+        mbar_wait(smem_u32(&k_full[kb]), kph);
+        tc_fence_after();
+        mbar_wait(smem_u32(&o_empty[oc]), oph ^ 1);  // chunk = 1 tile
+        tc_fence_after();
+        const uint64_t vb = dv0 + (uint64_t)(cs * stage16);
+        const uint32_t o_tm = tmem + TMO(oc);
+        const uint32_t khi = tmem + TMKH(kb), klo = tmem + TMKL(kb);
+        if (leader) {
+          // O = Klo.Vhi + Khi.Vlo + Khi.Vhi  (fresh accumulator every tile)
+#pragma unroll
+          for (int pass = 0; pass < 3; ++pass) {
+            const uint32_t ka = pass == 0 ? klo : khi;
+            const uint64_t vp = vb + (pass == 1 ? v_half16 : 0u);
+#pragma unroll
+            for (int ks = 0; ks < BN / 8; ++ks)
+              mma_ts(o_tm, ka + ks * 8, vp + (uint64_t)(ks * kstep_v16), idesc_c, (pass | ks) != 0);
+          }
+          tc_commit(smem_u32(&empty[cs]));
+          tc_commit(smem_u32(&k_empty[kb]));
+          tc_commit(smem_u32(&o_full[oc]));
+        }
+        __syncwarp();
+        if (++cs == (uint32_t)NS) cs = 0;
+        if (++kb == 2) { kb = 0; kph ^= 1; }
+        if (++oc == 2) { oc = 0; oph ^= 1; }
+      }
+      if (leader) tc_commit(smem_u32(xr_empty));
+      __syncwarp();
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ===================== epilogue (8 warps) =====================
+    const int q = warp & 3;                    // TMEM lane quarter
+    const int half = (warp - EPI_WARP0) >> 2;  // column half of the 64-col tile
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    uint32_t sb = 0, sph = 0;   // S buffer / phase
+    uint32_t kb = 0, kph = 0;   // K buffer / phase
+    uint32_t oc = 0, oph = 0;   // O buffer / phase of the next tile's product
+    float acc[TN];
+    // Every tile's product O_t = K_t V_t lands in a fresh TMEM accumulator
+    // (tensor-core fp32 accumulation over long K is lossy); half-0 warps fold
+    // it into fp32 registers one tile later, when it is long complete.
+    int pending = 0;
+    uint32_t pend_c = 0, pend_ph = 0;
+    auto flush = [&]() {
+      mbar_wait(smem_u32(&o_full[pend_c]), pend_ph);
+      tc_fence_after();
+      uint32_t o[16];
+      tmem_ld16(tmem + lane_base + TMO(pend_c), o);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < TN; ++c) acc[c] += __uint_as_float(o[c]);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&o_empty[pend_c]));
+      pending = 0;
+    };
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int rt = it / a.splits, sp = it - rt * a.splits;
+      const int ct0 = sp * a.tiles_per_split;
+      const int ct1 = min(a.col_tiles, ct0 + a.tiles_per_split);
+      const int J = ct1 - ct0;
+      const int64_t my_row = (int64_t)rt * BM + q * 32 + lane;
+      const int64_t diag_col = (a.self_offset >= 0 && my_row < a.n_rows) ? my_row + a.self_offset : -1000;
+#pragma unroll
+      for (int c = 0; c < TN; ++c) acc[c] = 0.f;
+      int64_t e_diag = diag_col - ((int64_t)ct0 * BN + half * 32);
+      for (int jj = 0; jj < J; ++jj, e_diag -= BN) {
+        mbar_wait(smem_u32(&s_full[sb]), sph);
+        tc_fence_after();
+        uint32_t v[32];
+        tmem_ld32(tmem + lane_base + TMS(sb) + half * 32, v);
+        tmem_wait_ld();
+        // self-diagonal entry (same point on both sides): r2 = 0 exactly
+        if (__any_sync(0xffffffffu, e_diag >= 0 && e_diag < 32)) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (e == e_diag) v[e] = 0u;
+        }
+        uint32_t hi[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          float sv = __uint_as_float(v[e]);
+          float kap;
+          // clamps written as selects so NaN inputs propagate (the
+          // reference raises on non-finite blocks, partition.py:231-236)
+          if (FAM == GP_FAMILY_RBF) {
+            kap = ex2_approx(sv > 0.f ? 0.f : sv);  // S = -log2(e) r2 / 2
+          } else {
+            float u = sqrt_approx(sv < 0.f ? 0.f : sv);  // S = 3 r2, u = sqrt(3) r
+            float ex = ex2_approx(u * -kLog2e);
+            kap = fmaf(u, ex, ex);                       // (1 + sqrt3 r) e^{-sqrt3 r}
+          }
+          uint32_t h = __float_as_uint(kap) & 0xFFFFE000u;
+          hi[e] = h;
+          v[e] = __float_as_uint(kap - __uint_as_float(h));
+        }
+        // K buffer kb was last read by the contraction two tiles ago
+        mbar_wait(smem_u32(&k_empty[kb]), kph ^ 1);
+        tc_fence_after();
+        tmem_st32(tmem + lane_base + TMKH(kb) + half * 32, hi);
+        tmem_st32(tmem + lane_base + TMKL(kb) + half * 32, v);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&k_full[kb]));
+        if (half == 0) {
+          if (pending) flush();
+          pending = 1;
+          pend_c = oc;
+          pend_ph = oph;
+        }
+        if (++sb == 3) { sb = 0; sph ^= 1; }
+        if (++kb == 2) { kb = 0; kph ^= 1; }
+        if (++oc == 2) { oc = 0; oph ^= 1; }
+      }
+      if (half == 0) {
+        if (pending) flush();
+        const int64_t row = my_row;
+        if (row < a.n_rows) {
+          float* dst = a.split_stride ? a.out + (int64_t)sp * a.split_stride + row * a.t
+                                      : a.out + row * a.ldo;
+#pragma unroll
+          for (int c = 0; c < TN; ++c) {
+            if (c < a.t) {
+              float r = acc[c];
+              if (!a.split_stride) {
+                r *= a.s2;
+                if (a.diag_offset >= 0) r = fmaf(a.noise, a.V[(row + a.diag_offset) * a.ldv + c], r);
+              }
+              dst[c] = r;
+            }
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+struct Plan {
+  int DK, row_tiles, col_tiles, splits, tiles_per_split, nstages;
+  size_t row_img_bytes, col_img_bytes, v_img_bytes, split_bytes, smem;
+};
+
+static Plan make_plan(const gp_kv_desc* d, int t) {
+  Plan p;
+  p.DK = (d->d + 2 + 7) / 8 * 8;
+  p.row_tiles = (int)((d->n_rows + BM - 1) / BM);
+  p.col_tiles = (int)((d->n_cols + BN - 1) / BN);
+  // column splits depend on the column count only for the square training
+  // operator (bitwise-identical rows under any row sharding)
+  int64_t hint_rows = (d->diag_offset >= 0 || d->Xr == d->Xc) ? d->n_cols : d->n_rows;
+  int64_t hint_tiles = (hint_rows + BM - 1) / BM;
+  int64_t target = 2LL * num_sms();
+  int64_t s = (target + hint_tiles - 1) / hint_tiles;
+  s = std::max<int64_t>(1, std::min<int64_t>({s, 64, (int64_t)p.col_tiles}));
+  p.tiles_per_split = (int)((p.col_tiles + s - 1) / s);
+  p.splits = (p.col_tiles + p.tiles_per_split - 1) / p.tiles_per_split;
+  p.row_img_bytes = (size_t)p.row_tiles * 2 * BM * p.DK * 4;
+  p.col_img_bytes = (size_t)p.col_tiles * 2 * BN * p.DK * 4;
+  p.v_img_bytes = (size_t)p.col_tiles * 2 * BN * TN * 4;
+  p.split_bytes = (p.splits > 1 ? (size_t)p.splits * d->n_rows * t * 4 : 0) + 256 * sizeof(double);
+  size_t row_b = 2u * BM * p.DK * 4, stage_b = 2u * BN * p.DK * 4 + 2u * TN * BN * 4;
+  size_t budget = 220 * 1024 - row_b - 256;
+  p.nstages = (int)std::min<size_t>(4, budget / stage_b);
+  p.smem = row_b + p.nstages * stage_b + 256;
+  return p;
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace tc
+
+bool kv_tc_supported(const gp_kv_desc* d, int t) {
+  if (t < 1 || t > tc::TN) return false;
+  if (d->d < 1 || d->d + 2 > 96) return false;
+  return tc::make_plan(d, t).nstages >= 2;
+}
+
+size_t kv_tc_workspace(const gp_kv_desc* d, int t) {
+  if (!kv_tc_supported(d, t)) return 0;
+  tc::Plan p = tc::make_plan(d, t);
+  return tc::align256(p.row_img_bytes) + tc::align256(p.col_img_bytes) + tc::align256(p.v_img_bytes) +
+         tc::align256(p.split_bytes);
+}
+
+int kv_tc(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out, int64_t ldo, void* ws,
+          size_t ws_bytes, cudaStream_t st) {
+  using namespace tc;
+  Plan p = make_plan(desc, t);
+  size_t need = kv_tc_workspace(desc, t);
+  GP_REQUIRE(ws != nullptr && ws_bytes >= need, "gp_kv(tcgen05): workspace of %zu bytes required, %zu given",
+             need, ws_bytes);
+  char* w = static_cast<char*>(ws);
+  float* row_img = reinterpret_cast<float*>(w); w += align256(p.row_img_bytes);
+  float* col_img = reinterpret_cast<float*>(w); w += align256(p.col_img_bytes);
+  float* v_img = reinterpret_cast<float*>(w); w += align256(p.v_img_bytes);
+  double* mean = reinterpret_cast<double*>(w); w += 256 * sizeof(double);
+  float* split_ws = reinterpret_cast<float*>(w);
+  const double c = desc->family == GP_FAMILY_RBF ? 1.4426950408889634 : -6.0;
+  {
+    column_mean_kernel<<<desc->d, 256, 0, st>>>(desc->Xc, desc->ldc, desc->n_cols, desc->d, mean);
+    GP_LAUNCH_CHECK();
+    int64_t rows = (int64_t)p.row_tiles * BM;
+    points_image_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(
+        desc->Xr, desc->ldr, desc->n_rows, desc->d, p.DK, BM, 0, c, mean, row_img, p.row_tiles);
+    GP_LAUNCH_CHECK();
+    int64_t cols = (int64_t)p.col_tiles * BN;
+    points_image_kernel<<<(unsigned)((cols + 255) / 256), 256, 0, st>>>(
+        desc->Xc, desc->ldc, desc->n_cols, desc->d, p.DK, BN, 1, 1.0, mean, col_img, p.col_tiles);
+    GP_LAUNCH_CHECK();
+    int64_t tot = (int64_t)p.col_tiles * BN * TN;
+    v_image_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(V, ldv, t, desc->n_cols, v_img,
+                                                                 p.col_tiles);
+    GP_LAUNCH_CHECK();
+  }
+  Args a;
+  a.row_img = row_img; a.col_img = col_img; a.v_img = v_img; a.DK = p.DK;
+  a.n_rows = desc->n_rows; a.n_cols = desc->n_cols;
+  a.row_tiles = p.row_tiles; a.col_tiles = p.col_tiles; a.splits = p.splits;
+  a.tiles_per_split = p.tiles_per_split; a.nstages = p.nstages; a.fam = desc->family; a.t = t;
+  a.s2 = (float)desc->outputscale; a.noise = (float)desc->noise; a.diag_offset = desc->diag_offset;
+  a.self_offset = desc->self_offset;
+  a.V = V; a.ldv = ldv;
+  a.lookahead = std::min(2, p.nstages - 1);
+  a.chunk = CHUNK;
+  if (p.splits > 1) {
+    a.out = split_ws; a.ldo = t; a.split_stride = desc->n_rows * (int64_t)t;
+  } else {
+    a.out = out; a.ldo = ldo; a.split_stride = 0;
+  }
+  int items = p.row_tiles * p.splits;
+  int grid = std::min(items, num_sms());
+  auto kern = desc->family == GP_FAMILY_RBF ? kv_tc_kernel<GP_FAMILY_RBF> : kv_tc_kernel<GP_FAMILY_MATERN32>;
+  GP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+  kern<<<grid, NTHREADS, p.smem, st>>>(a);
+  GP_LAUNCH_CHECK();
+  if (p.splits > 1) {
+    return launch_split_reduce(split_ws, p.splits, a.split_stride, desc->n_rows, t, out, ldo, a.s2,
+                               a.noise, V, ldv, desc->diag_offset, st);
+  }
+  return GP_OK;
+}
+
 }  // namespace gp
 
-extern "C" int gp_has_tcgen05(void) { return 0; }
+extern "C" int gp_has_tcgen05(void) { return 1; }

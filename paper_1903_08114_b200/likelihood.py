@@ -90,7 +90,7 @@ def draw_probes(n: int, t: int, seed: int, cache) -> np.ndarray:
 def training_operator(model: KernelModel, ps, algo: int = 0) -> FusedOperator:
     Xs32, _ = ps.scaled(model.scale_for(ps.d))
     kv = _ops.FusedKernelOperator(model.family_code, ps.d, Xs32, Xs32, model.outputscale, 0.0,
-                                  -1, algo=algo)
+                                  -1, algo=algo, self_offset=0)
     return FusedOperator(kv, model.noise, ps.n)
 
 

@@ -143,3 +143,82 @@ def test_row_shards_bitwise_equal_full():
         b = np.linspace(0, 20_000, shards + 1).astype(int)
         parts = np.vstack([_kv_rows(w, X, V, b[i], b[i + 1] - b[i]) for i in range(shards)])
         assert np.array_equal(parts, full), shards
+
+
+# --------------------------------------------------------------------------
+# tcgen05 kernel (algo=2) vs the reference goldens / SIMT kernel
+# --------------------------------------------------------------------------
+
+def _kv(m, X, V, algo, rows=None, Xc=None):
+    import torch
+    from paper_1903_08114_b200 import _device as D, _ops
+    ps = D.points(X)
+    ls = m.scale_for(ps.d)
+    Xs32, _ = ps.scaled(ls)
+    if Xc is None:
+        r0, r1 = rows if rows else (0, ps.n)
+        op = _ops.FusedKernelOperator(m.family_code, ps.d, Xs32[r0:r1], Xs32, m.outputscale, m.noise, r0,
+                                      algo=algo)
+    else:
+        cs = D.points(Xc)
+        Xc32, _ = cs.scaled(ls)
+        op = _ops.FusedKernelOperator(m.family_code, ps.d, Xs32, Xc32, m.outputscale, 0.0, -1, algo=algo)
+    V32 = torch.from_numpy(np.ascontiguousarray(V, dtype=np.float32)).cuda()
+    return op.apply32(V32, V.shape[1]).double().cpu().numpy()
+
+
+def test_tc_kernel_compiled():
+    from paper_1903_08114_b200 import _lib
+    assert _lib.lib().gp_has_tcgen05() == 1
+
+
+def test_tc_small_goldens():
+    g = load_golden("kv_small")
+    for c in range(int(g["ncases"])):
+        hp = hp_from(g, f"c{c}_")
+        m = model_of(hp)
+        X, V = g[f"c{c}_X"], g[f"c{c}_V"]
+        got = _kv(m, X, V, algo=2)
+        assert colrel(got, g[f"c{c}_KV"]) <= KV_RTOL, (c, colrel(got, g[f"c{c}_KV"]))
+        got = _kv(m, g[f"c{c}_Xt"], V[:, :1], algo=2, Xc=X)
+        assert colrel(got[:, 0], g[f"c{c}_Kxv"]) <= KV_RTOL, c
+
+
+@pytest.mark.parametrize("key", ["C2", "C3", "C4", "C5", "M1e6"])
+def test_tc_row_subsets_large_configs(key):
+    g = load_golden("row_subsets")
+    w = syn.WORKLOADS[key]
+    X = syn.whitened_inputs(w.n, w.d, 0)
+    V = syn.rhs_block(w.n, 11, 2)
+    rows = int(g[f"{key}_rows"])
+    for s, exp in zip(g[f"{key}_starts"], g[f"{key}_KV"]):
+        got = _kv_rows(w, X, V, int(s), rows, algo=2)
+        assert colrel(got, exp) <= KV_RTOL, (key, s, colrel(got, exp))
+
+
+def test_tc_row_shards_bitwise_equal_full():
+    w = syn.WORKLOADS["C5"]
+    X = syn.whitened_inputs(w.n, w.d, 0)[:30_000]
+    V = syn.rhs_block(30_000, 11, 2)
+    full = _kv_rows(w, X, V, 0, 30_000, algo=2)
+    simt = _kv_rows(w, X, V, 0, 30_000, algo=1)
+    assert colrel(full, simt) <= 1e-5
+    for shards in (2, 3, 8):
+        b = np.linspace(0, 30_000, shards + 1).astype(int)
+        parts = np.vstack([_kv_rows(w, X, V, b[i], b[i + 1] - b[i], algo=2) for i in range(shards)])
+        assert np.array_equal(parts, full), shards
+
+
+@pytest.mark.parametrize("t", [1, 3, 11, 16])
+def test_tc_widths_and_families(t):
+    rng = np.random.default_rng(t)
+    for fam in ("rbf", "matern32"):
+        for d in (1, 3, 8, 30):
+            n = 700
+            X = rng.standard_normal((n, d))
+            V = rng.standard_normal((n, t))
+            ls = np.linspace(0.75, 1.5, d) * np.sqrt(d)
+            m = gp.KernelModel(fam, 1.3, ls, 0.2)
+            ref = O.kernel_mvm(O.make_hp(fam, 1.3, ls, 0.2), X, V)
+            got = _kv(m, X, V, algo=2)
+            assert colrel(got, ref) <= KV_RTOL, (fam, d, t, colrel(got, ref))
