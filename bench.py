@@ -50,6 +50,16 @@ def parse():
     return ap.parse_args()
 
 
+def load_traffic():
+    """dram bytes per K·V launch from the committed ncu --set full capture
+    (profiles/kv_tc_ncu_summary.json), scaled to this launch's rows x cols."""
+    try:
+        with open(os.path.join(HERE, "profiles", "kv_tc_ncu_summary.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return None
+
+
 def load_peaks():
     try:
         with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as fh:
@@ -278,6 +288,10 @@ def run_ours(args):
     sfu_peak_entries = 148 * 16 * sm_mhz_max * 1e6 / mufu_per_entry
     job_tflops = n * n * (2 * w.d + 2 * T_RHS) / (kv_ms_max / 1e3) / 1e12
 
+    traffic = None
+    tsum = load_traffic()
+    if tsum and tsum.get("n") == n and tsum.get("rows") == (r1 - r0):
+        traffic = tsum["dram_bytes_per_launch"]
     e2e = None
     if not args.no_e2e:
         e2e = e2e_run(args, w, n, X, y, model, comm, r0, r1)
@@ -310,7 +324,7 @@ def run_ours(args):
             "kv_tflops": job_tflops,
             "kv_ms_per_launch": kv_ms_max,
             "roofline": {"bound": "tensor", "achieved": tflops, "peak": peaks["bf16_tflops"],
-                         "unit": "TFLOP/s", "frac": tflops / peaks["bf16_tflops"], "traffic": None,
+                         "unit": "TFLOP/s", "frac": tflops / peaks["bf16_tflops"], "traffic": traffic,
                          "peak_source": f"{peak_kind} bf16 dense (MEASURED_PEAKS.json)",
                          "binding_unit": {
                              "bound": "sfu", "achieved": entries_per_s / 1e9,
