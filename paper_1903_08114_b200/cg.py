@@ -158,6 +158,82 @@ class DeviceSolve:
         return [_tridiagonal(a, b) for a, b in zip(self.alphas, self.betas)]
 
 
+class CudaPhases:
+    """The mBCG phase kernels of the C ABI (gp_mbcg_*) on this device's rows,
+    owning the solver state in HBM. MbcgRun drives it; tests substitute a
+    restatement with the same interface to exercise the sharded driver on CPU."""
+
+    def __init__(self, n, t, k, max_iters, noise, precond, L_local, rows32):
+        T = D.torch()
+        self.T = T
+        self.lib = _lib.lib()
+        self.st = _lib.stream_handle()
+        dev = D.device()
+        self.n, self.t, self.k = n, t, k
+        self.ld32 = ld32 = (t + 3) // 4 * 4
+        f64 = dict(dtype=T.float64, device=dev)
+        self.U, self.R, self.P, self.Z = (T.empty((n, t), **f64) for _ in range(4))
+        self.P32 = T.zeros((max(rows32, n), ld32), dtype=T.float32, device=dev)
+        self.red = T.zeros(3 * t + k * t, **f64)
+        self.cbuf = T.zeros(max(k * t, 1), **f64)
+        self.hist = T.zeros((3, max_iters, t), **f64)  # alpha, beta, rel
+        self.vec = T.zeros((3, t), **f64)  # bnorm, gamma, rel
+        self.ints = T.zeros(2 * t + 4, dtype=T.int32, device=dev)
+        plen = int(self.lib.gp_mbcg_partials_len(n, t, k))
+        self.partials = _ops.workspace().f64("mbcg_partials", plen)
+        self.state = _lib.MbcgState(
+            n=n, t=t, k=k, ld=t, ld32=ld32, U=_lib.ptr(self.U), R=_lib.ptr(self.R),
+            P=_lib.ptr(self.P), Z=_lib.ptr(self.Z), P32=_lib.ptr(self.P32), noise=float(noise),
+            L=_lib.ptr(L_local) if k else 0, ldl=L_local.stride(0) if k else 0,
+            Binv=_lib.ptr(precond.binv_device) if k else 0,
+            pc_noise=float(precond.noise) if precond is not None else 0.0,
+            bnorm=_lib.ptr(self.vec[0]), gamma=_lib.ptr(self.vec[1]), red=_lib.ptr(self.red),
+            cbuf=_lib.ptr(self.cbuf), alpha_hist=_lib.ptr(self.hist[0]),
+            beta_hist=_lib.ptr(self.hist[1]), rel=_lib.ptr(self.vec[2]),
+            rel_hist=_lib.ptr(self.hist[2]), active=_lib.ptr(self.ints[:t]),
+            converged=_lib.ptr(self.ints[t:2 * t]), status=_lib.ptr(self.ints[2 * t:]),
+            partials=_lib.ptr(self.partials), partials_len=plen, max_iters=max_iters, nblocks=0)
+        self.sp = _lib.C.byref(self.state)
+        self.status_host = T.zeros(4, dtype=T.int32).pin_memory()
+
+    def init_a(self, B):
+        _lib.check(self.lib.gp_mbcg_init_a(self.sp, _lib.ptr(B), B.stride(0), self.st), "gp_mbcg_init_a")
+
+    def init_b(self):
+        _lib.check(self.lib.gp_mbcg_init_b(self.sp, self.st), "gp_mbcg_init_b")
+
+    def init_c(self):
+        _lib.check(self.lib.gp_mbcg_init_c(self.sp, self.st), "gp_mbcg_init_c")
+
+    def pv(self, Q, q_f64):
+        _lib.check(self.lib.gp_mbcg_pv(self.sp, _lib.ptr(Q), Q.stride(0), int(q_f64), self.st),
+                   "gp_mbcg_pv")
+
+    def update(self, Q, q_f64, it):
+        _lib.check(self.lib.gp_mbcg_update(self.sp, _lib.ptr(Q), Q.stride(0), int(q_f64), it,
+                                           self.st), "gp_mbcg_update")
+
+    def precond(self, it, tol):
+        _lib.check(self.lib.gp_mbcg_precond(self.sp, it, float(tol), self.st), "gp_mbcg_precond")
+
+    def direction(self, it):
+        _lib.check(self.lib.gp_mbcg_direction(self.sp, it, self.st), "gp_mbcg_direction")
+
+    def active(self):
+        return self.ints[:self.t]
+
+    def status(self):
+        """(active columns, first non-PD column or >= t, its iteration); syncs."""
+        self.status_host.copy_(self.ints[2 * self.t:], non_blocking=True)
+        self.T.cuda.current_stream().synchronize()
+        s = self.status_host
+        return int(s[0]), int(s[1]), int(s[2])
+
+    def history(self, its):
+        return (D.to_host(self.hist[:, :its]), D.to_host(self.vec[2]),
+                D.to_host(self.ints[self.t:2 * self.t]).astype(bool))
+
+
 class MbcgRun:
     """Steppable device-resident mBCG (cg.py:84-164) on this device's rows.
 
@@ -168,13 +244,11 @@ class MbcgRun:
     and the fp32 search directions are all-gathered before each K·P."""
 
     def __init__(self, mvm, B, tol: float, max_iters: int = 1000,
-                 precond: PreconditionerCache | None = None, comm=None, row_offset: int = 0):
+                 precond: PreconditionerCache | None = None, comm=None, row_offset: int = 0,
+                 phases_factory=None):
         T = D.torch()
         self.T = T
         self.comm = comm or _Comm()
-        self.lib = _lib.lib()
-        self.st = _lib.stream_handle()
-        dev = D.device()
         B = B.to(T.float64).contiguous()
         n, t = B.shape
         self.n, self.t, self.tol, self.max_iters = n, t, float(tol), int(max_iters)
@@ -182,90 +256,63 @@ class MbcgRun:
         self.precond = precond
         k = precond.rank if precond is not None else 0
         self.k = k
-        ld32 = (t + 3) // 4 * 4
-        self.ld32 = ld32
-        f64 = dict(dtype=T.float64, device=dev)
-        self.U, self.R, self.P, self.Z = (T.empty((n, t), **f64) for _ in range(4))
-        rows32 = getattr(self.comm, "rows_per_rank", n) if self.comm.world > 1 else n
-        self.P32 = T.zeros((max(rows32, n), ld32), dtype=T.float32, device=dev)
-        self.red = T.zeros(3 * t + k * t, **f64)
-        self.cbuf = T.zeros(max(k * t, 1), **f64)
-        self.hist = T.zeros((3, max_iters, t), **f64)  # alpha, beta, rel
-        self.vec = T.zeros((3, t), **f64)  # bnorm, gamma, rel
-        self.ints = T.zeros(2 * t + 4, dtype=T.int32, device=dev)
-        plen = int(self.lib.gp_mbcg_partials_len(n, t, k))
-        self.partials = _ops.workspace().f64("mbcg_partials", plen)
         L = precond.factor_device if precond is not None else None
         if L is not None and L.shape[0] != n:
             L = L[row_offset:row_offset + n]
-        self.L = L
         self.fused = bool(getattr(mvm, "fused", False))
-        self.state = _lib.MbcgState(
-            n=n, t=t, k=k, ld=t, ld32=ld32, U=_lib.ptr(self.U), R=_lib.ptr(self.R),
-            P=_lib.ptr(self.P), Z=_lib.ptr(self.Z), P32=_lib.ptr(self.P32),
-            noise=float(mvm.noise) if self.fused else 0.0,
-            L=_lib.ptr(L) if k else 0, ldl=L.stride(0) if k else 0,
-            Binv=_lib.ptr(precond.binv_device) if k else 0,
-            pc_noise=float(precond.noise) if precond is not None else 0.0,
-            bnorm=_lib.ptr(self.vec[0]), gamma=_lib.ptr(self.vec[1]), red=_lib.ptr(self.red),
-            cbuf=_lib.ptr(self.cbuf), alpha_hist=_lib.ptr(self.hist[0]),
-            beta_hist=_lib.ptr(self.hist[1]), rel=_lib.ptr(self.vec[2]),
-            rel_hist=_lib.ptr(self.hist[2]), active=_lib.ptr(self.ints[:t]),
-            converged=_lib.ptr(self.ints[t:2 * t]), status=_lib.ptr(self.ints[2 * t:]),
-            partials=_lib.ptr(self.partials), partials_len=plen, max_iters=max_iters, nblocks=0)
-        self.sp = _lib.C.byref(self.state)
+        rows32 = getattr(self.comm, "rows_per_rank", n) if self.comm.world > 1 else n
+        factory = phases_factory or CudaPhases
+        self.ph = factory(n, t, k, self.max_iters, float(mvm.noise) if self.fused else 0.0,
+                          precond, L, rows32)
+        self.U = self.ph.U
         if self.fused:
-            self.Q = T.empty((n, t), dtype=T.float32, device=dev)
+            P32 = self.ph.P32
+            self.Q = T.empty((n, t), dtype=T.float32, device=P32.device)
             total = mvm.n_total if self.comm.world == 1 else rows32 * self.comm.world
-            self.P32_full = self.P32 if self.comm.world == 1 else \
-                T.zeros((total, ld32), dtype=T.float32, device=dev)
-        self.status_host = T.zeros(4, dtype=T.int32).pin_memory()
+            self.P32_full = P32 if self.comm.world == 1 else \
+                T.zeros((total, P32.shape[1]), dtype=T.float32, device=P32.device)
         self.iterations = 0
         self.kv_events = None  # optional (start, end) CUDA events around K·P
-        lib, sp, st = self.lib, self.sp, self.st
-        _lib.check(lib.gp_mbcg_init_a(sp, _lib.ptr(B), t, st), "gp_mbcg_init_a")
+        self.ph.init_a(B)
         self._allreduce(t, 2 * t + k * t)
-        _lib.check(lib.gp_mbcg_init_b(sp, st), "gp_mbcg_init_b")
+        self.ph.init_b()
         self._allreduce(2 * t + k * t, 3 * t + k * t)
-        _lib.check(lib.gp_mbcg_init_c(sp, st), "gp_mbcg_init_c")
+        self.ph.init_c()
 
     def _allreduce(self, a, b):
         if self.comm.world > 1 and b > a:
-            self.comm.allreduce_(self.red[a:b])
+            self.comm.allreduce_(self.ph.red[a:b])
 
     def step(self) -> int:
         """One mBCG iteration; returns the active-column count after the freeze."""
         it = self.iterations + 1
         if it > self.max_iters:
             raise RuntimeError("mBCG iteration cap exceeded")
-        lib, sp, st, t, k = self.lib, self.sp, self.st, self.t, self.k
+        t, k, ph = self.t, self.k, self.ph
         if self.fused:
             if self.comm.world > 1:
-                self.comm.allgather_rows(self.P32, self.P32_full)
+                self.comm.allgather_rows(ph.P32, self.P32_full)
             if self.kv_events is not None:
                 self.kv_events[0].record()
             self.mvm.kv.apply32(self.P32_full, t, self.Q)
             if self.kv_events is not None:
                 self.kv_events[1].record()
-            qptr, qf64 = _lib.ptr(self.Q), 0
+            Q, qf64 = self.Q, False
         else:
-            Qd = _apply_user_operator(self.mvm, self.P, self.ints[:t])
-            qptr, qf64 = _lib.ptr(Qd), 1
-        _lib.check(lib.gp_mbcg_pv(sp, qptr, t, qf64, st), "gp_mbcg_pv")
+            Q, qf64 = _apply_user_operator(self.mvm, ph.P, ph.active()), True
+        ph.pv(Q, qf64)
         self._allreduce(0, t)
-        _lib.check(lib.gp_mbcg_update(sp, qptr, t, qf64, it, st), "gp_mbcg_update")
+        ph.update(Q, qf64, it)
         self._allreduce(t, 2 * t + (k * t if self.precond is not None else 0))
-        _lib.check(lib.gp_mbcg_precond(sp, it, self.tol, st), "gp_mbcg_precond")
+        ph.precond(it, self.tol)
         self._allreduce(2 * t + k * t, 3 * t + k * t)
         self.iterations = it
-        self.status_host.copy_(self.ints[2 * t:], non_blocking=True)
-        self.T.cuda.current_stream().synchronize()
-        n_active, bad_col = int(self.status_host[0]), int(self.status_host[1])
+        n_active, bad_col, bad_it = ph.status()
         if bad_col < t:
             raise NumericError(f"operator is not positive definite: p^T A p <= 0 for column "
-                               f"{bad_col} at iteration {int(self.status_host[2])}")
+                               f"{bad_col} at iteration {bad_it}")
         if n_active:
-            _lib.check(lib.gp_mbcg_direction(sp, it, st), "gp_mbcg_direction")
+            ph.direction(it)
         return n_active
 
     def run(self) -> "DeviceSolve":
@@ -276,9 +323,7 @@ class MbcgRun:
 
     def finish(self) -> "DeviceSolve":
         t, its, tol = self.t, self.iterations, self.tol
-        H = D.to_host(self.hist[:, :its])
-        rel = D.to_host(self.vec[2])
-        conv = D.to_host(self.ints[t:2 * t]).astype(bool)
+        H, rel, conv = self.ph.history(its)
         alphas, betas = [], []
         for j in range(t):
             hit = np.flatnonzero(H[2, :, j] <= tol)
