@@ -200,14 +200,18 @@ int gp_precond_factor(int64_t n, int k, const double* L, int64_t ldl, double noi
  * For every geometric hyperparameter p returns sum_ij (dK/dtheta_p)_ij H_ij
  * with H = Y R^T (Y, R: n x w fp32), using prescaled fp32 points:
  *   out[0]     : p = outputscale   (dK/ds2 = kappa)
- *   out[1]     : shared lengthscale, times l  (env * D)
- *   out[1 + i] : ARD lengthscale i, times l_i (env * (xs_i - xs'_i)^2)
- * env = s2 e^{-D/2} (RBF) or 3 s2 e^{-sqrt3 r} (Matern). fp64 output. */
-size_t gp_grad_forms_workspace_bytes(int64_t n_rows, int d, int ard);
+ *   out[1]     : shared lengthscale: sum eps * D * H
+ *   out[1 + i] : ARD lengthscale i:  sum eps * (xs_i - xs'_i)^2 * H
+ * with eps = e^{-D/2} (RBF) or 3 e^{-sqrt3 r} (Matern) (the host multiplies by
+ * s2 and divides by l). fp64 output, deterministic fixed-order reduction. */
+size_t gp_grad_forms_workspace_bytes(int64_t n_rows, int64_t n_cols, int d, int ard, int w);
+/* self_offset: row i of Xr is column i + self_offset of Xc (-1 = unrelated);
+ * algo: 0 = auto (tcgen05 when d + 2 <= 32 and w <= 128), 1 = SIMT, 2 = tcgen05 */
 int gp_grad_forms(int family, int d, int ard, const float* Xr, int64_t ldr, int64_t n_rows,
                   const float* Xc, int64_t ldc, int64_t n_cols, double outputscale,
                   const float* Y, int64_t ldy, const float* R, int64_t ldrr, int w,
-                  double* out, void* workspace, size_t workspace_bytes, void* stream);
+                  int64_t self_offset, int algo, double* out, void* workspace,
+                  size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

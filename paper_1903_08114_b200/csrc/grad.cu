@@ -182,6 +182,12 @@ __global__ void grad_finalize(const double* __restrict__ partials, int nblocks, 
   out[s == 0 ? 0 : 1 + p0 + (s - 1)] = acc;
 }
 
+bool grad_tc_supported(int64_t nr, int64_t nc, int d, int ard, int w);
+size_t grad_tc_workspace(int64_t nr, int64_t nc, int d, int ard, int w);
+int grad_tc(int family, int d, int ard, const float* Xr, int64_t ldr, int64_t nr, const float* Xc,
+            int64_t ldc, int64_t nc, const float* Y, int64_t ldy, const float* R, int64_t ldrr, int w,
+            int64_t self_offset, double* out, void* ws, size_t ws_bytes, cudaStream_t st);
+
 static int grad_splits(int64_t nr, int64_t nc) {
   int64_t row_tiles = (nr + gBM - 1) / gBM;
   int64_t col_tiles = (nc + gBN - 1) / gBN;
@@ -198,18 +204,19 @@ using namespace gp;
 
 extern "C" {
 
-size_t gp_grad_forms_workspace_bytes(int64_t n_rows, int d, int ard) {
-  (void)d; (void)ard;
-  // blocks = row_tiles * S with S <= ceil(2*SMs / row_tiles)
+size_t gp_grad_forms_workspace_bytes(int64_t n_rows, int64_t n_cols, int d, int ard, int w) {
+  // SIMT: blocks = row_tiles * S with S <= ceil(2*SMs / row_tiles)
   int64_t row_tiles = (n_rows + gBM - 1) / gBM;
-  int64_t blocks = row_tiles + 2LL * num_sms() + 1;
-  return (size_t)(blocks * 17) * sizeof(double);
+  size_t simt = (size_t)((row_tiles + 2LL * num_sms() + 1) * 17) * sizeof(double);
+  size_t tcw = grad_tc_supported(n_rows, n_cols, d, ard, w) ? grad_tc_workspace(n_rows, n_cols, d, ard, w) : 0;
+  return simt > tcw ? simt : tcw;
 }
 
 int gp_grad_forms(int family, int d, int ard, const float* Xr, int64_t ldr, int64_t n_rows,
                   const float* Xc, int64_t ldc, int64_t n_cols, double outputscale,
-                  const float* Y, int64_t ldy, const float* R, int64_t ldrr, int w, double* out,
-                  void* workspace, size_t workspace_bytes, void* stream) {
+                  const float* Y, int64_t ldy, const float* R, int64_t ldrr, int w,
+                  int64_t self_offset, int algo, double* out, void* workspace,
+                  size_t workspace_bytes, void* stream) {
   (void)outputscale;
   GP_REQUIRE(family == 0 || family == 1, "gp_grad_forms: family %d", family);
   GP_REQUIRE(d >= 1 && d <= 256 && w >= 1 && w <= 1024, "gp_grad_forms: d=%d w=%d", d, w);
@@ -218,6 +225,12 @@ int gp_grad_forms(int family, int d, int ard, const float* Xr, int64_t ldr, int6
   if (n_rows == 0 || n_cols == 0) {
     GP_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double) * nparams, st));
     return GP_OK;
+  }
+  const bool tc_ok = grad_tc_supported(n_rows, n_cols, d, ard, w);
+  if (algo == 2 || (algo == 0 && tc_ok)) {
+    GP_REQUIRE(tc_ok, "gp_grad_forms: shape unsupported by the tcgen05 kernel (d=%d w=%d)", d, w);
+    return grad_tc(family, d, ard, Xr, ldr, n_rows, Xc, ldc, n_cols, Y, ldy, R, ldrr, w, self_offset, out,
+                   workspace, workspace_bytes, st);
   }
   int S = grad_splits(n_rows, n_cols);
   int64_t col_tiles = (n_cols + gBN - 1) / gBN;

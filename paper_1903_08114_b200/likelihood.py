@@ -159,19 +159,22 @@ def _gradients(model: KernelModel, ps, a, S, W, cache) -> dict:
     return assemble_gradients(model, raw, a, S, W, cache, n)
 
 
-def _grad_forms_raw(model, d, Xr32, Xc32, Y, R):
+def _grad_forms_raw(model, d, Xr32, Xc32, Y, R, self_offset=0, algo=0):
+    """Raw fused gradient forms (csrc/grad_tc.cu, csrc/grad.cu); row i of
+    Xr32 is column i + self_offset of Xc32."""
     T = D.torch()
     ard = 1 if model.ard else 0
     npar = 1 + (d if ard else 1)
     out = T.zeros(npar, dtype=T.float64, device=D.device())
     lib = _lib.lib()
-    nbytes = lib.gp_grad_forms_workspace_bytes(Xr32.shape[0], d, ard)
+    w = Y.shape[1]
+    nbytes = lib.gp_grad_forms_workspace_bytes(Xr32.shape[0], Xc32.shape[0], d, ard, w)
     ws = _ops.workspace().bytes("grad", nbytes)
     _lib.check(lib.gp_grad_forms(model.family_code, d, ard, _lib.ptr(Xr32), Xr32.stride(0),
                                  Xr32.shape[0], _lib.ptr(Xc32), Xc32.stride(0), Xc32.shape[0],
                                  float(model.outputscale), _lib.ptr(Y), Y.stride(0), _lib.ptr(R),
-                                 R.stride(0), Y.shape[1], _lib.ptr(out), _lib.ptr(ws), nbytes,
-                                 _lib.stream_handle()), "gp_grad_forms")
+                                 R.stride(0), w, int(self_offset), int(algo), _lib.ptr(out),
+                                 _lib.ptr(ws), nbytes, _lib.stream_handle()), "gp_grad_forms")
     return out
 
 

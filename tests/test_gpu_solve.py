@@ -190,3 +190,31 @@ def test_grad_forms_match_dense_oracle():
         for k, v in ref["gradients"].items():
             assert abs(res.gradients[k] - v) <= 2e-4 * scale, (fam, ard, k, res.gradients[k], v)
         assert res.value == pytest.approx(ref["value"], rel=1e-5)
+
+
+@pytest.mark.parametrize("fam,ard,d,w", [("rbf", False, 3, 111), ("matern32", True, 11, 111),
+                                         ("matern32", False, 8, 16), ("rbf", True, 20, 40)])
+def test_grad_forms_tcgen05_vs_simt(fam, ard, d, w):
+    """The tensor-core gradient pass matches the FFMA kernel (both fp32
+    inputs, fp64 reductions) on random operands, incl. a multi-chunk ARD."""
+    import torch
+    from paper_1903_08114_b200 import _device as D
+    rng = np.random.default_rng(d * 7 + w)
+    n = 3000
+    X = rng.standard_normal((n, d))
+    ls = np.linspace(0.75, 1.5, d) * np.sqrt(d) if ard else np.array([np.sqrt(d)])
+    m = gp.KernelModel(fam, 1.2, ls, 0.3)
+    ps = D.points(X)
+    Xs32, _ = ps.scaled(ls)
+    Y = torch.from_numpy(rng.standard_normal((n, w))).float().cuda()
+    R = torch.from_numpy(rng.standard_normal((n, w))).float().cuda()
+    a = likelihood._grad_forms_raw(m, d, Xs32, Xs32, Y, R, 0, algo=1).cpu().numpy()
+    b = likelihood._grad_forms_raw(m, d, Xs32, Xs32, Y, R, 0, algo=2).cpu().numpy()
+    # reference sums of |terms| bound the tolerance (random operands cancel)
+    scale = np.abs(a).max()
+    np.testing.assert_allclose(b, a, rtol=0, atol=2e-5 * scale + 1e-9)
+    # sharded rows (self_offset) add up to the full pass
+    h = n // 2
+    b0 = likelihood._grad_forms_raw(m, d, Xs32[:h], Xs32, Y[:h], R, 0, algo=2).cpu().numpy()
+    b1 = likelihood._grad_forms_raw(m, d, Xs32[h:], Xs32, Y[h:], R, h, algo=2).cpu().numpy()
+    np.testing.assert_allclose(b0 + b1, b, rtol=0, atol=2e-5 * scale + 1e-9)
