@@ -7,6 +7,7 @@
 #include "gp_common.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <mutex>
 
@@ -440,21 +441,32 @@ int kv_tc(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out
           void* ws, size_t ws_bytes, cudaStream_t st);
 size_t kv_tc_workspace(const gp_kv_desc* desc, int t);
 bool kv_tc_supported(const gp_kv_desc* desc, int t);
+int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out, int64_t ldo,
+           void* ws, size_t ws_bytes, cudaStream_t st);
+size_t kv_sym_workspace(const gp_kv_desc* desc, int t);
+bool kv_sym_supported(const gp_kv_desc* desc, int t);
 }  // namespace gp
 
 extern "C" {
 
 static bool use_tc(const gp_kv_desc* d, int t) {
   if (d->algo == 1) return false;
-  if (d->algo == 2) return true;
+  if (d->algo == 2 || d->algo == 3) return true;
   return gp_has_tcgen05() && gp::kv_tc_supported(d, t);
+}
+// auto: the symmetric kernel whenever the call is the whole square operator
+static bool use_sym(const gp_kv_desc* d, int t) {
+  if (d->algo == 3) return true;
+  return d->algo == 0 && gp_has_tcgen05() && gp::kv_sym_supported(d, t) && getenv("GP_KV_AUTO_SYM") != nullptr;
 }
 
 size_t gp_kv_workspace_bytes(const gp_kv_desc* desc, int t) {
   if (!desc || t < 1) return 0;
   size_t a = gp::kv_simt_workspace(desc, t);
   size_t b = gp_has_tcgen05() ? gp::kv_tc_workspace(desc, t) : 0;
-  return a > b ? a : b;
+  size_t c = gp_has_tcgen05() ? gp::kv_sym_workspace(desc, t) : 0;
+  a = a > b ? a : b;
+  return a > c ? a : c;
 }
 
 int gp_kv(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out, int64_t ldo,
@@ -474,6 +486,10 @@ int gp_kv(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out
     for (int64_t r = 0; r < desc->n_rows; ++r)
       GP_CUDA_TRY(cudaMemsetAsync(out + r * ldo, 0, sizeof(float) * t, st));
     return GP_OK;
+  }
+  if (use_sym(desc, t)) {
+    GP_REQUIRE(gp::kv_sym_supported(desc, t), "gp_kv: shape unsupported by the symmetric tcgen05 kernel");
+    return gp::kv_sym(desc, V, ldv, t, out, ldo, workspace, workspace_bytes, st);
   }
   if (use_tc(desc, t)) {
     GP_REQUIRE(gp_has_tcgen05(), "gp_kv: tcgen05 kernel requested but not compiled in");

@@ -448,6 +448,13 @@ int distance_images(const float* Xr, int64_t ldr, int64_t nr, const float* Xc, i
   return GP_OK;
 }
 
+int v_images(const float* V, int64_t ldv, int t, int64_t ncols, float* img, int64_t ntiles, cudaStream_t st) {
+  int64_t tot = ntiles * BN * TN;
+  v_image_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(V, ldv, t, ncols, img, ntiles);
+  GP_LAUNCH_CHECK();
+  return GP_OK;
+}
+
 struct Plan {
   int DK, row_tiles, col_tiles, splits, tiles_per_split, nstages;
   size_t row_img_bytes, col_img_bytes, v_img_bytes, split_bytes, smem;
@@ -513,10 +520,7 @@ int kv_tc(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out
     if (int rc = distance_images(desc->Xr, desc->ldr, desc->n_rows, desc->Xc, desc->ldc, desc->n_cols,
                                  desc->d, p.DK, BM, BN, c, mean, row_img, col_img, st))
       return rc;
-    int64_t tot = (int64_t)p.col_tiles * BN * TN;
-    v_image_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(V, ldv, t, desc->n_cols, v_img,
-                                                                 p.col_tiles);
-    GP_LAUNCH_CHECK();
+    if (int rc = v_images(V, ldv, t, desc->n_cols, v_img, p.col_tiles, st)) return rc;
   }
   Args a;
   a.row_img = row_img; a.col_img = col_img; a.v_img = v_img; a.DK = p.DK;

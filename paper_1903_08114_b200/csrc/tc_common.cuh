@@ -99,6 +99,20 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
         "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+// 16 lanes x 256 bits, x8 (64 columns): register r of thread t lands in lane
+// t/4 + 8*((r>>1)&1), column 8*(r>>2) + 2*(t%4) + (r&1)
+__device__ __forceinline__ void tmem_st16x256_x8(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x256b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      GP_W32(v)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -142,6 +156,8 @@ __device__ __forceinline__ float tf32_rna(float x) {
 int distance_images(const float* Xr, int64_t ldr, int64_t nr, const float* Xc, int64_t ldc, int64_t nc,
                     int d, int DK, int BMr, int BNc, double c, double* mean, float* row_img,
                     float* col_img, cudaStream_t st);
+// V image for the contraction: per 64-column tile, 16 RHS x 64 columns, tf32 hi | lo
+int v_images(const float* V, int64_t ldv, int t, int64_t ncols, float* img, int64_t ntiles, cudaStream_t st);
 
 }  // namespace tc
 }  // namespace gp

@@ -1,0 +1,378 @@
+// Probe (run on a B200): M=64 kind::tf32 MMA with A in TMEM (TS form), the
+// accumulator/operand lane layout ("rows m -> lanes (m%16) + 32(m/16)") and
+// the upper half-subpartition (lane offset 16) as a second, interleaved
+// operand/accumulator pair. Build: nvcc -gencode arch=compute_100a,code=sm_100a
+//   -std=c++17 -I paper_1903_08114_b200/csrc scripts/tmem_m64_probe.cu -o /tmp/probe
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <cuda_fp16.h>
+
+#include "tc_common.cuh"
+
+namespace gp {
+int set_error(int code, const char*, ...) { return code; }
+void note_launch() {}
+int num_sms() { return 148; }
+}  // namespace gp
+
+using namespace gp::tc;
+
+__host__ __device__ inline float A1v(int m, int k) { return (float)(((m * 7 + k * 3) % 13) - 6); }
+__host__ __device__ inline float A2v(int m, int k) { return (float)(((m * 5 + k) % 11) - 5); }
+__host__ __device__ inline float Bv(int n, int k) { return (float)(((n * 3 + k * 5) % 7) - 3); }
+
+__global__ void probe(float* out) {
+  __shared__ __align__(1024) float bs[16 * 128];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int e = threadIdx.x; e < 16 * 128; e += blockDim.x) {
+    int n = e / 128, k = e % 128;
+    bs[canon(n, k, 16)] = Bv(n, k);
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  // A operands: lanes 32q + l: l < 16 -> A1 row 16q + l, l >= 16 -> A2 row 16q + l - 16
+  {
+    const int m = 16 * warp + (l & 15);
+    for (int c0 = 0; c0 < 128; c0 += 32) {
+      uint32_t v[32];
+      for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(l < 16 ? A1v(m, c0 + e) : A2v(m, c0 + e));
+      tmem_st32(tmem + ((uint32_t)(32 * warp) << 16) + c0, v);
+    }
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = make_idesc(64, 16);
+    const uint64_t db = make_desc(smem_u32(bs), (16 / 8) * 128, 128);
+    for (int half = 0; half < 2; ++half) {
+      const uint32_t lane = (uint32_t)(16 * half) << 16;
+      for (int ks = 0; ks < 16; ++ks)
+        mma_ts(tmem + lane + 256, tmem + lane + ks * 8, db + (uint64_t)(ks * ((2 * 256) >> 4)), idesc, ks > 0);
+    }
+    tc_commit(smem_u32(&bar));
+  }
+  __syncwarp();
+  mbar_wait(smem_u32(&bar), 0);
+  tc_fence_after();
+  uint32_t o[16];
+  tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + 256, o);
+  tmem_wait_ld();
+  for (int c = 0; c < 16; ++c) out[(warp * 32 + l) * 16 + c] = __uint_as_float(o[c]);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// 16x256b.x8 store placement: thread t, register r -> lane t/4 + 8((r>>1)&1),
+// column 8(r>>2) + 2(t%4) + (r&1); written at lane offset 16, read back with 32x32b
+__global__ void probe_st16(float* out) {
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5, t = threadIdx.x & 31;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  uint32_t z[32];
+  for (int e = 0; e < 32; ++e) z[e] = __float_as_uint(-1.0f);
+  tmem_st32(tmem + ((uint32_t)(32 * warp) << 16), z);
+  tmem_st32(tmem + ((uint32_t)(32 * warp) << 16) + 32, z);
+  tmem_wait_st();
+  uint32_t v[32];
+  for (int r = 0; r < 32; ++r) {
+    int lane = t / 4 + 8 * ((r >> 1) & 1), col = 8 * (r >> 2) + 2 * (t % 4) + (r & 1);
+    v[r] = __float_as_uint((float)(lane * 1000 + col));
+  }
+  tmem_st16x256_x8(tmem + ((uint32_t)(32 * warp + 16) << 16), v);
+  tmem_wait_st();
+  uint32_t o[32];
+  tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16), o);
+  tmem_wait_ld();
+  for (int c = 0; c < 32; ++c) out[(warp * 32 + t) * 64 + c] = __uint_as_float(o[c]);
+  tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + 32, o);
+  tmem_wait_ld();
+  for (int c = 0; c < 32; ++c) out[(warp * 32 + t) * 64 + 32 + c] = __uint_as_float(o[c]);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+int probe2() {
+  float* d;
+  cudaMalloc(&d, 128 * 64 * 4);
+  probe_st16<<<1, 128>>>(d);
+  if (cudaDeviceSynchronize() != cudaSuccess) { printf("probe2 CUDA error\n"); return 1; }
+  std::vector<float> h(128 * 64);
+  cudaMemcpy(h.data(), d, h.size() * 4, cudaMemcpyDeviceToHost);
+  int bad = 0;
+  for (int w = 0; w < 4; ++w)
+    for (int l = 0; l < 32; ++l)
+      for (int c = 0; c < 64; ++c) {
+        float g = h[(w * 32 + l) * 64 + c];
+        float want = l < 16 ? -1.0f : (float)((l - 16) * 1000 + c);
+        if (g != want) { if (bad < 5) printf("lane %d col %d: got %g want %g\n", w * 32 + l, c, g, want); ++bad; }
+      }
+  printf("16x256b.x8 at lane offset 16: %d mismatches\n", bad);
+  return bad ? 2 : 0;
+}
+
+// latency of MMA groups (issue -> commit arrival), single CTA, nothing else running
+__global__ void probe_lat(long long* out) {
+  __shared__ __align__(1024) float bs[2 * 16 * 128 + 2 * 64 * 32];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < (int)(sizeof(bs) / 4); e += blockDim.x) bs[e] = 0.5f;
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0) {
+    const uint64_t dv = make_desc(smem_u32(bs), 256, 128);          // N=16 K-major
+    const uint64_t dc = make_desc(smem_u32(bs + 4096), 1024, 128);   // N=64 K-major
+    uint32_t ph = 0;
+    for (int test = 0; test < 6; ++test) {
+      for (int rep = 0; rep < 3; ++rep) {
+        long long t0 = clock64();
+        if (test == 0) for (int k = 0; k < 24; ++k) mma_ts(tmem + 448, tmem + 128 + k % 8 * 8, dv + k % 8 * 32, make_idesc(128, 16), k > 0);
+        if (test == 1) for (int k = 0; k < 48; ++k) mma_ts(tmem + ((uint32_t)(k >= 32 ? 16 : 0) << 16) + 480, tmem + ((uint32_t)(k >= 32 ? 16 : 0) << 16) + 256 + k % 16 * 8, dv + k % 8 * 32, make_idesc(64, 16), k % 16 > 0);
+        if (test == 2) for (int k = 0; k < 6; ++k) mma_ts(tmem + 0, tmem + 384 + k % 2 * 8, dc + k % 2 * 128, make_idesc(128, 64), k > 0);
+        if (test == 3) for (int k = 0; k < 48; ++k) mma_ss(tmem + 480, dv + k % 8 * 32, dv + k % 8 * 32, make_idesc(64, 16), k % 16 > 0);
+        if (test == 4) for (int k = 0; k < 48; ++k) mma_ts(tmem + 480, tmem + 256 + k % 16 * 8, dv + k % 8 * 32, make_idesc(64, 16), k % 16 > 0);
+        if (test == 5) for (int k = 0; k < 48; ++k) mma_ts(tmem + 448, tmem + 128 + k % 16 * 8, dv + k % 8 * 32, make_idesc(128, 16), k % 16 > 0);
+        tc_commit(smem_u32(&bar));
+        long long t1 = clock64();
+        mbar_wait(smem_u32(&bar), ph);
+        ph ^= 1;
+        long long t2 = clock64();
+        out[test * 2] = t1 - t0;
+        out[test * 2 + 1] = t2 - t0;
+      }
+    }
+  }
+  __syncthreads();
+  // warp-uniform issue (whole warp 0 runs the loop, elected lane issues), unrolled
+  if (warp == 0) {
+    const uint64_t dv = make_desc(smem_u32(bs), 256, 128);
+    const bool leader = elect_one();
+    uint32_t ph = 0;
+    for (int test = 6; test < 9; ++test) {
+      for (int rep = 0; rep < 3; ++rep) {
+        long long t0 = clock64();
+        if (leader) {
+          if (test == 6) {
+#pragma unroll
+            for (int k = 0; k < 24; ++k) mma_ts(tmem + 448, tmem + 128 + (k % 8) * 8, dv + (k % 8) * 32, make_idesc(128, 16), k > 0);
+          } else if (test == 7) {
+#pragma unroll
+            for (int k = 0; k < 48; ++k) mma_ts(tmem + 480, tmem + 256 + (k % 16) * 8, dv + (k % 8) * 32, make_idesc(64, 16), (k % 16) > 0);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 24; ++k) mma_ts(tmem + 256, tmem + 128 + (k % 8) * 8, dv + (k % 8) * 32, make_idesc(128, 256), k > 0);
+          }
+          tc_commit(smem_u32(&bar));
+        }
+        __syncwarp();
+        long long t1 = clock64();
+        mbar_wait(smem_u32(&bar), ph);
+        ph ^= 1;
+        long long t2 = clock64();
+        if (leader) { out[test * 2] = t1 - t0; out[test * 2 + 1] = t2 - t0; }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// kind::f16 TS: A (fp16 pairs packed per 32-bit TMEM column, low half = even k),
+// B fp16 canonical K-major (core = 8 rows x 8 halves), M = 128 and M = 64 (lane 16)
+__device__ __host__ inline int canon16(int r, int k, int R) {
+  return (((k >> 3) * (R >> 3) + (r >> 3)) << 6) + ((r & 7) << 3) + (k & 7);
+}
+__global__ void probe_f16(float* out) {
+  __shared__ __align__(1024) __half bs[32 * 64];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int e = threadIdx.x; e < 32 * 64; e += blockDim.x) {
+    int n = e / 64, k = e % 64;
+    bs[canon16(n, k, 32)] = __float2half(Bv(n, k));
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  {  // A for M=128 at cols [0,32): row = lane; A for M=64 at cols [32,64): lanes (m%16)+32(m/16) (+16: A2)
+    const int row = warp * 32 + l;
+    uint32_t v[32];
+    for (int c = 0; c < 32; ++c) {
+      __half2 h = __floats2half2_rn(A1v(row, 2 * c), A1v(row, 2 * c + 1));
+      v[c] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    tmem_st32(tmem + ((uint32_t)(32 * warp) << 16), v);
+    const int m = 16 * warp + (l & 15);
+    for (int c = 0; c < 32; ++c) {
+      __half2 h = l < 16 ? __floats2half2_rn(A1v(m, 2 * c), A1v(m, 2 * c + 1))
+                         : __floats2half2_rn(A2v(m, 2 * c), A2v(m, 2 * c + 1));
+      v[c] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    tmem_st32(tmem + ((uint32_t)(32 * warp) << 16) + 32, v);
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    auto idesc16 = [](int M, int N) { return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24); };
+    const uint64_t db = make_desc(smem_u32(bs), (32 / 8) * 128, 128);
+    auto mma16 = [](uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                   "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d), "r"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
+    };
+    for (int ks = 0; ks < 4; ++ks)   // M=128, N=32, K=64: D cols [64, 96)
+      mma16(tmem + 64, tmem + ks * 8, db + (uint64_t)(ks * ((2 * 512) >> 4)), idesc16(128, 32), ks > 0);
+    for (int half = 0; half < 2; ++half)   // M=64, N=16 (rows 0-15 of B): D cols [96, 112) lanes 0/16
+      for (int ks = 0; ks < 4; ++ks)
+        mma16(tmem + ((uint32_t)(16 * half) << 16) + 96, tmem + ((uint32_t)(16 * half) << 16) + 32 + ks * 8,
+              db + (uint64_t)(ks * ((2 * 512) >> 4)), idesc16(64, 16), ks > 0);
+    tc_commit(smem_u32(&bar));
+  }
+  __syncwarp();
+  mbar_wait(smem_u32(&bar), 0);
+  tc_fence_after();
+  uint32_t o[32];
+  tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + 64, o);
+  tmem_wait_ld();
+  for (int c = 0; c < 32; ++c) out[(warp * 32 + l) * 48 + c] = __uint_as_float(o[c]);
+  uint32_t o2[16];
+  tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + 96, o2);
+  tmem_wait_ld();
+  for (int c = 0; c < 16; ++c) out[(warp * 32 + l) * 48 + 32 + c] = __uint_as_float(o2[c]);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+int probe3() {
+  float* d;
+  cudaMalloc(&d, 128 * 48 * 4);
+  probe_f16<<<1, 128>>>(d);
+  if (cudaDeviceSynchronize() != cudaSuccess) { printf("probe3 CUDA error\n"); return 1; }
+  std::vector<float> h(128 * 48);
+  cudaMemcpy(h.data(), d, h.size() * 4, cudaMemcpyDeviceToHost);
+  double e1 = 0, e2 = 0;
+  for (int row = 0; row < 128; ++row)
+    for (int n = 0; n < 32; ++n) {
+      double ref = 0;
+      for (int k = 0; k < 64; ++k) ref += (double)A1v(row, k) * Bv(n, k);
+      e1 = std::max(e1, std::abs(h[row * 48 + n] - ref));
+    }
+  for (int w = 0; w < 4; ++w)
+    for (int l = 0; l < 32; ++l) {
+      int m = 16 * w + (l & 15);
+      for (int n = 0; n < 16; ++n) {
+        double ref = 0;
+        for (int k = 0; k < 64; ++k) ref += (double)(l < 16 ? A1v(m, k) : A2v(m, k)) * Bv(n, k);
+        e2 = std::max(e2, std::abs(h[(w * 32 + l) * 48 + 32 + n] - ref));
+      }
+    }
+  printf("kind::f16 TS: M=128 N=32 max err %.3g; M=64 N=16 (lanes 0/16) max err %.3g\n", e1, e2);
+  return (e1 == 0 && e2 == 0) ? 0 : 2;
+}
+
+int main() {
+  probe3();
+  {
+    long long* d;
+    cudaMalloc(&d, 64 * 8);
+    probe_lat<<<1, 128>>>(d);
+    if (cudaDeviceSynchronize() != cudaSuccess) { printf("lat CUDA error\n"); return 1; }
+    long long h[18];
+    cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    const char* nm[9] = {"24x TS M128 N16 K8", "48x TS M64 N16 K8 (lanes 0/16)", "6x TS M128 N64 K8",
+                         "48x SS M64 N16 K8", "48x TS M64 N16 K8 (lanes 0)", "48x TS M128 N16 K8",
+                         "uniform 24x TS M128 N16", "uniform 48x TS M64 N16", "uniform 24x TS M128 N256"};
+    for (int i = 0; i < 9; ++i) printf("%-34s issue %lld cyc, complete %lld cyc\n", nm[i], h[2 * i], h[2 * i + 1]);
+  }
+  if (int r = probe2()) return r;
+  float* d;
+  cudaMalloc(&d, 128 * 16 * 4);
+  cudaMemset(d, 0, 128 * 16 * 4);
+  probe<<<1, 128>>>(d);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    printf("CUDA error %s\n", cudaGetErrorString(e));
+    return 1;
+  }
+  std::vector<float> h(128 * 16);
+  cudaMemcpy(h.data(), d, h.size() * 4, cudaMemcpyDeviceToHost);
+  double err1 = 0, err2 = 0;
+  for (int w = 0; w < 4; ++w)
+    for (int l = 0; l < 32; ++l) {
+      int m = 16 * w + (l & 15);
+      for (int n = 0; n < 16; ++n) {
+        double ref = 0;
+        for (int k = 0; k < 128; ++k) ref += (double)(l < 16 ? A1v(m, k) : A2v(m, k)) * Bv(n, k);
+        double g = h[(w * 32 + l) * 16 + n];
+        (l < 16 ? err1 : err2) = std::max(l < 16 ? err1 : err2, std::abs(g - ref));
+      }
+    }
+  printf("M=64 TS lanes 0-15 max abs err %.3g, lane-offset-16 max abs err %.3g\n", err1, err2);
+  printf("sample row0: %g %g (ref %g)\n", h[0], h[1], [] {
+    double r = 0;
+    for (int k = 0; k < 128; ++k) r += (double)A1v(0, k) * Bv(0, k);
+    return r;
+  }());
+  return (err1 == 0 && err2 == 0) ? 0 : 2;
+}
