@@ -1,21 +1,28 @@
 // Symmetric tcgen05 K·V kernel for the square training operator (sm_100a).
 //
 // out = s2 * kappa(X, X) V (+ noise V), evaluating every unordered pair of
-// points ONCE: K is symmetric, so the tile K_IJ (row tile I, column tile J
-// strictly above the 128 x 128 diagonal block) serves both
-//     out_I += K_IJ   V_J      (direct:  A = K from TMEM, as in kv_tc.cu)
+// points ONCE: K is symmetric, so the tile K_IJ (row tile I of 128 points,
+// column tile J of 64 points strictly above the 128 x 128 diagonal block)
+// serves both
+//     out_I += K_IJ   V_J      (direct:  A = K   from TMEM, M = 128)
 //     out_J += K_IJ^T V_I      (mirror:  A = K^T from TMEM, M = 64)
 // which halves the transcendental (SFU) work that bounds the kernel at CG
 // width. Diagonal blocks are evaluated in full, direct only.
 //
+// Per tile, on the tensor core (one elected thread issues, TMEM accumulators):
+//   S = A_I . B_J^T        3xTF32 (kind::tf32), A = row image in TMEM
+//   O_I = K . V_J          2-term fp16 split of K and of V (kind::f16, K = 16
+//   O_J = K^T . V_I        per instruction): K1.[V1|V2] (N = 32) + K2.V1
+// The fp16 split (K = K1 + K2 with K1 = K truncated to 11 bits, V scaled per
+// column by 2^s into fp16 range) is as accurate as 3xTF32 but needs half the
+// MMA instructions; the kernel is bound by MMA issue (~30 cycles per small-N
+// tcgen05.mma, measured) and the SFU, so instruction count is what matters.
+//
 // The mirror product needs K^T with j in TMEM lanes while the distance tile
-// lands with i in lanes, so each mirrored tile is transposed once through a
-// double-buffered fp32 SMEM tile (producers store kappa, one 4-byte store per
-// entry; consumers load 8-byte pairs, split tf32 hi/lo and write the M = 64
-// TMEM operand with 16x256b stores: hi in lanes 0-15, lo in lanes 16-31).
-// Reading K^T from TMEM rather than SMEM keeps the tensor core off the SMEM
-// port (an SS-form mirror was measured 0.74x of the row-tiled kernel); the
-// row image is TMEM-resident too (TS-form distance product).
+// lands with i in lanes, so each mirrored tile is transposed through a
+// double-buffered fp32 SMEM tile (producers: one 4-byte store per entry;
+// consumers: 8-byte pair loads, fp16 split, 16x256b TMEM stores with K1 in
+// lanes 0-15 and K2 in lanes 16-31 of each sub-partition, the M = 64 layout).
 //
 // Contributions to one output row come from many CTAs, so they are summed in
 // 64-bit FIXED POINT (red.global.add.u64, per-column scale 2^E_c chosen from
@@ -23,11 +30,13 @@
 // the result is bitwise reproducible run to run and independent of the CTA
 // schedule, like the reference's partition-count independence
 // (test_partition.py:92-102). Quantisation error per partial is
-// <= ||V_c||_1 2^-62 (~1e-13 relative at n = 10^6), far below fp32 round-off.
+// <= ||V_c||_1 2^-61 (~1e-13 relative at n = 10^6), far below fp32 round-off.
 //
 // Reference semantics: kernels.py:225-244 (kappa), :293-316 (rows of K̂ incl.
 // the sigma^2 diagonal), partition.py:224-241 (row-block products).
 #include "tc_common.cuh"
+
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -45,31 +54,33 @@ constexpr int NTHREADS = 384;
 constexpr int EPI_WARP0 = 4;
 constexpr int NUM_EPI_WARPS = 8;
 // fp32 kappa^T staging tile in SMEM (double buffered): element (j, i) at
-// j * KT_LD + i. Producers (lane = i) store conflict-free; the row stride of
-// 136 floats (8 banks) makes the consumers' 8-byte loads (16x256b fragment:
-// rows j = lane/4, columns 2(lane%4)) conflict-free as well.
+// j * KT_LD + (i ^ 2(j & 1)). Producers (lane = i) store conflict-free; the
+// 136-float row stride plus the pair swizzle makes the consumers' 8-byte
+// loads (16x256b fragment: rows j = lane/4, column pairs 4(lane%4)) hit 32
+// distinct banks per half-warp.
 constexpr int KT_LD = 136;
 constexpr uint32_t KT32_BYTES = 64u * KT_LD * 4u;
-constexpr uint32_t V_TILE_BYTES = 2u * TN * BN * 4u;  // hi + lo image of one 64-column V tile
+// V image of one 64-point tile: 32 x 64 fp16, rows 0-15 = V1, 16-31 = V2
+constexpr uint32_t V_TILE_BYTES = 2u * TN * BN * 2u;
 
 struct Args {
-  const float* row_img;   // [row tiles][2][BM*DK]
+  const float* row_img;   // [row tiles][2][BM*DK] tf32 hi|lo
   const float* col_img;   // [col tiles][2][BN*DK]
-  const float* v_img;     // [col tiles][2][TN*BN]
+  const __half* v_img;    // [col tiles][32 x 64] fp16
   int DK;
   int64_t n;
   int row_tiles, col_tiles, splits, n_items;
-  int nstages, lookahead;
+  int nstages;
   int t;
-  const int* expo;                  // [TN] E_c: partials are summed as round(v 2^E_c)
+  const int* expo;                  // [TN] partials (in scaled units) summed as round(v 2^expo_c)
   unsigned long long* acc;          // [TN][acc_ld] fixed-point sums (column-major)
   int64_t acc_ld;
   int* bad;                         // [acc_ld] non-finite partial seen for the row
   long long* prof;                  // optional per-warp phase cycle counters (GP_SYM_PROF=1)
-  int atom_mode;                    // diagnostic: 0 fixed-point u64, 1 none, 2 f32, 3 convert only
+  int skip;                         // diagnostic: bit 0 skips mirror MMAs, bit 1 direct, bit 2 dist
 };
 
-// phase timing for the GP_SYM_PROF diagnostic (lane counters, no effect when a.prof == nullptr)
+// phase timing for the GP_SYM_PROF diagnostic (no effect when a.prof == nullptr)
 #define SYM_T(slot, ...)                                  \
   do {                                                    \
     const long long _t0 = a.prof ? clock64() : 0;         \
@@ -78,19 +89,20 @@ struct Args {
   } while (0)
 
 // TMEM columns (512):
-//   SK 2 x 128: the distance tile S lands in [0, 64) of buffer b and the
-//     epilogue overwrites it in place with K_hi, K_lo going to [64, 128)
-//   K^T 128 (M = 64 layout: hi in lanes 0-15, lo in lanes 16-31 of each
-//     sub-partition) | row image hi|lo 2 x DK (DK <= 16)
-//   O_I 32 = [K_hi V_hi + K_lo V_hi | K_hi V_lo]
-//   O_J 2 x 32 (lanes 0-15 [KT_hi V_hi | KT_hi V_lo], lanes 16-31 [KT_lo V_hi | -])
+//   SK 2 x 128: S (fp32) lands in [0, 64) of buffer b; the epilogue writes
+//     K1 | K2 (fp16 pairs along j) into [64, 96) | [96, 128)
+//   K^T 64 (fp16 pairs along i; M = 64 layout: K1 in lanes 0-15, K2 in lanes
+//     16-31 of each sub-partition) | row image hi|lo 2 x DK (<= 64)
+//   O_I 2 x 32 = [K1 V1 + K2 V1 | K1 V2]
+//   O_J 2 x 32 (lanes 0-15 [KT1 V1 | KT1 V2], lanes 16-31 [KT2 V1 | -])
 __device__ __forceinline__ uint32_t TMSK(uint32_t b) { return b * 128; }
-constexpr uint32_t TMKT = 256, TMXA = 384, TMO = 448;
-__device__ __forceinline__ uint32_t TMOJ(uint32_t b) { return b ? 416 : 480; }
+constexpr uint32_t TMKT = 256, TMXA = 320;
+__device__ __forceinline__ uint32_t TMO(uint32_t b) { return 384 + 32 * b; }
+__device__ __forceinline__ uint32_t TMOJ(uint32_t b) { return 448 + 32 * b; }
+
 __device__ __forceinline__ void red_add_u64(unsigned long long* p, long long v) {
   asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-
 // row-tile items: item L = I * splits + sp covers column tiles
 // [2I + sp*C, min(col_tiles, 2I + (sp+1)*C)), C = ceil((col_tiles - 2I) / splits)
 struct Item {
@@ -114,10 +126,9 @@ __device__ __forceinline__ int item_index(int r, int b, int G) {
   return r * G + ((r & 1) ? (G - 1 - b) : b);
 }
 
-// v * 2^E as a (truncated) signed 64-bit integer, on the integer pipes: the
-// F2I.S64 conversion runs on the SFU's XU pipe, which the kappa epilogue
-// saturates. Exact for |v| 2^E >= 2^23; smaller magnitudes lose their
-// sub-unit fraction (<= 2^-E absolute, i.e. <= ||V_c||_1 2^-61).
+// v * 2^E as a (truncated) signed 64-bit integer on the integer pipes (the
+// F2I.S64 conversion would run on the XU pipe the kappa epilogue saturates).
+// Exact for |v| 2^E >= 2^23; smaller magnitudes lose their sub-unit fraction.
 __device__ __forceinline__ long long fixed_point(float v, int E) {
   const uint32_t bits = __float_as_uint(v);
   const int sh = (int)((bits >> 23) & 0xFFu) - 150 + E;      // |v| 2^E = m 2^sh
@@ -126,24 +137,21 @@ __device__ __forceinline__ long long fixed_point(float v, int E) {
   if (((bits >> 23) & 0xFFu) == 0u) mag = 0ull;                 // zero / denormal
   return (bits >> 31) ? -(long long)mag : (long long)mag;
 }
-
-// one fixed-point contribution (lane-parallel)
 __device__ __forceinline__ void contribute(const Args& a, int64_t row, int c, float v, int E) {
   if (!(fabsf(v) < INFINITY)) {
     a.bad[row] = 1;
     return;
   }
-  if (a.atom_mode == 1) return;
-  if (a.atom_mode == 2) {
-    atomicAdd(reinterpret_cast<float*>(a.acc + (int64_t)c * a.acc_ld + row), v);
+  if (a.skip & 8) {   // diagnostic: conversion only
+    if (fixed_point(v, E) == 0x7fffffffffffffffLL) a.bad[row] = 2;
     return;
   }
-  const long long q = fixed_point(v, E);
-  if (a.atom_mode == 3) {
-    if (q == 0x7fffffffffffffffLL) a.bad[row] = 2;
+  if (a.skip & 16) {  // diagnostic: RED without the conversion
+    red_add_u64(a.acc + (int64_t)c * a.acc_ld + row, (long long)__float_as_uint(v));
     return;
   }
-  red_add_u64(a.acc + (int64_t)c * a.acc_ld + row, q);
+  if (a.skip & 32) return;
+  red_add_u64(a.acc + (int64_t)c * a.acc_ld + row, fixed_point(v, E));
 }
 
 template <int FAM>
@@ -164,37 +172,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
   uint64_t* empty = bars + NS;       // [NS]  MMA -> TMA
   uint64_t* s_full = bars + 2 * NS;  // [2]   distance tile landed in SK buffer b
   uint64_t* k_empty = s_full + 2;    // [2]   direct product done reading K in SK buffer b
-  uint64_t* k_full = k_empty + 2;    // K written over S (+ O_I drained)
-  uint64_t* o_full = k_full + 1;     // direct product done
-  uint64_t* o_empty = o_full + 1;    // O_I read
-  uint64_t* kt_full = o_empty + 1;   // K^T written (+ O_J drained)
+  uint64_t* o_full = k_empty + 2;    // [2]   direct product done
+  uint64_t* o_empty = o_full + 2;    // [2]   O_I read
+  uint64_t* oj_full = o_empty + 2;   // [2]   mirror product done
+  uint64_t* oj_empty = oj_full + 2;  // [2]   O_J read
+  uint64_t* k_full = oj_empty + 2;   // K written over S
+  uint64_t* kt_full = k_full + 1;    // K^T written
   uint64_t* kt_empty = kt_full + 1;  // mirror product done reading K^T
-  uint64_t* oj_full = kt_empty + 1;  // [2] mirror product done
-  uint64_t* oj_empty = oj_full + 2;  // [2] O_J read
-  uint64_t* xr_full = oj_empty + 2;  // row image + V_I landed
+  uint64_t* xr_full = kt_empty + 1;  // row image + V_I landed
   uint64_t* xr_empty = xr_full + 1;  // item's products done with them
   uint64_t* xa_full = xr_empty + 1;  // row image copied into TMEM
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xa_full + 1);
+  int* expo_s = reinterpret_cast<int*>(tmem_slot + 4);   // [TN] fixed-point exponents
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < TN) expo_s[threadIdx.x] = a.expo[threadIdx.x];
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
       mbar_init(smem_u32(&empty[s]), 1);
     }
-    mbar_init(smem_u32(&s_full[0]), 1);
-    mbar_init(smem_u32(&s_full[1]), 1);
-    mbar_init(smem_u32(&k_empty[0]), 1);
-    mbar_init(smem_u32(&k_empty[1]), 1);
-    mbar_init(smem_u32(k_full), NUM_EPI_WARPS);
-    mbar_init(smem_u32(o_full), 1);
-    mbar_init(smem_u32(o_empty), 4);
-    mbar_init(smem_u32(kt_full), NUM_EPI_WARPS);
-    mbar_init(smem_u32(kt_empty), 1);
     for (int q = 0; q < 2; ++q) {
+      mbar_init(smem_u32(&s_full[q]), 1);
+      mbar_init(smem_u32(&k_empty[q]), 1);
+      mbar_init(smem_u32(&o_full[q]), 1);
+      mbar_init(smem_u32(&o_empty[q]), 4);
       mbar_init(smem_u32(&oj_full[q]), 1);
       mbar_init(smem_u32(&oj_empty[q]), 4);
     }
+    mbar_init(smem_u32(k_full), NUM_EPI_WARPS);
+    mbar_init(smem_u32(kt_full), NUM_EPI_WARPS);
+    mbar_init(smem_u32(kt_empty), 1);
     mbar_init(smem_u32(xr_full), 1);
     mbar_init(smem_u32(xr_empty), 1);
     mbar_init(smem_u32(xa_full), 4);
@@ -225,11 +233,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
         const int vt = min(2, a.col_tiles - 2 * it.rt);  // V tiles of this row tile
         mbar_expect_tx(smem_u32(xr_full), row_bytes + vt * v_bytes);
         bulk_g2s(smem_u32(xr_s), a.row_img + (int64_t)it.rt * (row_bytes / 4), row_bytes, smem_u32(xr_full));
-        bulk_g2s(smem_u32(vi_s), a.v_img + (int64_t)(2 * it.rt) * (v_bytes / 4), vt * v_bytes,
+        bulk_g2s(smem_u32(vi_s), a.v_img + (int64_t)(2 * it.rt) * (v_bytes / 2), vt * v_bytes,
                  smem_u32(xr_full));
         ++itc;
         const float* cimg = a.col_img + (int64_t)it.ct0 * (col_bytes / 4);
-        const float* vimg = a.v_img + (int64_t)it.ct0 * (v_bytes / 4);
+        const __half* vimg = a.v_img + (int64_t)it.ct0 * (v_bytes / 2);
         for (int ct = it.ct0; ct < it.ct1; ++ct) {
           mbar_wait(smem_u32(&empty[s]), ph ^ 1);
           uint8_t* st = stages + s * stage_bytes;
@@ -237,18 +245,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
           bulk_g2s(smem_u32(st), cimg, col_bytes, smem_u32(&full[s]));
           bulk_g2s(smem_u32(st + col_bytes), vimg, v_bytes, smem_u32(&full[s]));
           cimg += col_bytes / 4;
-          vimg += v_bytes / 4;
+          vimg += v_bytes / 2;
           if (++s == (uint32_t)NS) { s = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    // per tile, in tensor-pipe order: direct(jj), mirror(jj), dist(jj+2) --
-    // dist(jj+2) overwrites the SK buffer direct(jj) just consumed
+    // per tile, in tensor-pipe order: direct(jj), mirror(jj), dist(jj+2); the
+    // distance tile jj+2 reuses the SK buffer of tile jj once direct(jj) is
+    // complete (the pipe does not order one MMA's TMEM-A reads against a
+    // later MMA's D writes, so that is an explicit k_empty wait)
     const uint32_t idesc_d = make_idesc(BM, BN);
-    const uint32_t idesc_c32 = make_idesc(BM, 2 * TN), idesc_c16 = make_idesc(BM, TN);
-    const uint32_t idesc_m32 = make_idesc(BN, 2 * TN), idesc_m16 = make_idesc(BN, TN);
+    const uint32_t idesc_c32 = idesc_f16(BM, 2 * TN), idesc_c16 = idesc_f16(BM, TN);
+    const uint32_t idesc_m32 = idesc_f16(BN, 2 * TN), idesc_m16 = idesc_f16(BN, TN);
     const uint32_t lbo_b = (BN / 8) * 128, lbo_v = (2 * TN / 8) * 128;
     const uint32_t b_half16 = (BN * DK * 4) >> 4;
     const int ksteps = DK / 8;
@@ -259,10 +269,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
     const uint32_t stage16 = stage_bytes >> 4;
     const uint32_t kstep_b16 = (2 * lbo_b) >> 4, kstep_v16 = (2 * lbo_v) >> 4;
     const uint32_t xa_hi = tmem + TMXA, xa_lo = tmem + TMXA + (uint32_t)DK;
-    const uint32_t kt_hi = tmem + TMKT, kt_lo = tmem + (16u << 16) + TMKT;
+    const uint32_t kt1 = tmem + TMKT, kt2 = tmem + (16u << 16) + TMKT;
     const bool leader = elect_one();
     uint32_t ds = 0, dph = 0, cs = 0, dbuf = 0, keph0 = 0, keph1 = 0;
-    uint32_t kph = 0, oph = 0, ktph = 0, ob = 0, ojph = 0;
+    uint32_t kph = 0, ob = 0, oph = 0, ktph = 0, jb = 0, jph = 0;
     uint32_t itc = 0;
     for (int r = 0;; ++r) {
       const int L = item_index(r, b, G);
@@ -276,16 +286,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       ++itc;
       tc_fence_after();
       auto dist = [&]() {   // S = A.B^T into SK[dbuf], A (row image) from TMEM, 3xTF32
-        // the previous direct product reading K from this buffer must be complete:
-        // the tensor pipe does not order an MMA's TMEM-A reads against a later MMA's D writes
         uint32_t& keph = dbuf ? keph1 : keph0;
-        mbar_wait(smem_u32(&k_empty[dbuf]), keph ^ 1);
+        SYM_T(5, mbar_wait(smem_u32(&k_empty[dbuf]), keph ^ 1));
         keph ^= 1;
         SYM_T(5, mbar_wait(smem_u32(&full[ds]), dph));
         tc_fence_after();
         const uint32_t d_tm = tmem + TMSK(dbuf);
         const uint64_t db = db0 + (uint64_t)(ds * stage16);
-        if (leader) {
+        if (leader && !(a.skip & 4)) {
 #pragma unroll
           for (int pass = 0; pass < 3; ++pass) {
             const uint32_t a_p = pass == 0 ? xa_lo : xa_hi;
@@ -293,6 +301,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
             for (int ks = 0; ks < ksteps; ++ks)
               mma_ts(d_tm, a_p + ks * 8, b_p + (uint64_t)(ks * kstep_b16), idesc_d, (pass | ks) != 0);
           }
+        }
+        if (leader) {
           tc_commit(smem_u32(&s_full[dbuf]));
         }
         __syncwarp();
@@ -305,52 +315,57 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       for (int jj = 0; jj < J; ++jj) {
         SYM_T(1, mbar_wait(smem_u32(k_full), kph));
         tc_fence_after();
-        SYM_T(2, mbar_wait(smem_u32(o_empty), oph ^ 1));
-        tc_fence_after();
         kph ^= 1;
-        oph ^= 1;
+        SYM_T(2, mbar_wait(smem_u32(&o_empty[ob]), oph ^ 1));
+        tc_fence_after();
         const uint64_t vb = dv0 + (uint64_t)(cs * stage16);
-        const uint32_t khi = tmem + TMSK(kbuf), klo = khi + 64;
+        const uint32_t k1 = tmem + TMSK(kbuf) + 64, k2 = k1 + 32;
+        if (leader && !(a.skip & 2)) {
+          // direct: O_I[:, 0:32] = K1.[V1 | V2];  O_I[:, 0:16] += K2.V1  (K = 64 = 4 x 16)
+#pragma unroll
+          for (int ks = 0; ks < BN / 16; ++ks)
+            mma16_ts(tmem + TMO(ob), k1 + ks * 8, vb + (uint64_t)(ks * kstep_v16), idesc_c32, ks != 0);
+#pragma unroll
+          for (int ks = 0; ks < BN / 16; ++ks)
+            mma16_ts(tmem + TMO(ob), k2 + ks * 8, vb + (uint64_t)(ks * kstep_v16), idesc_c16, 1);
+        }
         if (leader) {
-          // direct: O_I[:, 0:32] = Khi.[Vhi | Vlo];  O_I[:, 0:16] += Klo.Vhi
-#pragma unroll
-          for (int ks = 0; ks < BN / 8; ++ks)
-            mma_ts(tmem + TMO, khi + ks * 8, vb + (uint64_t)(ks * kstep_v16), idesc_c32, ks != 0);
-#pragma unroll
-          for (int ks = 0; ks < BN / 8; ++ks)
-            mma_ts(tmem + TMO, klo + ks * 8, vb + (uint64_t)(ks * kstep_v16), idesc_c16, 1);
           tc_commit(smem_u32(&empty[cs]));
-          tc_commit(smem_u32(o_full));
+          tc_commit(smem_u32(&o_full[ob]));
           tc_commit(smem_u32(&k_empty[kbuf]));
         }
         __syncwarp();
+        ob ^= 1;
+        if (ob == 0) oph ^= 1;
         if (jj >= first_mirror) {
-          // mirror (M = 64, K = 128 rows of I): lanes 0-15 O_J[:, 0:32] = KThi.[VIhi | VIlo],
-          // lanes 16-31 O_J[:, 0:16] = KTlo.VIhi (summed by the reader)
+          // mirror (M = 64, K = 128 points of I = 8 x 16): lanes 0-15 O_J = KT1.[V1 | V2],
+          // lanes 16-31 O_J[:, 0:16] = KT2.V1 (summed by the reader)
           SYM_T(3, mbar_wait(smem_u32(kt_full), ktph));
           tc_fence_after();
-          SYM_T(4, mbar_wait(smem_u32(&oj_empty[ob]), ojph ^ 1));
-          tc_fence_after();
           ktph ^= 1;
+          SYM_T(4, mbar_wait(smem_u32(&oj_empty[jb]), jph ^ 1));
+          tc_fence_after();
           tacc[7] += 1;
-          const uint32_t oj_hi = tmem + TMOJ(ob), oj_lo = tmem + (16u << 16) + TMOJ(ob);
+          const uint32_t oj1 = tmem + TMOJ(jb), oj2 = tmem + (16u << 16) + TMOJ(jb);
+          if (leader && !(a.skip & 1)) {
+#pragma unroll
+            for (int ks = 0; ks < BM / 16; ++ks)
+              mma16_ts(oj1, kt1 + ks * 8, dvi + (uint64_t)((ks >> 2) * vtile16 + (ks & 3) * kstep_v16),
+                       idesc_m32, ks != 0);
+#pragma unroll
+            for (int ks = 0; ks < BM / 16; ++ks)
+              mma16_ts(oj2, kt2 + ks * 8, dvi + (uint64_t)((ks >> 2) * vtile16 + (ks & 3) * kstep_v16),
+                       idesc_m16, ks != 0);
+          }
           if (leader) {
-#pragma unroll
-            for (int ks = 0; ks < BM / 8; ++ks)
-              mma_ts(oj_hi, kt_hi + ks * 8, dvi + (uint64_t)((ks >> 3) * vtile16 + (ks & 7) * kstep_v16), idesc_m32,
-                     ks != 0);
-#pragma unroll
-            for (int ks = 0; ks < BM / 8; ++ks)
-              mma_ts(oj_lo, kt_lo + ks * 8, dvi + (uint64_t)((ks >> 3) * vtile16 + (ks & 7) * kstep_v16), idesc_m16,
-                     ks != 0);
             tc_commit(smem_u32(kt_empty));
-            tc_commit(smem_u32(&oj_full[ob]));
+            tc_commit(smem_u32(&oj_full[jb]));
           }
           __syncwarp();
-          ob ^= 1;
-          if (ob == 0) ojph ^= 1;
+          jb ^= 1;
+          if (jb == 0) jph ^= 1;
         }
-        if (jj + 2 < J) dist();   // into the buffer direct(jj) just read (in-order pipe)
+        if (jj + 2 < J) dist();
         kbuf ^= 1;
         if (++cs == (uint32_t)NS) cs = 0;
       }
@@ -363,39 +378,40 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
     const int half = (warp - EPI_WARP0) >> 2;  // column half of the 64-col tile
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const int i_loc = q * 32 + lane;
-    // consumer view of K^T: rows j = 16q + lane/4 (+8), columns i = 64 half + 8g + 2(lane%4) + c
-    const int cj = 16 * q + (lane >> 2), ci = 64 * half + 2 * (lane & 3);
-    uint32_t sb = 0, sph = 0, oph = 0, ob = 0, ojph = 0, ktph = 0, kbuf = 0;
+    uint32_t sb = 0, sph = 0, ob = 0, oph = 0, jb = 0, jph = 0, ktph = 0, kbuf = 0;
     uint32_t itc = 0, kf_tiles = 0;
     float acc[TN];
     int pending = 0;   // half 0: a direct product not yet folded into acc
     int pendj = 0;     // half 1: a mirror product not yet drained
     int64_t pendj_row0 = 0;
-    auto flush = [&]() {  // half 0: fold the last direct product into registers
-      SYM_T(4, mbar_wait(smem_u32(o_full), oph));
-      oph ^= 1;
+    int ej[TN / 2];   // exponents of this lane's mirror columns (c0 = 0 or 8)
+#pragma unroll
+    for (int c = 0; c < TN / 2; ++c) ej[c] = expo_s[(lane < 16 ? 0 : TN / 2) + c];
+    auto flush = [&]() {  // half 0: fold the oldest direct product into registers
+      SYM_T(4, mbar_wait(smem_u32(&o_full[ob]), oph));
       tc_fence_after();
       uint32_t o[32];
-      tmem_ld32(tmem + lane_base + TMO, o);
+      tmem_ld32(tmem + lane_base + TMO(ob), o);
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(o_empty));
+      if (lane == 0) mbar_arrive(smem_u32(&o_empty[ob]));
+      ob ^= 1;
+      if (ob == 0) oph ^= 1;
 #pragma unroll
       for (int c = 0; c < TN; ++c) acc[c] += __uint_as_float(o[c]) + __uint_as_float(o[c + TN]);
       pending = 0;
     };
-    auto flushj = [&]() {  // half 1: last mirror product -> fixed-point sums
-      mbar_wait(smem_u32(&oj_full[ob]), ojph);
+    auto flushj = [&]() {  // half 1: oldest mirror product -> fixed-point sums
+      SYM_T(4, mbar_wait(smem_u32(&oj_full[jb]), jph));
       tc_fence_after();
       uint32_t o[32];
-      tmem_ld32(tmem + lane_base + TMOJ(ob), o);   // lanes 0-15: [hi.Vhi | hi.Vlo], 16-31: [lo.Vhi | -]
-      tmem_wait_ld();
+      SYM_T(1, tmem_ld32(tmem + lane_base + TMOJ(jb), o); tmem_wait_ld());   // lanes 0-15: [1.V1 | 1.V2], 16-31: [2.V1 | -]
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&oj_empty[ob]));
-      ob ^= 1;
-      if (ob == 0) ojph ^= 1;
+      if (lane == 0) mbar_arrive(smem_u32(&oj_empty[jb]));
+      jb ^= 1;
+      if (jb == 0) jph ^= 1;
       float v[TN];
 #pragma unroll
       for (int c = 0; c < TN; ++c) {
@@ -408,7 +424,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
 #pragma unroll
         for (int c = 0; c < TN / 2; ++c)
           if (c0 + c < a.t)
-            contribute(a, row, c0 + c, lane < 16 ? v[c] : v[c + TN / 2], __ldg(&a.expo[c0 + c]));
+            contribute(a, row, c0 + c, lane < 16 ? v[c] : v[c + TN / 2], ej[c]);
       }
       pendj = 0;
     };
@@ -470,21 +486,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
         }
         float* ktb = kt32 + kbuf * (64 * KT_LD);
         if (mirror) {
-          // kappa^T (fp32) for the transposition: element (j, i) at j*KT_LD + i
+          // kappa^T (fp32) for the transposition
 #pragma unroll
-          for (int e = 0; e < 32; ++e) ktb[(32 * half + e) * KT_LD + i_loc] = __uint_as_float(v[e]);
+          for (int e = 0; e < 32; ++e)
+            ktb[(32 * half + e) * KT_LD + (i_loc ^ ((e & 1) << 1))] = __uint_as_float(v[e]);
         }
-        uint32_t hi[32];
+        uint32_t p1[16], p2[16];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          uint32_t h = v[e] & 0xFFFFE000u;
-          hi[e] = h;
-          v[e] = __float_as_uint(__uint_as_float(v[e]) - __uint_as_float(h));
-        }
-        // K over S in the same buffer (this warp's S reads completed above)
-        tmem_st32(sk + half * 32, hi);
-        tmem_st32(sk + 64 + half * 32, v);
-        if (half == 0 && pending) SYM_T(1, flush());     // drain O_I before direct(jj) reuses it
+        for (int e = 0; e < 16; ++e)
+          split_pair(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]), p1[e], p2[e]);
+        tmem_st16(sk + 64 + half * 16, p1);
+        tmem_st16(sk + 96 + half * 16, p2);
+        if (half == 0 && pending) SYM_T(1, flush());   // direct product of the previous tile
         tmem_wait_st();
         tc_fence_before();
         // k_full counts 8 arrivals per tile; a warp running a tile ahead must
@@ -499,30 +512,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
           SYM_T(3, mbar_wait(smem_u32(kt_empty), ktph ^ 1));        // previous mirror product done with K^T
           ktph ^= 1;
           tc_fence_after();
-          uint32_t w[32];
+          // consumer: register r -> row j = 16q + lane/4 + 8((r>>1)&1), points
+          // i = 64 half + 16(r>>2) + 4(lane%4) + 2(r&1) and i + 1
+          uint32_t w1[16], w2[16];
 #pragma unroll
-          for (int g = 0; g < 8; ++g)
-#pragma unroll
-            for (int h8 = 0; h8 < 2; ++h8) {
-              const float2 x = *reinterpret_cast<const float2*>(&ktb[(cj + 8 * h8) * KT_LD + ci + 8 * g]);
-              w[4 * g + 2 * h8] = __float_as_uint(x.x);
-              w[4 * g + 2 * h8 + 1] = __float_as_uint(x.y);
-            }
-          uint32_t wh[32];
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            wh[e] = w[e] & 0xFFFFE000u;
-            w[e] = __float_as_uint(__uint_as_float(w[e]) - __uint_as_float(wh[e]));
+          for (int r = 0; r < 16; ++r) {
+            const int j = 16 * q + (lane >> 2) + 8 * ((r >> 1) & 1);
+            const int i = 64 * half + 16 * (r >> 2) + 4 * (lane & 3) + 2 * (r & 1);
+            const float2 x = *reinterpret_cast<const float2*>(&ktb[j * KT_LD + (i ^ ((j & 1) << 1))]);
+            split_pair(x.x, x.y, w1[r], w2[r]);
           }
-          tmem_st16x256_x8(tmem + lane_base + TMKT + 64 * half, wh);
-          tmem_st16x256_x8(tmem + lane_base + (16u << 16) + TMKT + 64 * half, w);
+          tmem_st16x256_x4(tmem + lane_base + TMKT + 32 * half, w1);
+          tmem_st16x256_x4(tmem + lane_base + (16u << 16) + TMKT + 32 * half, w2);
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(kt_full));
           kbuf ^= 1;
-          if (half == 1 && pendj) SYM_T(5, flushj());     // previous mirror product (other O_J buffer)
           if (half == 1) {
+            if (pendj) SYM_T(5, flushj());     // previous mirror product (other O_J buffer)
             pendj = 1;
             pendj_row0 = (int64_t)(it.ct0 + jj) * BN;
           }
@@ -535,7 +543,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
         if (my_row < a.n) {
 #pragma unroll
           for (int c = 0; c < TN; ++c)
-            if (c < a.t) contribute(a, my_row, c, acc[c], __ldg(&a.expo[c]));
+            if (c < a.t) contribute(a, my_row, c, acc[c], expo_s[c]);
         }
       } else if (pendj) {
         flushj();
@@ -555,49 +563,46 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
   }
 }
 
-// V image for the sym kernel: per 64-column tile a 32-row K-major operand
-// [V_hi (rows 0-15) | V_lo (rows 16-31)] in the canonical layout, so one
-// N = 32 MMA forms both K_hi.V_hi and K_hi.V_lo
-__global__ void v_image32_kernel(const float* __restrict__ V, int64_t ldv, int t, int64_t ncols, float* img,
-                                 int64_t ntiles) {
-  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= ntiles * BN * TN) return;
-  int64_t tile = idx / (BN * TN);
-  int rem = (int)(idx - tile * BN * TN);
-  int k = rem / TN, nn = rem - k * TN;
-  int64_t col = tile * BN + k;
-  float v = (col < ncols && nn < t) ? V[col * ldv + nn] : 0.f;
-  float h = tf32_rna(v);
-  float* base = img + tile * 2 * BN * TN;
-  base[canon(nn, k, 2 * TN)] = h;
-  base[canon(TN + nn, k, 2 * TN)] = v - h;
-}
-
-// per-column scale 2^E_c with 2^E_c ||V_c||_1 <= 2^61: no partial sum of
-// kappa (<= 1) times V can overflow the signed 64-bit accumulator
+// per column: E_c with 2^E_c ||V_c||_1 <= 2^61 (no fixed-point overflow: kappa
+// <= 1), s_c with 2^s_c max|V_c| <= 2^14 (fp16 range); partial sums arrive in
+// units of 2^s_c, so they are converted with exponent E_c - s_c
 __global__ void sym_scale_kernel(const float* __restrict__ V, int64_t ldv, int64_t n, int t, int* expo,
-                                 double* inv_scale) {
+                                 float* vscale, double* inv_scale) {
   __shared__ double red[256];
+  __shared__ float mx[256];
   const int c = blockIdx.x;
   double s = 0.0;
+  float m = 0.f;
   if (c < t)
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += fabs((double)V[i * ldv + c]);
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const float x = fabsf(V[i * ldv + c]);
+      s += (double)x;
+      m = fmaxf(m, x);
+    }
   red[threadIdx.x] = s;
+  mx[threadIdx.x] = m;
   __syncthreads();
   for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    if ((int)threadIdx.x < o) {
+      red[threadIdx.x] += red[threadIdx.x + o];
+      mx[threadIdx.x] = fmaxf(mx[threadIdx.x], mx[threadIdx.x + o]);
+    }
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    int E = 61;
-    double l1 = red[0];
+    int E = 61, S = 0;
+    const double l1 = red[0];
     if (l1 > 0.0 && l1 < INFINITY) {
       int ex;
       frexp(l1, &ex);  // l1 < 2^ex
       E = 61 - ex;
+      frexp((double)mx[0], &ex);
+      S = 14 - ex;
     }
-    E = max(-120, min(120, E));
-    expo[c] = E;
+    E = max(-100, min(100, E));
+    S = max(-100, min(100, S));
+    expo[c] = E - S;
+    vscale[c] = ldexpf(1.0f, S);
     inv_scale[c] = ldexp(1.0, -E);
   }
 }
@@ -637,7 +642,7 @@ static Plan make_plan(const gp_kv_desc* d) {
   p.v_img_bytes = (size_t)p.col_tiles * V_TILE_BYTES;
   p.acc_bytes = (size_t)TN * p.acc_ld * 8;
   p.bad_bytes = (size_t)p.acc_ld * 4;
-  const size_t fixed = 2 * KT32_BYTES + 2u * BM * p.DK * 4 + 2 * V_TILE_BYTES + 512;
+  const size_t fixed = 2 * KT32_BYTES + 2u * BM * p.DK * 4 + 2 * V_TILE_BYTES + 640;
   const size_t stage_b = 2u * BN * p.DK * 4 + V_TILE_BYTES;
   const size_t budget = 227 * 1024;
   p.nstages = fixed >= budget ? 0 : (int)std::min<size_t>(4, (budget - fixed) / stage_b);
@@ -653,7 +658,7 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // the same point set on both sides, every row and column, t <= 16
 bool kv_sym_supported(const gp_kv_desc* d, int t) {
   if (t < 1 || t > tcs::TN) return false;
-  if (d->d < 1 || d->d + 2 > 16) return false;   // row image hi|lo must fit 32 TMEM columns
+  if (d->d < 1 || d->d + 2 > 32) return false;   // row image hi|lo must fit 64 TMEM columns
   if (d->Xr != d->Xc || d->ldr != d->ldc || d->n_rows != d->n_cols || d->n_rows < 1) return false;
   if (d->self_offset != 0 || (d->diag_offset != 0 && d->diag_offset >= 0)) return false;
   return tcs::make_plan(d).nstages >= 3;
@@ -664,7 +669,7 @@ size_t kv_sym_workspace(const gp_kv_desc* d, int t) {
   tcs::Plan p = tcs::make_plan(d);
   using tcs::align256;
   return align256(p.row_img_bytes) + align256(p.col_img_bytes) + align256(p.v_img_bytes) +
-         align256(p.acc_bytes) + align256(p.bad_bytes) + 256 * sizeof(double) + 2 * 64 * sizeof(double);
+         align256(p.acc_bytes) + align256(p.bad_bytes) + 256 * sizeof(double) + 3 * 64 * sizeof(double);
 }
 
 int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out, int64_t ldo, void* ws,
@@ -677,37 +682,35 @@ int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* ou
   char* w = static_cast<char*>(ws);
   float* row_img = reinterpret_cast<float*>(w); w += align256(p.row_img_bytes);
   float* col_img = reinterpret_cast<float*>(w); w += align256(p.col_img_bytes);
-  float* v_img = reinterpret_cast<float*>(w); w += align256(p.v_img_bytes);
+  __half* v_img = reinterpret_cast<__half*>(w); w += align256(p.v_img_bytes);
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(w); w += align256(p.acc_bytes);
   int* bad = reinterpret_cast<int*>(w); w += align256(p.bad_bytes);
   double* mean = reinterpret_cast<double*>(w); w += 256 * sizeof(double);
   int* expo = reinterpret_cast<int*>(w); w += 64 * sizeof(double);
+  float* vscale = reinterpret_cast<float*>(w); w += 64 * sizeof(double);
   double* inv_scale = reinterpret_cast<double*>(w);
   const int64_t n = desc->n_rows;
   const double c = desc->family == GP_FAMILY_RBF ? 1.4426950408889634 : -6.0;
   GP_CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)t * p.acc_ld * 8, st));
   GP_CUDA_TRY(cudaMemsetAsync(bad, 0, p.bad_bytes, st));
-  sym_scale_kernel<<<TN, 256, 0, st>>>(V, ldv, n, t, expo, inv_scale);
+  sym_scale_kernel<<<TN, 256, 0, st>>>(V, ldv, n, t, expo, vscale, inv_scale);
   GP_LAUNCH_CHECK();
   if (int rc = tc::distance_images(desc->Xr, desc->ldr, n, desc->Xc, desc->ldc, n, desc->d, p.DK, BM, BN, c,
                                    mean, row_img, col_img, st))
     return rc;
   {
-    int64_t tot = (int64_t)p.col_tiles * BN * TN;
-    v_image32_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(V, ldv, t, n, v_img, p.col_tiles);
-    GP_LAUNCH_CHECK();
+    if (int rc = tc::v_images16(V, ldv, t, n, vscale, v_img, p.col_tiles, st)) return rc;
   }
   Args a;
   a.row_img = row_img; a.col_img = col_img; a.v_img = v_img; a.DK = p.DK;
   a.n = n; a.row_tiles = p.row_tiles; a.col_tiles = p.col_tiles; a.splits = p.splits; a.n_items = p.n_items;
-  a.nstages = p.nstages; a.lookahead = 1; a.t = t;
+  a.nstages = p.nstages; a.t = t;
   a.expo = expo; a.acc = acc; a.acc_ld = p.acc_ld; a.bad = bad;
+  a.prof = nullptr;
+  a.skip = getenv("GP_SYM_SKIP") ? atoi(getenv("GP_SYM_SKIP")) : 0;
   int grid = std::min(p.n_items, num_sms());
   auto kern = desc->family == GP_FAMILY_RBF ? kv_sym_kernel<GP_FAMILY_RBF> : kv_sym_kernel<GP_FAMILY_MATERN32>;
   GP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
-  a.prof = nullptr;
-  const char* am = getenv("GP_SYM_ATOM");
-  a.atom_mode = am ? atoi(am) : 0;
   const char* pe = getenv("GP_SYM_PROF");
   if (pe && *pe == '1') GP_CUDA_TRY(cudaMalloc(&a.prof, (size_t)grid * (NTHREADS / 32) * 8 * sizeof(long long)));
   kern<<<grid, NTHREADS, p.smem, st>>>(a);
@@ -717,13 +720,12 @@ int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* ou
     GP_CUDA_TRY(cudaStreamSynchronize(st));
     GP_CUDA_TRY(cudaMemcpy(h.data(), a.prof, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
     cudaFree(a.prof);
-    const char* names[8] = {"wait0", "wait1", "wait2", "wait3", "wait4", "wait5", "total", "tiles"};
-    for (int w : {1, 4, 5, 6, 8, 9}) {
+    for (int wi : {1, 4, 5, 8, 9}) {
       double s[8] = {0};
-      for (int c = 0; c < grid; ++c)
-        for (int k = 0; k < 8; ++k) s[k] += (double)h[((size_t)c * (NTHREADS / 32) + w) * 8 + k];
-      fprintf(stderr, "[sym prof] warp %d:", w);
-      for (int k = 0; k < 8; ++k) fprintf(stderr, " %s=%.0f", names[k], k == 7 ? s[7] / grid : s[k] / std::max(1.0, s[7]));
+      for (int cta = 0; cta < grid; ++cta)
+        for (int k = 0; k < 8; ++k) s[k] += (double)h[((size_t)cta * (NTHREADS / 32) + wi) * 8 + k];
+      fprintf(stderr, "[sym prof] warp %d:", wi);
+      for (int k = 0; k < 8; ++k) fprintf(stderr, " w%d=%.0f", k, k == 7 ? s[7] / grid : s[k] / std::max(1.0, s[7]));
       fprintf(stderr, "\n");
     }
   }

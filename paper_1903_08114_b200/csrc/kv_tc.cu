@@ -6,7 +6,7 @@
 // Per column tile j of a row tile (one CTA per SM, persistent over items):
 //   1. TMA warp   : cp.async.bulk the pre-tiled column image (X_c hi/lo, with
 //                   the squared norm folded in as an extra K column) and the
-//                   V image (hi/lo) into a 4-stage SMEM ring.
+//                   V image [V_hi | V_lo] (tf32, 32 rows) into a 4-stage ring.
 //   2. MMA thread : S = A . B^T on tcgen05 (kind::tf32, M=128, N=64), where
 //                   a_i = [c x_i, -c|x_i|^2/2, -c/2], b_j = [x_j, 1, |x_j|^2]
 //                   so S = -(c/2) r2 exactly in the expansion of
@@ -15,9 +15,16 @@
 //   3. 8 epilogue warps: tcgen05.ld S, kappa on the SFU (RBF: 1 ex2;
 //                   Matern: sqrt + ex2), split K = K_hi + K_lo (tf32), and
 //                   tcgen05.st both back into TMEM as the A operand.
-//   4. MMA thread : O += K_hi.V_hi + K_hi.V_lo + K_lo.V_hi (A from TMEM,
-//                   M=128, N=16, K=64) into a TMEM accumulator that is
-//                   flushed to fp32 registers every 64 tiles (4096 columns).
+//   4. MMA thread : O = K_hi.[V_hi | V_lo] (N = 32) + K_lo.V_hi (N = 16,
+//                   accumulated into the first half), A from TMEM, M=128,
+//                   K=64; a fresh accumulator every tile, folded into fp32
+//                   registers one tile later. Merging two 3xTF32 passes into
+//                   one N = 32 instruction matters: a small-N tcgen05.mma
+//                   costs ~30 cycles of issue (measured), and the 24 N = 16
+//                   instructions of the unmerged contraction bound the tile.
+//                   (A 2-term fp16 split halves the count again but its
+//                   F2FP conversions run on the XU pipe the SFU epilogue
+//                   saturates; measured slower for Matern-3/2.)
 // Reference semantics: kernels.py:225-244 (kappa), :293-316 (rows of K̂),
 // partition.py:224-241 (row-block product). Per-row column order is fixed by
 // the column count, so row sharding across GPUs is bitwise neutral.
@@ -25,6 +32,8 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
+#include <vector>
 
 namespace gp {
 namespace tc {
@@ -35,15 +44,22 @@ constexpr int TN = 16;    // right-hand sides (contraction N)
 constexpr int CHUNK = 1;  // column tiles per O-accumulator flush: TMEM fp32 accumulation
                           // is lossy over long K (measured: 64 tiles -> 4e-5 rel error,
                           // 1 tile -> 5e-7), and the lagged flush hides its latency
-constexpr int NTHREADS = 384;
+// contraction operand format: fp16 2-term split (kind::f16, K = 16 per MMA)
+// or tf32 hi/lo (kind::tf32, K = 8 per MMA); the kernel is bound by the
+// single MMA-issuing thread, so halving the instruction count matters
+constexpr bool KV_F16 = true;
+constexpr uint32_t V_TILE = KV_F16 ? 2u * TN * BN * 2u : 2u * TN * BN * 4u;   // [V1 | V2] of one column tile
+constexpr int NUM_EPI_WARPS = 16;                   // 4 per TMEM lane quarter (SMSP)
+constexpr int EPI_COLS = BN / (NUM_EPI_WARPS / 4);   // columns of a tile per epilogue warp
+constexpr int NTHREADS = 32 * (4 + NUM_EPI_WARPS);
 constexpr int EPI_WARP0 = 4;
-constexpr int NUM_EPI_WARPS = 8;
 
 
 struct Args {
   const float* row_img;   // [row tiles][2][BM*DK]
   const float* col_img;   // [col tiles][2][BN*DK]
-  const float* v_img;     // [col tiles][2][TN*BN]
+  const void* v_img;      // [col tiles][32 x 64] [V1 | V2] (fp16 or tf32)
+  const float* inv_vscale; // [TN] 2^-s_c (fp16 image scaling)
   int DK;
   int64_t n_rows, n_cols;
   int row_tiles, col_tiles, splits, tiles_per_split;
@@ -58,7 +74,15 @@ struct Args {
   int64_t split_stride;   // 0 = final output
   int chunk;              // column tiles per O flush
   int lookahead;          // distance MMAs issued this many tiles ahead (<= nstages - 1)
+  long long* prof;        // optional per-warp wait counters (GP_TC_PROF=1, diagnostic)
 };
+
+#define TC_T(slot, ...)                                   \
+  do {                                                    \
+    const long long _t0 = a.prof ? clock64() : 0;         \
+    __VA_ARGS__;                                          \
+    if (a.prof) tacc[slot] += clock64() - _t0;            \
+  } while (0)
 
 // ---------------------------------------------------------------------------
 // image preparation (fp64 arithmetic, tf32 hi/lo split)
@@ -118,35 +142,20 @@ __global__ void points_image_kernel(const float* __restrict__ X, int64_t ldx, in
   }
 }
 
-// V image: per column tile, element (n = rhs, k = column within tile), R = TN
-__global__ void v_image_kernel(const float* __restrict__ V, int64_t ldv, int t, int64_t ncols,
-                               float* img, int64_t ntiles) {
-  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= ntiles * BN * TN) return;
-  int64_t tile = idx / (BN * TN);
-  int rem = (int)(idx - tile * BN * TN);
-  int k = rem / TN, nn = rem - k * TN;  // consecutive threads: consecutive rhs of one column
-  int64_t col = tile * BN + k;
-  float v = (col < ncols && nn < t) ? V[col * ldv + nn] : 0.f;
-  float h = tf32_rna(v);
-  float* base = img + tile * 2 * BN * TN;
-  base[canon(nn, k, TN)] = h;
-  base[BN * TN + canon(nn, k, TN)] = v - h;
-}
-
 // ---------------------------------------------------------------------------
 // the fused kernel
 //   TMEM: S_0..2 (3 x 64 cols, distance accumulators, 2 tiles of look-ahead),
 //         K_0..1 (hi 64 + lo 64 cols each, contraction A operand),
-//         O_0..1 (16 cols each, flushed to registers every CHUNK tiles).
+//         O_0..1 (32 cols each = [K_hi V_hi + K_lo V_hi | K_hi V_lo]).
 //   Barriers: full/empty (SMEM ring), s_full[3] (MMA -> epilogue),
 //   k_full[2] (epilogue -> MMA), k_empty[2] (MMA -> epilogue, contraction
 //   done reading K), o_full/o_empty[2], xr_full/xr_empty (row image).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t TMS(uint32_t b) { return b * 64; }           // 0, 64, 128
+// K buffer b: tf32 hi [192 + 128b, +64) | lo [+64, +128); fp16 pairs K1 [.., +32) | K2 [+32, +64)
 __device__ __forceinline__ uint32_t TMKH(uint32_t b) { return 192 + b * 128; }   // 192, 320
-__device__ __forceinline__ uint32_t TMKL(uint32_t b) { return 256 + b * 128; }   // 256, 384
-__device__ __forceinline__ uint32_t TMO(uint32_t c) { return 448 + c * 16; }     // 448, 464
+__device__ __forceinline__ uint32_t TMKL(uint32_t b) { return (KV_F16 ? 224 : 256) + b * 128; }
+__device__ __forceinline__ uint32_t TMO(uint32_t c) { return 448 + c * 32; }     // 448, 480
 
 template <int FAM>
 __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
@@ -154,7 +163,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
   const int DK = a.DK;
   const uint32_t row_bytes = 2u * BM * DK * 4u;
   const uint32_t col_bytes = 2u * BN * DK * 4u;
-  const uint32_t v_bytes = 2u * TN * BN * 4u;
+  const uint32_t v_bytes = V_TILE;
   const uint32_t stage_bytes = col_bytes + v_bytes;
   const int NS = a.nstages;
   uint8_t* xr_s = smem;
@@ -179,7 +188,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
     }
     for (int b = 0; b < 3; ++b) mbar_init(smem_u32(&s_full[b]), 1);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(smem_u32(&k_full[b]), NUM_EPI_WARPS);
+      mbar_init(smem_u32(&k_full[b]), NUM_EPI_WARPS / 2);
       mbar_init(smem_u32(&k_empty[b]), 1);
       mbar_init(smem_u32(&o_full[b]), 1);
       mbar_init(smem_u32(&o_empty[b]), 4);
@@ -196,6 +205,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const long long t_start = clock64();
 
   const int n_items = a.row_tiles * a.splits;
 
@@ -211,7 +222,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
         mbar_expect_tx(smem_u32(xr_full), row_bytes);
         bulk_g2s(smem_u32(xr_s), a.row_img + (int64_t)rt * (row_bytes / 4), row_bytes, smem_u32(xr_full));
         const float* cimg = a.col_img + (int64_t)ct0 * (col_bytes / 4);
-        const float* vimg = a.v_img + (int64_t)ct0 * (v_bytes / 4);
+        const uint8_t* vimg = static_cast<const uint8_t*>(a.v_img) + (int64_t)ct0 * v_bytes;
         for (int ct = ct0; ct < ct1; ++ct) {
           mbar_wait(smem_u32(&empty[s]), ph ^ 1);
           uint8_t* st = stages + s * stage_bytes;
@@ -219,7 +230,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
           bulk_g2s(smem_u32(st), cimg, col_bytes, smem_u32(&full[s]));
           bulk_g2s(smem_u32(st + col_bytes), vimg, v_bytes, smem_u32(&full[s]));
           cimg += col_bytes / 4;
-          vimg += v_bytes / 4;
+          vimg += v_bytes;
           if (++s == (uint32_t)NS) { s = 0; ph ^= 1; }
         }
       }
@@ -231,10 +242,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
     // Descriptors are built once; per-MMA work is a 32-bit add on the
     // start-address field (addresses advance in 16-byte units).
     const uint32_t idesc_d = make_idesc(BM, BN);
-    const uint32_t idesc_c = make_idesc(BM, TN);
-    const uint32_t lbo_a = (BM / 8) * 128, lbo_b = (BN / 8) * 128, lbo_v = (TN / 8) * 128;
+    const uint32_t idesc_c32 = KV_F16 ? idesc_f16(BM, 2 * TN) : make_idesc(BM, 2 * TN);
+    const uint32_t idesc_c16 = KV_F16 ? idesc_f16(BM, TN) : make_idesc(BM, TN);
+    const uint32_t lbo_a = (BM / 8) * 128, lbo_b = (BN / 8) * 128, lbo_v = (2 * TN / 8) * 128;
     const uint32_t a_half16 = (BM * DK * 4) >> 4, b_half16 = (BN * DK * 4) >> 4;
-    const uint32_t v_half16 = (TN * BN * 4) >> 4;
     const int ksteps = DK / 8;
     const uint64_t da0 = make_desc(smem_u32(xr_s), lbo_a, 128);
     const uint64_t db0 = make_desc(smem_u32(stages), lbo_b, 128);
@@ -259,7 +270,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
       mbar_wait(smem_u32(xr_full), itc & 1);
       tc_fence_after();
       auto dist = [&]() {
-        mbar_wait(smem_u32(&full[ds]), dph);
+        TC_T(0, mbar_wait(smem_u32(&full[ds]), dph));
         tc_fence_after();
         const uint32_t d_tm = tmem + TMS(sb_next);
         const uint64_t db = db0 + (uint64_t)(ds * stage16);
@@ -283,22 +294,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
         // S buffer of tile jj+LA was last read by the epilogue for tile
         // jj+LA-3 <= jj-1, whose k_full we waited for already
         if (jj + LA < J) dist();
-        mbar_wait(smem_u32(&k_full[kb]), kph);
+        TC_T(1, mbar_wait(smem_u32(&k_full[kb]), kph));
+        tacc[7] += 1;
         tc_fence_after();
-        mbar_wait(smem_u32(&o_empty[oc]), oph ^ 1);  // chunk = 1 tile
+        TC_T(2, mbar_wait(smem_u32(&o_empty[oc]), oph ^ 1));  // chunk = 1 tile
         tc_fence_after();
         const uint64_t vb = dv0 + (uint64_t)(cs * stage16);
         const uint32_t o_tm = tmem + TMO(oc);
         const uint32_t khi = tmem + TMKH(kb), klo = tmem + TMKL(kb);
         if (leader) {
-          // O = Klo.Vhi + Khi.Vlo + Khi.Vhi  (fresh accumulator every tile)
+          // O = K_hi.[V_hi | V_lo];  O[:, 0:16] += K_lo.V_hi  (fresh accumulator every tile)
+          if constexpr (KV_F16) {
 #pragma unroll
-          for (int pass = 0; pass < 3; ++pass) {
-            const uint32_t ka = pass == 0 ? klo : khi;
-            const uint64_t vp = vb + (pass == 1 ? v_half16 : 0u);
+            for (int ks = 0; ks < BN / 16; ++ks)
+              mma16_ts(o_tm, khi + ks * 8, vb + (uint64_t)(ks * kstep_v16), idesc_c32, ks != 0);
+#pragma unroll
+            for (int ks = 0; ks < BN / 16; ++ks)
+              mma16_ts(o_tm, klo + ks * 8, vb + (uint64_t)(ks * kstep_v16), idesc_c16, 1);
+          } else {
 #pragma unroll
             for (int ks = 0; ks < BN / 8; ++ks)
-              mma_ts(o_tm, ka + ks * 8, vp + (uint64_t)(ks * kstep_v16), idesc_c, (pass | ks) != 0);
+              mma_ts(o_tm, khi + ks * 8, vb + (uint64_t)(ks * kstep_v16), idesc_c32, ks != 0);
+#pragma unroll
+            for (int ks = 0; ks < BN / 8; ++ks)
+              mma_ts(o_tm, klo + ks * 8, vb + (uint64_t)(ks * kstep_v16), idesc_c16, 1);
           }
           tc_commit(smem_u32(&empty[cs]));
           tc_commit(smem_u32(&k_empty[kb]));
@@ -313,30 +332,36 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
       __syncwarp();
     }
   } else if (warp >= EPI_WARP0) {
-    // ===================== epilogue (8 warps) =====================
+    // ===================== epilogue (16 warps, two groups) =====================
+    // Group g = (warp - 4) / 8 takes the tiles of parity g (global tile count
+    // of this CTA), so one group's SFU phase overlaps the other's TMEM store /
+    // barrier tail; tile parity also selects the K and O buffers, so each
+    // group owns K[g], O[g]. Within a group two warps per TMEM lane quarter
+    // cover 32 columns each, in two 16-column chunks (register budget).
+    const int e = warp - EPI_WARP0;
+    const int g = e >> 3;                      // tile parity group
     const int q = warp & 3;                    // TMEM lane quarter
-    const int half = (warp - EPI_WARP0) >> 2;  // column half of the 64-col tile
+    const int half = (e >> 2) & 1;             // column half of the 64-col tile
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    uint32_t sb = 0, sph = 0;   // S buffer / phase
-    uint32_t kb = 0, kph = 0;   // K buffer / phase
-    uint32_t oc = 0, oph = 0;   // O buffer / phase of the next tile's product
+    uint32_t T = 0;                            // tiles seen by this CTA (both groups)
+    uint32_t kuse = 0, ouse = 0;               // uses of K[g] / O[g] by this group
     float acc[TN];
-    // Every tile's product O_t = K_t V_t lands in a fresh TMEM accumulator
-    // (tensor-core fp32 accumulation over long K is lossy); half-0 warps fold
-    // it into fp32 registers one tile later, when it is long complete.
+    float* comb = reinterpret_cast<float*>(tmem_slot + 4);   // [BM][TN] group-1 partials
+    // Every tile's product lands in a fresh TMEM accumulator (tensor-core fp32
+    // accumulation over long K is lossy); slice-0 warps fold it into fp32
+    // registers one group-tile later, when it is long complete.
     int pending = 0;
-    uint32_t pend_c = 0, pend_ph = 0;
     auto flush = [&]() {
-      mbar_wait(smem_u32(&o_full[pend_c]), pend_ph);
+      TC_T(2, mbar_wait(smem_u32(&o_full[g]), (ouse - 1) & 1));
       tc_fence_after();
-      uint32_t o[16];
-      tmem_ld16(tmem + lane_base + TMO(pend_c), o);
+      uint32_t o[32];
+      tmem_ld32(tmem + lane_base + TMO(g), o);
       tmem_wait_ld();
 #pragma unroll
-      for (int c = 0; c < TN; ++c) acc[c] += __uint_as_float(o[c]);
+      for (int c = 0; c < TN; ++c) acc[c] += __uint_as_float(o[c]) + __uint_as_float(o[c + TN]);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&o_empty[pend_c]));
+      if (lane == 0) mbar_arrive(smem_u32(&o_empty[g]));
       pending = 0;
     };
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
@@ -348,78 +373,110 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
       const int64_t diag_col = (a.self_offset >= 0 && my_row < a.n_rows) ? my_row + a.self_offset : -1000;
 #pragma unroll
       for (int c = 0; c < TN; ++c) acc[c] = 0.f;
-      int64_t e_diag = diag_col - ((int64_t)ct0 * BN + half * 32);
-      for (int jj = 0; jj < J; ++jj, e_diag -= BN) {
-        mbar_wait(smem_u32(&s_full[sb]), sph);
+      for (int jj = 0; jj < J; ++jj, ++T) {
+        if ((int)(T & 1) != g) continue;
+        const uint32_t sb = T % 3, sph = (T / 3) & 1;
+        TC_T(0, mbar_wait(smem_u32(&s_full[sb]), sph));
+        tacc[7] += 1;
         tc_fence_after();
-        uint32_t v[32];
-        tmem_ld32(tmem + lane_base + TMS(sb) + half * 32, v);
-        tmem_wait_ld();
-        // self-diagonal entry (same point on both sides): r2 = 0 exactly
-        if (__any_sync(0xffffffffu, e_diag >= 0 && e_diag < 32)) {
+        // K[g] was last read by this group's previous contraction
+        TC_T(1, mbar_wait(smem_u32(&k_empty[g]), (kuse & 1) ^ 1));
+        ++kuse;
+        tc_fence_after();
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (e == e_diag) v[e] = 0u;
-        }
-        uint32_t hi[32];
+        for (int sub = 0; sub < 2; ++sub) {
+          const int c0 = half * 32 + sub * EPI_COLS;
+          uint32_t v[EPI_COLS];
+          tmem_ld16(tmem + lane_base + TMS(sb) + c0, v);
+          tmem_wait_ld();
+          const int64_t e_diag = diag_col - ((int64_t)(ct0 + jj) * BN + c0);
+          // self-diagonal entry (same point on both sides): r2 = 0 exactly
+          if (__any_sync(0xffffffffu, e_diag >= 0 && e_diag < EPI_COLS)) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          float sv = __uint_as_float(v[e]);
-          float kap;
-          // clamps written as selects so NaN inputs propagate (the
-          // reference raises on non-finite blocks, partition.py:231-236)
-          if (FAM == GP_FAMILY_RBF) {
-            kap = ex2_approx(sv > 0.f ? 0.f : sv);  // S = -log2(e) r2 / 2
-          } else {
-            float u = sqrt_approx(sv < 0.f ? 0.f : sv);  // S = 3 r2, u = sqrt(3) r
-            float ex = ex2_approx(u * -kLog2e);
-            kap = fmaf(u, ex, ex);                       // (1 + sqrt3 r) e^{-sqrt3 r}
+            for (int k = 0; k < EPI_COLS; ++k)
+              if (k == e_diag) v[k] = 0u;
           }
-          uint32_t h = __float_as_uint(kap) & 0xFFFFE000u;
-          hi[e] = h;
-          v[e] = __float_as_uint(kap - __uint_as_float(h));
+#pragma unroll
+          for (int k = 0; k < EPI_COLS; ++k) {
+            float sv = __uint_as_float(v[k]);
+            float kap;
+            // clamps written as selects so NaN inputs propagate (the
+            // reference raises on non-finite blocks, partition.py:231-236)
+            if (FAM == GP_FAMILY_RBF) {
+              kap = ex2_approx(sv > 0.f ? 0.f : sv);  // S = -log2(e) r2 / 2
+            } else {
+              float u = sqrt_approx(sv < 0.f ? 0.f : sv);  // S = 3 r2, u = sqrt(3) r
+              float ex = ex2_approx(u * -kLog2e);
+              kap = fmaf(u, ex, ex);                       // (1 + sqrt3 r) e^{-sqrt3 r}
+            }
+            v[k] = __float_as_uint(kap);
+          }
+          if constexpr (KV_F16) {
+            uint32_t p1[EPI_COLS / 2], p2[EPI_COLS / 2];
+#pragma unroll
+            for (int k = 0; k < EPI_COLS / 2; ++k)
+              split_pair(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]), p1[k], p2[k]);
+            tmem_st8(tmem + lane_base + TMKH(g) + c0 / 2, p1);
+            tmem_st8(tmem + lane_base + TMKL(g) + c0 / 2, p2);
+          } else {
+            uint32_t hi[EPI_COLS];
+#pragma unroll
+            for (int k = 0; k < EPI_COLS; ++k) {
+              hi[k] = v[k] & 0xFFFFE000u;
+              v[k] = __float_as_uint(__uint_as_float(v[k]) - __uint_as_float(hi[k]));
+            }
+            tmem_st16(tmem + lane_base + TMKH(g) + c0, hi);
+            tmem_st16(tmem + lane_base + TMKL(g) + c0, v);
+          }
         }
-        // K buffer kb was last read by the contraction two tiles ago
-        mbar_wait(smem_u32(&k_empty[kb]), kph ^ 1);
-        tc_fence_after();
-        tmem_st32(tmem + lane_base + TMKH(kb) + half * 32, hi);
-        tmem_st32(tmem + lane_base + TMKL(kb) + half * 32, v);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&k_full[kb]));
+        if (lane == 0) mbar_arrive(smem_u32(&k_full[g]));
         if (half == 0) {
           if (pending) flush();
           pending = 1;
-          pend_c = oc;
-          pend_ph = oph;
+          ++ouse;
         }
-        if (++sb == 3) { sb = 0; sph ^= 1; }
-        if (++kb == 2) { kb = 0; kph ^= 1; }
-        if (++oc == 2) { oc = 0; oph ^= 1; }
       }
       if (half == 0) {
         if (pending) flush();
-        const int64_t row = my_row;
-        if (row < a.n_rows) {
-          float* dst = a.split_stride ? a.out + (int64_t)sp * a.split_stride + row * a.t
-                                      : a.out + row * a.ldo;
+        // combine the two groups' partial row sums (named barrier over the 8
+        // slice-0 warps of both groups)
+        if (g == 1) {
 #pragma unroll
-          for (int c = 0; c < TN; ++c) {
-            if (c < a.t) {
-              float r = acc[c];
-              if (!a.split_stride) {
-                r *= a.s2;
-                if (a.diag_offset >= 0) r = fmaf(a.noise, a.V[(row + a.diag_offset) * a.ldv + c], r);
+          for (int c = 0; c < TN; ++c) comb[(q * 32 + lane) * TN + c] = acc[c];
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (g == 0) {
+#pragma unroll
+          for (int c = 0; c < TN; ++c) acc[c] += comb[(q * 32 + lane) * TN + c];
+          const int64_t row = my_row;
+          if (row < a.n_rows) {
+            float* dst = a.split_stride ? a.out + (int64_t)sp * a.split_stride + row * a.t
+                                        : a.out + row * a.ldo;
+#pragma unroll
+            for (int c = 0; c < TN; ++c) {
+              if (c < a.t) {
+                float r = KV_F16 ? acc[c] * __ldg(&a.inv_vscale[c]) : acc[c];
+                if (!a.split_stride) {
+                  r *= a.s2;
+                  if (a.diag_offset >= 0) r = fmaf(a.noise, a.V[(row + a.diag_offset) * a.ldv + c], r);
+                }
+                dst[c] = r;
               }
-              dst[c] = r;
             }
           }
         }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
       }
     }
   }
 
+  if (a.prof && lane == 0) {
+    tacc[6] = clock64() - t_start;
+    for (int k = 0; k < 8; ++k) a.prof[((int64_t)blockIdx.x * (NTHREADS / 32) + warp) * 8 + k] = tacc[k];
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -448,9 +505,84 @@ int distance_images(const float* Xr, int64_t ldr, int64_t nr, const float* Xc, i
   return GP_OK;
 }
 
-int v_images(const float* V, int64_t ldv, int t, int64_t ncols, float* img, int64_t ntiles, cudaStream_t st) {
+// V image: per 64-point tile a 32-row K-major fp16 operand (canonical
+// no-swizzle layout, core = 8 rows x 8 halves): rows 0-15 V1 = fp16(2^s V),
+// rows 16-31 V2 = fp16(2^s V - V1), so one N = 32 MMA forms K1.V1 and K1.V2
+__global__ void v_image16_kernel(const float* __restrict__ V, int64_t ldv, int t, int64_t ncols,
+                                 const float* __restrict__ vscale, __half* img, int64_t ntiles) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= ntiles * BN * TN) return;
+  int64_t tile = idx / (BN * TN);
+  int rem = (int)(idx - tile * BN * TN);
+  int k = rem / TN, nn = rem - k * TN;
+  int64_t col = tile * BN + k;
+  float v = (col < ncols && nn < t) ? V[col * ldv + nn] * vscale[nn] : 0.f;
+  __half h1 = __float2half_rn(v);
+  __half h2 = __float2half_rn(v - __half2float(h1));
+  __half* base = img + tile * (2 * TN * BN);
+  base[canon16(nn, k, 2 * TN)] = h1;
+  base[canon16(TN + nn, k, 2 * TN)] = h2;
+}
+
+// V image for the contraction: per column tile a 32-row K-major tf32 operand,
+// rows 0-15 V_hi, rows 16-31 V_lo, so one N = 32 MMA forms K_hi.V_hi and K_hi.V_lo
+__global__ void v_image32_kernel(const float* __restrict__ V, int64_t ldv, int t, int64_t ncols, float* img,
+                                 int64_t ntiles) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= ntiles * BN * TN) return;
+  int64_t tile = idx / (BN * TN);
+  int rem = (int)(idx - tile * BN * TN);
+  int k = rem / TN, nn = rem - k * TN;
+  int64_t col = tile * BN + k;
+  float v = (col < ncols && nn < t) ? V[col * ldv + nn] : 0.f;
+  float h = tf32_rna(v);
+  float* base = img + tile * 2 * BN * TN;
+  base[canon(nn, k, 2 * TN)] = h;
+  base[canon(TN + nn, k, 2 * TN)] = v - h;
+}
+
+int v_images32(const float* V, int64_t ldv, int t, int64_t ncols, float* img, int64_t ntiles, cudaStream_t st) {
   int64_t tot = ntiles * BN * TN;
-  v_image_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(V, ldv, t, ncols, img, ntiles);
+  v_image32_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(V, ldv, t, ncols, img, ntiles);
+  GP_LAUNCH_CHECK();
+  return GP_OK;
+}
+
+int v_images16(const float* V, int64_t ldv, int t, int64_t ncols, const float* vscale, __half* img,
+               int64_t ntiles, cudaStream_t st) {
+  int64_t tot = ntiles * BN * TN;
+  v_image16_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(V, ldv, t, ncols, vscale, img, ntiles);
+  GP_LAUNCH_CHECK();
+  return GP_OK;
+}
+
+__global__ void v_colscale_kernel(const float* __restrict__ V, int64_t ldv, int64_t n, int t, float* vscale,
+                                  float* inv_vscale) {
+  __shared__ float mx[256];
+  const int c = blockIdx.x;
+  float m = 0.f;
+  if (c < t)
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = fmaxf(m, fabsf(V[i * ldv + c]));
+  mx[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) mx[threadIdx.x] = fmaxf(mx[threadIdx.x], mx[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int S = 0;
+    if (mx[0] > 0.f && mx[0] < INFINITY) {
+      int ex;
+      frexpf(mx[0], &ex);   // max < 2^ex
+      S = max(-100, min(100, 14 - ex));
+    }
+    vscale[c] = ldexpf(1.0f, S);
+    inv_vscale[c] = ldexpf(1.0f, -S);
+  }
+}
+
+int v_colscale(const float* V, int64_t ldv, int64_t n, int t, float* vscale, float* inv_vscale, cudaStream_t st) {
+  v_colscale_kernel<<<TN, 256, 0, st>>>(V, ldv, n, t, vscale, inv_vscale);
   GP_LAUNCH_CHECK();
   return GP_OK;
 }
@@ -476,12 +608,13 @@ static Plan make_plan(const gp_kv_desc* d, int t) {
   p.splits = (p.col_tiles + p.tiles_per_split - 1) / p.tiles_per_split;
   p.row_img_bytes = (size_t)p.row_tiles * 2 * BM * p.DK * 4;
   p.col_img_bytes = (size_t)p.col_tiles * 2 * BN * p.DK * 4;
-  p.v_img_bytes = (size_t)p.col_tiles * 2 * BN * TN * 4;
-  p.split_bytes = (p.splits > 1 ? (size_t)p.splits * d->n_rows * t * 4 : 0) + 256 * sizeof(double);
-  size_t row_b = 2u * BM * p.DK * 4, stage_b = 2u * BN * p.DK * 4 + 2u * TN * BN * 4;
-  size_t budget = 220 * 1024 - row_b - 256;
+  p.v_img_bytes = (size_t)p.col_tiles * V_TILE;
+  p.split_bytes = (p.splits > 1 ? (size_t)p.splits * d->n_rows * t * 4 : 0) + 256 * sizeof(double) +
+                  2 * TN * sizeof(float);
+  size_t row_b = 2u * BM * p.DK * 4, stage_b = 2u * BN * p.DK * 4 + V_TILE;
+  size_t budget = 220 * 1024 - row_b - 256 - BM * TN * 4;
   p.nstages = (int)std::min<size_t>(4, budget / stage_b);
-  p.smem = row_b + p.nstages * stage_b + 256;
+  p.smem = row_b + p.nstages * stage_b + 256 + BM * TN * 4;
   return p;
 }
 
@@ -512,18 +645,26 @@ int kv_tc(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out
   char* w = static_cast<char*>(ws);
   float* row_img = reinterpret_cast<float*>(w); w += align256(p.row_img_bytes);
   float* col_img = reinterpret_cast<float*>(w); w += align256(p.col_img_bytes);
-  float* v_img = reinterpret_cast<float*>(w); w += align256(p.v_img_bytes);
+  void* v_img = w; w += align256(p.v_img_bytes);
   double* mean = reinterpret_cast<double*>(w); w += 256 * sizeof(double);
+  float* vscale = reinterpret_cast<float*>(w); w += TN * sizeof(float);
+  float* inv_vscale = reinterpret_cast<float*>(w); w += TN * sizeof(float);
   float* split_ws = reinterpret_cast<float*>(w);
   const double c = desc->family == GP_FAMILY_RBF ? 1.4426950408889634 : -6.0;
   {
     if (int rc = distance_images(desc->Xr, desc->ldr, desc->n_rows, desc->Xc, desc->ldc, desc->n_cols,
                                  desc->d, p.DK, BM, BN, c, mean, row_img, col_img, st))
       return rc;
-    if (int rc = v_images(V, ldv, t, desc->n_cols, v_img, p.col_tiles, st)) return rc;
+    if (KV_F16) {
+      if (int rc = v_colscale(V, ldv, desc->n_cols, t, vscale, inv_vscale, st)) return rc;
+      if (int rc = v_images16(V, ldv, t, desc->n_cols, vscale, static_cast<__half*>(v_img), p.col_tiles, st))
+        return rc;
+    } else if (int rc = v_images32(V, ldv, t, desc->n_cols, static_cast<float*>(v_img), p.col_tiles, st)) {
+      return rc;
+    }
   }
   Args a;
-  a.row_img = row_img; a.col_img = col_img; a.v_img = v_img; a.DK = p.DK;
+  a.row_img = row_img; a.col_img = col_img; a.v_img = v_img; a.inv_vscale = inv_vscale; a.DK = p.DK;
   a.n_rows = desc->n_rows; a.n_cols = desc->n_cols;
   a.row_tiles = p.row_tiles; a.col_tiles = p.col_tiles; a.splits = p.splits;
   a.tiles_per_split = p.tiles_per_split; a.nstages = p.nstages; a.fam = desc->family; a.t = t;
@@ -541,8 +682,25 @@ int kv_tc(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out
   int grid = std::min(items, num_sms());
   auto kern = desc->family == GP_FAMILY_RBF ? kv_tc_kernel<GP_FAMILY_RBF> : kv_tc_kernel<GP_FAMILY_MATERN32>;
   GP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+  a.prof = nullptr;
+  const char* pe = getenv("GP_TC_PROF");
+  if (pe && *pe == '1') GP_CUDA_TRY(cudaMalloc(&a.prof, (size_t)grid * (NTHREADS / 32) * 8 * sizeof(long long)));
   kern<<<grid, NTHREADS, p.smem, st>>>(a);
   GP_LAUNCH_CHECK();
+  if (a.prof) {   // diagnostic only: per-role average wait cycles per tile
+    std::vector<long long> h((size_t)grid * (NTHREADS / 32) * 8);
+    GP_CUDA_TRY(cudaStreamSynchronize(st));
+    GP_CUDA_TRY(cudaMemcpy(h.data(), a.prof, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+    cudaFree(a.prof);
+    for (int wi : {1, 4, 5, 8, 12}) {
+      double s[8] = {0};
+      for (int cta = 0; cta < grid; ++cta)
+        for (int k = 0; k < 8; ++k) s[k] += (double)h[((size_t)cta * (NTHREADS / 32) + wi) * 8 + k];
+      fprintf(stderr, "[tc prof] warp %d:", wi);
+      for (int k = 0; k < 8; ++k) fprintf(stderr, " w%d=%.0f", k, k == 7 ? s[7] / grid : s[k] / std::max(1.0, s[7]));
+      fprintf(stderr, "\n");
+    }
+  }
   if (p.splits > 1) {
     return launch_split_reduce(split_ws, p.splits, a.split_stride, desc->n_rows, t, out, ldo, a.s2,
                                a.noise, V, ldv, desc->diag_offset, st);

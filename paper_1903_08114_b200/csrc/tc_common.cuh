@@ -4,6 +4,8 @@
 
 #include "gp_common.cuh"
 
+#include <cuda_fp16.h>
+
 namespace gp {
 namespace tc {
 
@@ -152,12 +154,62 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float(y);
 }
 
+// instruction descriptor, kind::f16 with fp16 A/B, fp32 D, K-major both
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma16_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+// 16 lanes x 256 bits, x4 (32 columns): register r of thread t lands in lane
+// t/4 + 8((r>>1)&1), column 8(r>>2) + 2(t%4) + (r&1)
+__device__ __forceinline__ void tmem_st16x256_x4(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+// fp16 split of a pair: K1 = K truncated to 11 significant bits, K2 = fp16(K - K1)
+__device__ __forceinline__ void split_pair(float a, float b, uint32_t& k1, uint32_t& k2) {
+  const float a1 = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
+  const float b1 = __uint_as_float(__float_as_uint(b) & 0xFFFFE000u);
+  __half2 h1 = __floats2half2_rn(a1, b1);
+  __half2 h2 = __floats2half2_rn(a - a1, b - b1);
+  k1 = *reinterpret_cast<uint32_t*>(&h1);
+  k2 = *reinterpret_cast<uint32_t*>(&h2);
+}
+
+// canonical K-major no-swizzle offset (halves) of element (r, k) in an R-row
+// 16-bit tile: core matrix = 8 rows x 8 halves (16 B)
+__host__ __device__ __forceinline__ int canon16(int r, int k, int R) {
+  return (((k >> 3) * (R >> 3) + (r >> 3)) << 6) + ((r & 7) << 3) + (k & 7);
+}
 
 int distance_images(const float* Xr, int64_t ldr, int64_t nr, const float* Xc, int64_t ldc, int64_t nc,
                     int d, int DK, int BMr, int BNc, double c, double* mean, float* row_img,
                     float* col_img, cudaStream_t st);
-// V image for the contraction: per 64-column tile, 16 RHS x 64 columns, tf32 hi | lo
-int v_images(const float* V, int64_t ldv, int t, int64_t ncols, float* img, int64_t ntiles, cudaStream_t st);
+// fp16 V image for the contraction: per 64-point tile a 32-row K-major operand,
+// rows 0-15 V1 = fp16(2^s_c V), rows 16-31 V2 = fp16(2^s_c V - V1)
+int v_images16(const float* V, int64_t ldv, int t, int64_t ncols, const float* vscale, __half* img,
+               int64_t ntiles, cudaStream_t st);
+// tf32 V image: per 64-point tile a 32-row K-major operand [V_hi | V_lo]
+int v_images32(const float* V, int64_t ldv, int t, int64_t ncols, float* img, int64_t ntiles, cudaStream_t st);
+// per-column power-of-two scales 2^s_c with 2^s_c max|V_c| <= 2^14 (fp16 range) and their inverses
+int v_colscale(const float* V, int64_t ldv, int64_t n, int t, float* vscale, float* inv_vscale, cudaStream_t st);
 
 }  // namespace tc
 }  // namespace gp

@@ -141,6 +141,10 @@ int probe2() {
   return bad ? 2 : 0;
 }
 
+__device__ __forceinline__ void mma16_probe(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d), "r"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
+}
 // latency of MMA groups (issue -> commit arrival), single CTA, nothing else running
 __global__ void probe_lat(long long* out) {
   __shared__ __align__(1024) float bs[2 * 16 * 128 + 2 * 64 * 32];
@@ -190,13 +194,28 @@ __global__ void probe_lat(long long* out) {
     const uint64_t dv = make_desc(smem_u32(bs), 256, 128);
     const bool leader = elect_one();
     uint32_t ph = 0;
-    for (int test = 6; test < 9; ++test) {
-      for (int rep = 0; rep < 3; ++rep) {
+    for (int test = 6; test < 14; ++test) {
+      for (int rep = 0; rep < 6; ++rep) {
         long long t0 = clock64();
         if (leader) {
           if (test == 6) {
 #pragma unroll
             for (int k = 0; k < 24; ++k) mma_ts(tmem + 448, tmem + 128 + (k % 8) * 8, dv + (k % 8) * 32, make_idesc(128, 16), k > 0);
+          } else if (test == 9) {
+#pragma unroll
+            for (int k = 0; k < 24; ++k) mma16_probe(tmem + 256, tmem + 128 + (k % 4) * 8, dv + (k % 4) * 64, (1u << 4) | (4u << 17) | (8u << 24), k > 0);
+          } else if (test == 10) {
+#pragma unroll
+            for (int k = 0; k < 24; ++k) mma16_probe(tmem + 256, tmem + 128 + (k % 4) * 8, dv + (k % 4) * 64, (1u << 4) | (2u << 17) | (8u << 24), k > 0);
+          } else if (test == 11) {
+#pragma unroll
+            for (int k = 0; k < 24; ++k) mma_ss(tmem + 256, dv + (k % 2) * 32, dv + (k % 2) * 32, make_idesc(128, 64), k > 0);
+          } else if (test == 12) {
+#pragma unroll
+            for (int k = 0; k < 24; ++k) mma_ts(tmem + 256, tmem + 128 + (k % 2) * 8, dv + (k % 2) * 32, make_idesc(128, 64), k > 0);
+          } else if (test == 13) {
+#pragma unroll
+            for (int k = 0; k < 24; ++k) mma_ts(tmem + 256, tmem + 128 + (k % 2) * 8, dv + (k % 2) * 32, make_idesc(128, 128), k > 0);
           } else if (test == 7) {
 #pragma unroll
             for (int k = 0; k < 48; ++k) mma_ts(tmem + 480, tmem + 256 + (k % 16) * 8, dv + (k % 8) * 32, make_idesc(64, 16), (k % 16) > 0);
@@ -225,9 +244,6 @@ __global__ void probe_lat(long long* out) {
 
 // kind::f16 TS: A (fp16 pairs packed per 32-bit TMEM column, low half = even k),
 // B fp16 canonical K-major (core = 8 rows x 8 halves), M = 128 and M = 64 (lane 16)
-__device__ __host__ inline int canon16(int r, int k, int R) {
-  return (((k >> 3) * (R >> 3) + (r >> 3)) << 6) + ((r & 7) << 3) + (k & 7);
-}
 __global__ void probe_f16(float* out) {
   __shared__ __align__(1024) __half bs[32 * 64];
   __shared__ uint64_t bar;
@@ -338,12 +354,14 @@ int main() {
     cudaMalloc(&d, 64 * 8);
     probe_lat<<<1, 128>>>(d);
     if (cudaDeviceSynchronize() != cudaSuccess) { printf("lat CUDA error\n"); return 1; }
-    long long h[18];
+    long long h[28];
     cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
-    const char* nm[9] = {"24x TS M128 N16 K8", "48x TS M64 N16 K8 (lanes 0/16)", "6x TS M128 N64 K8",
+    const char* nm[14] = {"24x TS M128 N16 K8", "48x TS M64 N16 K8 (lanes 0/16)", "6x TS M128 N64 K8",
                          "48x SS M64 N16 K8", "48x TS M64 N16 K8 (lanes 0)", "48x TS M128 N16 K8",
-                         "uniform 24x TS M128 N16", "uniform 48x TS M64 N16", "uniform 24x TS M128 N256"};
-    for (int i = 0; i < 9; ++i) printf("%-34s issue %lld cyc, complete %lld cyc\n", nm[i], h[2 * i], h[2 * i + 1]);
+                         "uniform 24x TS M128 N16", "uniform 48x TS M64 N16", "uniform 24x TS M128 N256",
+                         "uniform 24x f16 TS M128 N32 K16", "uniform 24x f16 TS M128 N16 K16",
+                         "uniform 24x tf32 SS M128 N64", "uniform 24x tf32 TS M128 N64", "uniform 24x tf32 TS M128 N128"};
+    for (int i = 0; i < 14; ++i) printf("%-34s issue %lld cyc, complete %lld cyc\n", nm[i], h[2 * i], h[2 * i + 1]);
   }
   if (int r = probe2()) return r;
   float* d;
