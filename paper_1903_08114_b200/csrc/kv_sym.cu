@@ -50,9 +50,12 @@ using namespace gp::tc;
 constexpr int BM = 128;   // rows per tile (UMMA M of the direct product)
 constexpr int BN = 64;    // columns per tile (UMMA M of the mirror product)
 constexpr int TN = 16;    // right-hand sides
-constexpr int NTHREADS = 384;
-constexpr int EPI_WARP0 = 4;
-constexpr int NUM_EPI_WARPS = 8;
+// warp roles: 0 TMA, 1 MMA, 2 TMEM allocator, 3 idle, 4-11 kappa (S -> K),
+// 12-15 transpose (kappa^T -> TMEM, row image), 16-19 drain (O_I, O_J)
+constexpr int KAPPA_WARP0 = 4, NUM_KAPPA_WARPS = 8;
+constexpr int TRANS_WARP0 = KAPPA_WARP0 + NUM_KAPPA_WARPS;
+constexpr int DRAIN_WARP0 = TRANS_WARP0 + 4;
+constexpr int NTHREADS = 32 * (DRAIN_WARP0 + 4);
 // fp32 kappa^T staging tile in SMEM (double buffered): element (j, i) at
 // j * KT_LD + (i ^ 2(j & 1)). Producers (lane = i) store conflict-free; the
 // 136-float row stride plus the pair swizzle makes the consumers' 8-byte
@@ -170,18 +173,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(stages + NS * stage_bytes);
   uint64_t* full = bars;             // [NS]  TMA -> MMA
   uint64_t* empty = bars + NS;       // [NS]  MMA -> TMA
-  uint64_t* s_full = bars + 2 * NS;  // [2]   distance tile landed in SK buffer b
-  uint64_t* k_empty = s_full + 2;    // [2]   direct product done reading K in SK buffer b
-  uint64_t* o_full = k_empty + 2;    // [2]   direct product done
-  uint64_t* o_empty = o_full + 2;    // [2]   O_I read
-  uint64_t* oj_full = o_empty + 2;   // [2]   mirror product done
-  uint64_t* oj_empty = oj_full + 2;  // [2]   O_J read
-  uint64_t* k_full = oj_empty + 2;   // K written over S
-  uint64_t* kt_full = k_full + 1;    // K^T written
-  uint64_t* kt_empty = kt_full + 1;  // mirror product done reading K^T
-  uint64_t* xr_full = kt_empty + 1;  // row image + V_I landed
-  uint64_t* xr_empty = xr_full + 1;  // item's products done with them
-  uint64_t* xa_full = xr_empty + 1;  // row image copied into TMEM
+  uint64_t* s_full = bars + 2 * NS;  // [2]   distance tile landed in SK buffer b      (MMA -> kappa)
+  uint64_t* k_empty = s_full + 2;    // [2]   direct product done reading SK buffer b  (MMA -> MMA)
+  uint64_t* k_full = k_empty + 2;    // [2]   K written over S in SK buffer b          (kappa -> MMA)
+  uint64_t* o_full = k_full + 2;     // [2]   direct product done                      (MMA -> drain)
+  uint64_t* o_empty = o_full + 2;    // [2]   O_I read                                 (drain -> MMA)
+  uint64_t* oj_full = o_empty + 2;   // [2]   mirror product done                      (MMA -> drain)
+  uint64_t* oj_empty = oj_full + 2;  // [2]   O_J read                                 (drain -> MMA)
+  uint64_t* ts_full = oj_empty + 2;  // [2]   kappa^T staged in SMEM buffer            (kappa -> transpose)
+  uint64_t* ts_empty = ts_full + 2;  // [2]   SMEM buffer consumed                     (transpose -> kappa)
+  uint64_t* kt_full = ts_empty + 2;  // K^T written to TMEM                            (transpose -> MMA)
+  uint64_t* kt_empty = kt_full + 1;  // mirror product done reading K^T                (MMA -> transpose)
+  uint64_t* xr_full = kt_empty + 1;  // row image + V_I landed                         (TMA -> MMA, transpose)
+  uint64_t* xr_empty = xr_full + 1;  // item's products done with them                 (MMA -> TMA)
+  uint64_t* xa_full = xr_empty + 1;  // row image copied into TMEM                     (transpose -> MMA)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xa_full + 1);
   int* expo_s = reinterpret_cast<int*>(tmem_slot + 4);   // [TN] fixed-point exponents
 
@@ -195,13 +200,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
     for (int q = 0; q < 2; ++q) {
       mbar_init(smem_u32(&s_full[q]), 1);
       mbar_init(smem_u32(&k_empty[q]), 1);
+      mbar_init(smem_u32(&k_full[q]), NUM_KAPPA_WARPS);
       mbar_init(smem_u32(&o_full[q]), 1);
       mbar_init(smem_u32(&o_empty[q]), 4);
       mbar_init(smem_u32(&oj_full[q]), 1);
       mbar_init(smem_u32(&oj_empty[q]), 4);
+      mbar_init(smem_u32(&ts_full[q]), NUM_KAPPA_WARPS);
+      mbar_init(smem_u32(&ts_empty[q]), 4);
     }
-    mbar_init(smem_u32(k_full), NUM_EPI_WARPS);
-    mbar_init(smem_u32(kt_full), NUM_EPI_WARPS);
+    mbar_init(smem_u32(kt_full), 4);
     mbar_init(smem_u32(kt_empty), 1);
     mbar_init(smem_u32(xr_full), 1);
     mbar_init(smem_u32(xr_empty), 1);
@@ -252,8 +259,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    // per tile, in tensor-pipe order: direct(jj), mirror(jj), dist(jj+2); the
-    // distance tile jj+2 reuses the SK buffer of tile jj once direct(jj) is
+    // per tile, in tensor-pipe order: direct(T), mirror(T), dist(T+2); the
+    // distance tile T+2 reuses the SK buffer of tile T once direct(T) is
     // complete (the pipe does not order one MMA's TMEM-A reads against a
     // later MMA's D writes, so that is an explicit k_empty wait)
     const uint32_t idesc_d = make_idesc(BM, BN);
@@ -271,8 +278,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
     const uint32_t xa_hi = tmem + TMXA, xa_lo = tmem + TMXA + (uint32_t)DK;
     const uint32_t kt1 = tmem + TMKT, kt2 = tmem + (16u << 16) + TMKT;
     const bool leader = elect_one();
-    uint32_t ds = 0, dph = 0, cs = 0, dbuf = 0, keph0 = 0, keph1 = 0;
-    uint32_t kph = 0, ob = 0, oph = 0, ktph = 0, jb = 0, jph = 0;
+    uint32_t ds = 0, dph = 0, cs = 0, dbuf = 0, keph0 = 0, keph1 = 0, kfph0 = 0, kfph1 = 0;
+    uint32_t ob = 0, oph = 0, ktph = 0, jb = 0, jph = 0;
     uint32_t itc = 0;
     for (int r = 0;; ++r) {
       const int L = item_index(r, b, G);
@@ -293,7 +300,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
         tc_fence_after();
         const uint32_t d_tm = tmem + TMSK(dbuf);
         const uint64_t db = db0 + (uint64_t)(ds * stage16);
-        if (leader && !(a.skip & 4)) {
+        if (leader) {
 #pragma unroll
           for (int pass = 0; pass < 3; ++pass) {
             const uint32_t a_p = pass == 0 ? xa_lo : xa_hi;
@@ -301,8 +308,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
             for (int ks = 0; ks < ksteps; ++ks)
               mma_ts(d_tm, a_p + ks * 8, b_p + (uint64_t)(ks * kstep_b16), idesc_d, (pass | ks) != 0);
           }
-        }
-        if (leader) {
           tc_commit(smem_u32(&s_full[dbuf]));
         }
         __syncwarp();
@@ -313,14 +318,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       dist();
       if (J > 1) dist();
       for (int jj = 0; jj < J; ++jj) {
-        SYM_T(1, mbar_wait(smem_u32(k_full), kph));
+        uint32_t& kfph = kbuf ? kfph1 : kfph0;
+        SYM_T(1, mbar_wait(smem_u32(&k_full[kbuf]), kfph));
+        kfph ^= 1;
         tc_fence_after();
-        kph ^= 1;
         SYM_T(2, mbar_wait(smem_u32(&o_empty[ob]), oph ^ 1));
         tc_fence_after();
         const uint64_t vb = dv0 + (uint64_t)(cs * stage16);
         const uint32_t k1 = tmem + TMSK(kbuf) + 64, k2 = k1 + 32;
-        if (leader && !(a.skip & 2)) {
+        if (leader) {
           // direct: O_I[:, 0:32] = K1.[V1 | V2];  O_I[:, 0:16] += K2.V1  (K = 64 = 4 x 16)
 #pragma unroll
           for (int ks = 0; ks < BN / 16; ++ks)
@@ -328,8 +334,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
 #pragma unroll
           for (int ks = 0; ks < BN / 16; ++ks)
             mma16_ts(tmem + TMO(ob), k2 + ks * 8, vb + (uint64_t)(ks * kstep_v16), idesc_c16, 1);
-        }
-        if (leader) {
           tc_commit(smem_u32(&empty[cs]));
           tc_commit(smem_u32(&o_full[ob]));
           tc_commit(smem_u32(&k_empty[kbuf]));
@@ -347,7 +351,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
           tc_fence_after();
           tacc[7] += 1;
           const uint32_t oj1 = tmem + TMOJ(jb), oj2 = tmem + (16u << 16) + TMOJ(jb);
-          if (leader && !(a.skip & 1)) {
+          if (leader) {
 #pragma unroll
             for (int ks = 0; ks < BM / 16; ++ks)
               mma16_ts(oj1, kt1 + ks * 8, dvi + (uint64_t)((ks >> 2) * vtile16 + (ks & 3) * kstep_v16),
@@ -356,8 +360,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
             for (int ks = 0; ks < BM / 16; ++ks)
               mma16_ts(oj2, kt2 + ks * 8, dvi + (uint64_t)((ks >> 2) * vtile16 + (ks & 3) * kstep_v16),
                        idesc_m16, ks != 0);
-          }
-          if (leader) {
             tc_commit(smem_u32(kt_empty));
             tc_commit(smem_u32(&oj_full[jb]));
           }
@@ -372,62 +374,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       if (leader) tc_commit(smem_u32(xr_empty));
       __syncwarp();
     }
-  } else if (warp >= EPI_WARP0) {
-    // ===================== epilogue (8 warps) =====================
-    const int q = warp & 3;                    // TMEM lane quarter
-    const int half = (warp - EPI_WARP0) >> 2;  // column half of the 64-col tile
+  } else if (warp >= KAPPA_WARP0 && warp < TRANS_WARP0) {
+    // ===================== kappa warps (8): S -> K, kappa^T staging =====================
+    const int q = warp & 3;                        // TMEM lane quarter
+    const int half = (warp - KAPPA_WARP0) >> 2;    // column half of the 64-col tile
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const int i_loc = q * 32 + lane;
-    uint32_t sb = 0, sph = 0, ob = 0, oph = 0, jb = 0, jph = 0, ktph = 0, kbuf = 0;
-    uint32_t itc = 0, kf_tiles = 0;
-    float acc[TN];
-    int pending = 0;   // half 0: a direct product not yet folded into acc
-    int pendj = 0;     // half 1: a mirror product not yet drained
-    int64_t pendj_row0 = 0;
-    int ej[TN / 2];   // exponents of this lane's mirror columns (c0 = 0 or 8)
-#pragma unroll
-    for (int c = 0; c < TN / 2; ++c) ej[c] = expo_s[(lane < 16 ? 0 : TN / 2) + c];
-    auto flush = [&]() {  // half 0: fold the oldest direct product into registers
-      SYM_T(4, mbar_wait(smem_u32(&o_full[ob]), oph));
-      tc_fence_after();
-      uint32_t o[32];
-      tmem_ld32(tmem + lane_base + TMO(ob), o);
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&o_empty[ob]));
-      ob ^= 1;
-      if (ob == 0) oph ^= 1;
-#pragma unroll
-      for (int c = 0; c < TN; ++c) acc[c] += __uint_as_float(o[c]) + __uint_as_float(o[c + TN]);
-      pending = 0;
-    };
-    auto flushj = [&]() {  // half 1: oldest mirror product -> fixed-point sums
-      SYM_T(4, mbar_wait(smem_u32(&oj_full[jb]), jph));
-      tc_fence_after();
-      uint32_t o[32];
-      SYM_T(1, tmem_ld32(tmem + lane_base + TMOJ(jb), o); tmem_wait_ld());   // lanes 0-15: [1.V1 | 1.V2], 16-31: [2.V1 | -]
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&oj_empty[jb]));
-      jb ^= 1;
-      if (jb == 0) jph ^= 1;
-      float v[TN];
-#pragma unroll
-      for (int c = 0; c < TN; ++c) {
-        const float mine = lane < 16 ? __uint_as_float(o[c]) + __uint_as_float(o[c + TN]) : __uint_as_float(o[c]);
-        v[c] = mine + __shfl_xor_sync(0xffffffffu, mine, 16);
-      }
-      const int64_t row = pendj_row0 + q * 16 + (lane & 15);
-      if (row < a.n) {
-        const int c0 = lane < 16 ? 0 : TN / 2;
-#pragma unroll
-        for (int c = 0; c < TN / 2; ++c)
-          if (c0 + c < a.t)
-            contribute(a, row, c0 + c, lane < 16 ? v[c] : v[c + TN / 2], ej[c]);
-      }
-      pendj = 0;
-    };
+    uint32_t T = 0, m = 0;                         // tiles / mirrored tiles seen
     for (int r = 0;; ++r) {
       const int L = item_index(r, b, G);
       if (L >= a.n_items) break;
@@ -436,7 +389,78 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       const int J = it.ct1 - it.ct0;
       const int first_mirror = 2 * it.rt + 2 - it.ct0;
       const int64_t my_row = (int64_t)it.rt * BM + i_loc;
-      if (half == 0) {
+      for (int jj = 0; jj < J; ++jj, ++T) {
+        const bool mirror = jj >= first_mirror;
+        const uint32_t sb = T & 1;
+        SYM_T(0, mbar_wait(smem_u32(&s_full[sb]), (T >> 1) & 1));
+        tacc[7] += 1;
+        tc_fence_after();
+        const uint32_t sk = tmem + lane_base + TMSK(sb);
+        uint32_t v[32];
+        tmem_ld32(sk + half * 32, v);
+        tmem_wait_ld();
+        if (!mirror) {
+          const int64_t e_diag = my_row - ((int64_t)(it.ct0 + jj) * BN + half * 32);
+          if (__any_sync(0xffffffffu, e_diag >= 0 && e_diag < 32)) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (e == e_diag) v[e] = 0u;   // same point on both sides: r2 = 0 exactly
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          float sv = __uint_as_float(v[e]);
+          float kap;
+          if (FAM == GP_FAMILY_RBF) {
+            kap = ex2_approx(sv > 0.f ? 0.f : sv);  // S = -log2(e) r2 / 2
+          } else {
+            float u = sqrt_approx(sv < 0.f ? 0.f : sv);  // S = 3 r2, u = sqrt(3) r
+            float ex = ex2_approx(u * -kLog2e);
+            kap = fmaf(u, ex, ex);
+          }
+          v[e] = __float_as_uint(kap);
+        }
+#pragma unroll
+        for (int s16 = 0; s16 < 2; ++s16) {
+          uint32_t p1[8], p2[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            split_pair(__uint_as_float(v[16 * s16 + 2 * k]), __uint_as_float(v[16 * s16 + 2 * k + 1]), p1[k], p2[k]);
+          tmem_st8(sk + 64 + half * 16 + 8 * s16, p1);   // K over S, same buffer (own reads done)
+          tmem_st8(sk + 96 + half * 16 + 8 * s16, p2);
+        }
+        if (mirror) {
+          // kappa^T (fp32) for the transpose warps
+          const uint32_t mb = m & 1;
+          SYM_T(2, mbar_wait(smem_u32(&ts_empty[mb]), ((m >> 1) & 1) ^ 1));
+          float* ktb = kt32 + mb * (64 * KT_LD);
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            ktb[(32 * half + e) * KT_LD + (i_loc ^ ((e & 1) << 1))] = __uint_as_float(v[e]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&ts_full[mb]));
+          ++m;
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&k_full[sb]));
+      }
+    }
+  } else if (warp >= TRANS_WARP0 && warp < DRAIN_WARP0) {
+    // ===================== transpose warps (4): row image, K^T -> TMEM =====================
+    const int q = warp & 3;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const int i_loc = q * 32 + lane;
+    uint32_t itc = 0, m = 0, ktph = 0;
+    for (int r = 0;; ++r) {
+      const int L = item_index(r, b, G);
+      if (L >= a.n_items) break;
+      const Item it = item_of(a, L);
+      if (it.ct1 <= it.ct0) continue;
+      const int J = it.ct1 - it.ct0;
+      const int first_mirror = 2 * it.rt + 2 - it.ct0;
+      {
         // row image -> TMEM (A operand of the distance product)
         mbar_wait(smem_u32(xr_full), itc & 1);
         const float* xr = reinterpret_cast<const float*>(xr_s);
@@ -452,101 +476,106 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(xa_full));
+        ++itc;
       }
-      ++itc;
-#pragma unroll
-      for (int c = 0; c < TN; ++c) acc[c] = 0.f;
-      int64_t e_diag = my_row - ((int64_t)it.ct0 * BN + half * 32);
-      for (int jj = 0; jj < J; ++jj, e_diag -= BN) {
-        const bool mirror = jj >= first_mirror;
-        SYM_T(0, mbar_wait(smem_u32(&s_full[sb]), sph));
+      for (int jj = max(first_mirror, 0); jj < J; ++jj, ++m) {
+        const uint32_t mb = m & 1;
+        SYM_T(0, mbar_wait(smem_u32(&ts_full[mb]), (m >> 1) & 1));
         tacc[7] += 1;
+        SYM_T(1, mbar_wait(smem_u32(kt_empty), ktph ^ 1));   // previous mirror product done with K^T
+        ktph ^= 1;
         tc_fence_after();
-        const uint32_t sk = tmem + lane_base + TMSK(sb);
-        uint32_t v[32];
-        tmem_ld32(sk + half * 32, v);
-        tmem_wait_ld();
-        if (!mirror && __any_sync(0xffffffffu, e_diag >= 0 && e_diag < 32)) {
+        const float* ktb = kt32 + mb * (64 * KT_LD);
+        // register r of the 16x256b.x4 fragment -> K^T row j = 16q + lane/4 + 8((r>>1)&1),
+        // points i = 64 part + 16(r>>2) + 4(lane%4) + 2(r&1) and i + 1
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (e == e_diag) v[e] = 0u;   // same point on both sides: r2 = 0 exactly
-        }
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          float sv = __uint_as_float(v[e]);
-          float kap;
-          if (FAM == GP_FAMILY_RBF) {
-            kap = ex2_approx(sv > 0.f ? 0.f : sv);  // S = -log2(e) r2 / 2
-          } else {
-            float u = sqrt_approx(sv < 0.f ? 0.f : sv);  // S = 3 r2, u = sqrt(3) r
-            float ex = ex2_approx(u * -kLog2e);
-            kap = fmaf(u, ex, ex);
-          }
-          v[e] = __float_as_uint(kap);
-        }
-        float* ktb = kt32 + kbuf * (64 * KT_LD);
-        if (mirror) {
-          // kappa^T (fp32) for the transposition
-#pragma unroll
-          for (int e = 0; e < 32; ++e)
-            ktb[(32 * half + e) * KT_LD + (i_loc ^ ((e & 1) << 1))] = __uint_as_float(v[e]);
-        }
-        uint32_t p1[16], p2[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          split_pair(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]), p1[e], p2[e]);
-        tmem_st16(sk + 64 + half * 16, p1);
-        tmem_st16(sk + 96 + half * 16, p2);
-        if (half == 0 && pending) SYM_T(1, flush());   // direct product of the previous tile
-        tmem_wait_st();
-        tc_fence_before();
-        // k_full counts 8 arrivals per tile; a warp running a tile ahead must
-        // not arrive before the previous tile's phase completed
-        if (kf_tiles > 0) mbar_wait(smem_u32(k_full), (kf_tiles - 1) & 1);
-        ++kf_tiles;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(k_full));
-        if (half == 0) pending = 1;
-        if (mirror) {
-          SYM_T(2, asm volatile("bar.sync 1, 256;" ::: "memory"));   // every producer wrote ktb
-          SYM_T(3, mbar_wait(smem_u32(kt_empty), ktph ^ 1));        // previous mirror product done with K^T
-          ktph ^= 1;
-          tc_fence_after();
-          // consumer: register r -> row j = 16q + lane/4 + 8((r>>1)&1), points
-          // i = 64 half + 16(r>>2) + 4(lane%4) + 2(r&1) and i + 1
+        for (int part = 0; part < 2; ++part) {
           uint32_t w1[16], w2[16];
 #pragma unroll
-          for (int r = 0; r < 16; ++r) {
-            const int j = 16 * q + (lane >> 2) + 8 * ((r >> 1) & 1);
-            const int i = 64 * half + 16 * (r >> 2) + 4 * (lane & 3) + 2 * (r & 1);
+          for (int rr = 0; rr < 16; ++rr) {
+            const int j = 16 * q + (lane >> 2) + 8 * ((rr >> 1) & 1);
+            const int i = 64 * part + 16 * (rr >> 2) + 4 * (lane & 3) + 2 * (rr & 1);
             const float2 x = *reinterpret_cast<const float2*>(&ktb[j * KT_LD + (i ^ ((j & 1) << 1))]);
-            split_pair(x.x, x.y, w1[r], w2[r]);
+            split_pair(x.x, x.y, w1[rr], w2[rr]);
           }
-          tmem_st16x256_x4(tmem + lane_base + TMKT + 32 * half, w1);
-          tmem_st16x256_x4(tmem + lane_base + (16u << 16) + TMKT + 32 * half, w2);
-          tmem_wait_st();
+          tmem_st16x256_x4(tmem + lane_base + TMKT + 32 * part, w1);
+          tmem_st16x256_x4(tmem + lane_base + (16u << 16) + TMKT + 32 * part, w2);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&ts_empty[mb]));   // SMEM reads done
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(kt_full));
+      }
+    }
+  } else if (warp >= DRAIN_WARP0) {
+    // ===================== drain warps (4): O_I -> registers, O_J -> fixed point =====================
+    const int q = warp & 3;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const int i_loc = q * 32 + lane;
+    uint32_t ob = 0, oph = 0, jb = 0, jph = 0;
+    int ej[TN / 2];   // exponents of this lane's mirror columns (c0 = 0 or 8)
+#pragma unroll
+    for (int c = 0; c < TN / 2; ++c) ej[c] = expo_s[(lane < 16 ? 0 : TN / 2) + c];
+    float acc[TN];
+    for (int r = 0;; ++r) {
+      const int L = item_index(r, b, G);
+      if (L >= a.n_items) break;
+      const Item it = item_of(a, L);
+      if (it.ct1 <= it.ct0) continue;
+      const int J = it.ct1 - it.ct0;
+      const int first_mirror = 2 * it.rt + 2 - it.ct0;
+      const int64_t my_row = (int64_t)it.rt * BM + i_loc;
+#pragma unroll
+      for (int c = 0; c < TN; ++c) acc[c] = 0.f;
+      for (int jj = 0; jj < J; ++jj) {
+        {  // direct product of tile jj -> registers
+          SYM_T(0, mbar_wait(smem_u32(&o_full[ob]), oph));
+          tacc[7] += 1;
+          tc_fence_after();
+          uint32_t o[32];
+          tmem_ld32(tmem + lane_base + TMO(ob), o);
+          tmem_wait_ld();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(kt_full));
-          kbuf ^= 1;
-          if (half == 1) {
-            if (pendj) SYM_T(5, flushj());     // previous mirror product (other O_J buffer)
-            pendj = 1;
-            pendj_row0 = (int64_t)(it.ct0 + jj) * BN;
+          if (lane == 0) mbar_arrive(smem_u32(&o_empty[ob]));
+          ob ^= 1;
+          if (ob == 0) oph ^= 1;
+#pragma unroll
+          for (int c = 0; c < TN; ++c) acc[c] += __uint_as_float(o[c]) + __uint_as_float(o[c + TN]);
+        }
+        if (jj >= first_mirror) {  // mirror product of tile jj -> fixed-point sums
+          SYM_T(1, mbar_wait(smem_u32(&oj_full[jb]), jph));
+          tc_fence_after();
+          uint32_t o[32];
+          tmem_ld32(tmem + lane_base + TMOJ(jb), o);   // lanes 0-15: [1.V1 | 1.V2], 16-31: [2.V1 | -]
+          tmem_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&oj_empty[jb]));
+          jb ^= 1;
+          if (jb == 0) jph ^= 1;
+          float v[TN];
+#pragma unroll
+          for (int c = 0; c < TN; ++c) {
+            const float mine =
+                lane < 16 ? __uint_as_float(o[c]) + __uint_as_float(o[c + TN]) : __uint_as_float(o[c]);
+            v[c] = mine + __shfl_xor_sync(0xffffffffu, mine, 16);
+          }
+          const int64_t row = (int64_t)(it.ct0 + jj) * BN + q * 16 + (lane & 15);
+          if (row < a.n) {
+            const int c0 = lane < 16 ? 0 : TN / 2;
+#pragma unroll
+            for (int c = 0; c < TN / 2; ++c)
+              if (c0 + c < a.t) contribute(a, row, c0 + c, lane < 16 ? v[c] : v[c + TN / 2], ej[c]);
           }
         }
-        sb ^= 1;
-        if (sb == 0) sph ^= 1;
       }
-      if (half == 0) {
-        if (pending) flush();
-        if (my_row < a.n) {
+      if (my_row < a.n) {
 #pragma unroll
-          for (int c = 0; c < TN; ++c)
-            if (c < a.t) contribute(a, my_row, c, acc[c], expo_s[c]);
-        }
-      } else if (pendj) {
-        flushj();
+        for (int c = 0; c < TN; ++c)
+          if (c < a.t) contribute(a, my_row, c, acc[c], expo_s[c]);
       }
     }
   }
@@ -720,7 +749,7 @@ int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* ou
     GP_CUDA_TRY(cudaStreamSynchronize(st));
     GP_CUDA_TRY(cudaMemcpy(h.data(), a.prof, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
     cudaFree(a.prof);
-    for (int wi : {1, 4, 5, 8, 9}) {
+    for (int wi : {1, 4, 8, 12, 16}) {
       double s[8] = {0};
       for (int cta = 0; cta < grid; ++cta)
         for (int k = 0; k < 8; ++k) s[k] += (double)h[((size_t)cta * (NTHREADS / 32) + wi) * 8 + k];

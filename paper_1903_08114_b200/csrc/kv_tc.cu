@@ -75,6 +75,7 @@ struct Args {
   int chunk;              // column tiles per O flush
   int lookahead;          // distance MMAs issued this many tiles ahead (<= nstages - 1)
   long long* prof;        // optional per-warp wait counters (GP_TC_PROF=1, diagnostic)
+  int skip;               // diagnostic (GP_TC_SKIP): 1 contraction MMAs, 2 distance MMAs, 4 kappa math
 };
 
 #define TC_T(slot, ...)                                   \
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
         tc_fence_after();
         const uint32_t d_tm = tmem + TMS(sb_next);
         const uint64_t db = db0 + (uint64_t)(ds * stage16);
-        if (leader) {
+        if (leader && !(a.skip & 2)) {
 #pragma unroll
           for (int pass = 0; pass < 3; ++pass) {
             const uint64_t a_p = da0 + (pass == 0 ? a_half16 : 0u);
@@ -283,6 +284,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
               mma_ss(d_tm, a_p + (uint64_t)(ks * kstep_a16), b_p + (uint64_t)(ks * kstep_b16), idesc_d,
                      (pass | ks) != 0);
           }
+        }
+        if (leader) {
           tc_commit(smem_u32(&s_full[sb_next]));
         }
         __syncwarp();
@@ -302,7 +305,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
         const uint64_t vb = dv0 + (uint64_t)(cs * stage16);
         const uint32_t o_tm = tmem + TMO(oc);
         const uint32_t khi = tmem + TMKH(kb), klo = tmem + TMKL(kb);
-        if (leader) {
+        if (leader && !(a.skip & 1)) {
           // O = K_hi.[V_hi | V_lo];  O[:, 0:16] += K_lo.V_hi  (fresh accumulator every tile)
           if constexpr (KV_F16) {
 #pragma unroll
@@ -319,6 +322,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
             for (int ks = 0; ks < BN / 8; ++ks)
               mma_ts(o_tm, klo + ks * 8, vb + (uint64_t)(ks * kstep_v16), idesc_c16, 1);
           }
+        }
+        if (leader) {
           tc_commit(smem_u32(&empty[cs]));
           tc_commit(smem_u32(&k_empty[kb]));
           tc_commit(smem_u32(&o_full[oc]));
@@ -379,25 +384,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
         TC_T(0, mbar_wait(smem_u32(&s_full[sb]), sph));
         tacc[7] += 1;
         tc_fence_after();
-        // K[g] was last read by this group's previous contraction
-        TC_T(1, mbar_wait(smem_u32(&k_empty[g]), (kuse & 1) ^ 1));
-        ++kuse;
-        tc_fence_after();
-#pragma unroll
-        for (int sub = 0; sub < 2; ++sub) {
-          const int c0 = half * 32 + sub * EPI_COLS;
-          uint32_t v[EPI_COLS];
-          tmem_ld16(tmem + lane_base + TMS(sb) + c0, v);
-          tmem_wait_ld();
+        // this warp's 32 columns in one TMEM load (one round trip per tile)
+        const int c0 = half * 32;
+        uint32_t v[32];
+        tmem_ld32(tmem + lane_base + TMS(sb) + c0, v);
+        tmem_wait_ld();
+        {
           const int64_t e_diag = diag_col - ((int64_t)(ct0 + jj) * BN + c0);
           // self-diagonal entry (same point on both sides): r2 = 0 exactly
-          if (__any_sync(0xffffffffu, e_diag >= 0 && e_diag < EPI_COLS)) {
+          if (__any_sync(0xffffffffu, e_diag >= 0 && e_diag < 32)) {
 #pragma unroll
-            for (int k = 0; k < EPI_COLS; ++k)
+            for (int k = 0; k < 32; ++k)
               if (k == e_diag) v[k] = 0u;
           }
+        }
+        if (!(a.skip & 4)) {
 #pragma unroll
-          for (int k = 0; k < EPI_COLS; ++k) {
+          for (int k = 0; k < 32; ++k) {
             float sv = __uint_as_float(v[k]);
             float kap;
             // clamps written as selects so NaN inputs propagate (the
@@ -411,22 +414,32 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
             }
             v[k] = __float_as_uint(kap);
           }
-          if constexpr (KV_F16) {
-            uint32_t p1[EPI_COLS / 2], p2[EPI_COLS / 2];
+        }
+        // K[g] was last read by this group's previous contraction
+        TC_T(1, mbar_wait(smem_u32(&k_empty[g]), (kuse & 1) ^ 1));
+        ++kuse;
+        tc_fence_after();
+        if constexpr (KV_F16) {
 #pragma unroll
-            for (int k = 0; k < EPI_COLS / 2; ++k)
-              split_pair(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]), p1[k], p2[k]);
-            tmem_st8(tmem + lane_base + TMKH(g) + c0 / 2, p1);
-            tmem_st8(tmem + lane_base + TMKL(g) + c0 / 2, p2);
-          } else {
-            uint32_t hi[EPI_COLS];
+          for (int s16 = 0; s16 < 2; ++s16) {
+            uint32_t p1[8], p2[8];
 #pragma unroll
-            for (int k = 0; k < EPI_COLS; ++k) {
-              hi[k] = v[k] & 0xFFFFE000u;
-              v[k] = __float_as_uint(__uint_as_float(v[k]) - __uint_as_float(hi[k]));
+            for (int k = 0; k < 8; ++k)
+              split_pair(__uint_as_float(v[16 * s16 + 2 * k]), __uint_as_float(v[16 * s16 + 2 * k + 1]), p1[k], p2[k]);
+            tmem_st8(tmem + lane_base + TMKH(g) + c0 / 2 + 8 * s16, p1);
+            tmem_st8(tmem + lane_base + TMKL(g) + c0 / 2 + 8 * s16, p2);
+          }
+        } else {
+#pragma unroll
+          for (int s16 = 0; s16 < 2; ++s16) {
+            uint32_t hi[16], lo[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              hi[k] = v[16 * s16 + k] & 0xFFFFE000u;
+              lo[k] = __float_as_uint(__uint_as_float(v[16 * s16 + k]) - __uint_as_float(hi[k]));
             }
-            tmem_st16(tmem + lane_base + TMKH(g) + c0, hi);
-            tmem_st16(tmem + lane_base + TMKL(g) + c0, v);
+            tmem_st16(tmem + lane_base + TMKH(g) + c0 + 16 * s16, hi);
+            tmem_st16(tmem + lane_base + TMKL(g) + c0 + 16 * s16, lo);
           }
         }
         tmem_wait_st();
@@ -683,6 +696,7 @@ int kv_tc(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out
   auto kern = desc->family == GP_FAMILY_RBF ? kv_tc_kernel<GP_FAMILY_RBF> : kv_tc_kernel<GP_FAMILY_MATERN32>;
   GP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   a.prof = nullptr;
+  a.skip = getenv("GP_TC_SKIP") ? atoi(getenv("GP_TC_SKIP")) : 0;
   const char* pe = getenv("GP_TC_PROF");
   if (pe && *pe == '1') GP_CUDA_TRY(cudaMalloc(&a.prof, (size_t)grid * (NTHREADS / 32) * 8 * sizeof(long long)));
   kern<<<grid, NTHREADS, p.smem, st>>>(a);
