@@ -445,6 +445,10 @@ int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* ou
            void* ws, size_t ws_bytes, cudaStream_t st);
 size_t kv_sym_workspace(const gp_kv_desc* desc, int t);
 bool kv_sym_supported(const gp_kv_desc* desc, int t);
+int kv_wide(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out, int64_t ldo,
+            void* ws, size_t ws_bytes, cudaStream_t st);
+size_t kv_wide_workspace(const gp_kv_desc* desc, int t);
+bool kv_wide_supported(const gp_kv_desc* desc, int t);
 }  // namespace gp
 
 extern "C" {
@@ -465,8 +469,10 @@ size_t gp_kv_workspace_bytes(const gp_kv_desc* desc, int t) {
   size_t a = gp::kv_simt_workspace(desc, t);
   size_t b = gp_has_tcgen05() ? gp::kv_tc_workspace(desc, t) : 0;
   size_t c = gp_has_tcgen05() ? gp::kv_sym_workspace(desc, t) : 0;
+  size_t w = gp_has_tcgen05() ? gp::kv_wide_workspace(desc, t) : 0;
   a = a > b ? a : b;
-  return a > c ? a : c;
+  a = a > c ? a : c;
+  return a > w ? a : w;
 }
 
 int gp_kv(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out, int64_t ldo,
@@ -491,6 +497,8 @@ int gp_kv(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out
     GP_REQUIRE(gp::kv_sym_supported(desc, t), "gp_kv: shape unsupported by the symmetric tcgen05 kernel");
     return gp::kv_sym(desc, V, ldv, t, out, ldo, workspace, workspace_bytes, st);
   }
+  if (desc->algo != 1 && t > 16 && gp_has_tcgen05() && gp::kv_wide_supported(desc, t))
+    return gp::kv_wide(desc, V, ldv, t, out, ldo, workspace, workspace_bytes, st);
   if (use_tc(desc, t)) {
     GP_REQUIRE(gp_has_tcgen05(), "gp_kv: tcgen05 kernel requested but not compiled in");
     GP_REQUIRE(gp::kv_tc_supported(desc, t), "gp_kv: shape unsupported by the tcgen05 kernel");

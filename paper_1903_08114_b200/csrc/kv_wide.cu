@@ -1,0 +1,409 @@
+// Wide-RHS tcgen05 K·V kernel (16 < t <= 256) for sm_100a: the predictive-
+// variance solves (predictor.py:135-182 batches 256 test points per chunk)
+// and any caller with many right-hand sides.
+//
+// Same tile pipeline as kv_tc.cu (persistent CTA per SM, TMA producer warp,
+// one elected MMA-issuing thread, epilogue warps computing kappa on the SFU),
+// but the contraction has N = t_pad (up to 256) and is tensor-bound rather
+// than SFU-bound: per 128 x 64 tile, O += K1.V1 + K1.V2 + K2.V1 (kind::f16,
+// 2-term fp16 splits of K and of the column-scaled V, fp32 accumulation in
+// TMEM), 12 MMAs of N = t_pad. O (t_pad TMEM columns) accumulates over CH
+// column tiles and is then folded into the fp32 destination by the epilogue
+// warps (plain read-modify-write: each CTA owns its rows of its column split),
+// bounding the length of any TMEM accumulation chain (long TMEM accumulation
+// loses precision, measured in kv_tc.cu).
+//
+// Reference semantics: kernels.py:225-244 (kappa), :293-316 / :319-325 (rows
+// of K̂ / cross blocks), partition.py:224-241 (row-block products).
+#include "tc_common.cuh"
+
+#include <algorithm>
+
+namespace gp {
+namespace tw {
+
+using namespace gp::tc;
+
+constexpr int BM = 128;
+constexpr int BN = 64;
+constexpr int TMAX = 256;          // widest right-hand-side block
+constexpr int CH = 32;             // column tiles per TMEM accumulation chain
+constexpr int NUM_EPI_WARPS = 8;   // two per TMEM lane quarter, 32 columns of a tile each
+constexpr int NTHREADS = 32 * (4 + NUM_EPI_WARPS);
+
+struct Args {
+  const float* row_img;   // [row tiles][2][BM*DK]
+  const float* col_img;   // [col tiles][2][BN*DK]
+  const __half* v_img;    // [col tiles][2*NW x 64] fp16 [V1 | V2]
+  const float* inv_vscale;  // [t] 2^-s_c
+  int DK, NW;             // NW = t rounded up to 16
+  int64_t n_rows, n_cols;
+  int row_tiles, col_tiles, splits, tiles_per_split;
+  int nstages;
+  int t;
+  float s2, noise;
+  int64_t diag_offset, self_offset;
+  float* accw;            // [splits][NW][rows_pad] column-major fp32 partial sums
+  int64_t rows_pad;
+};
+
+// TMEM: S 2 x 64 | K1 32 + K2 32 (x2 buffers) | O NW (<= 256)
+__device__ __forceinline__ uint32_t TMS(uint32_t b) { return b * 64; }
+__device__ __forceinline__ uint32_t TMK1(uint32_t b) { return 128 + b * 64; }
+__device__ __forceinline__ uint32_t TMK2(uint32_t b) { return 160 + b * 64; }
+constexpr uint32_t TMO = 256;
+
+template <int FAM>
+__global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int DK = a.DK, NW = a.NW;
+  const uint32_t row_bytes = 2u * BM * DK * 4u;
+  const uint32_t col_bytes = 2u * BN * DK * 4u;
+  const uint32_t v_bytes = 2u * NW * BN * 2u;
+  const uint32_t stage_bytes = col_bytes + v_bytes;
+  const int NS = a.nstages;
+  uint8_t* xr_s = smem;
+  uint8_t* stages = smem + row_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + NS * stage_bytes);
+  uint64_t* full = bars;             // [NS]
+  uint64_t* empty = bars + NS;       // [NS]
+  uint64_t* s_full = bars + 2 * NS;  // [2]
+  uint64_t* k_full = s_full + 2;     // [2]
+  uint64_t* k_empty = k_full + 2;    // [2]
+  uint64_t* o_full = k_empty + 2;    // chunk accumulated
+  uint64_t* o_empty = o_full + 1;    // chunk folded into the destination
+  uint64_t* xr_full = o_empty + 1;
+  uint64_t* xr_empty = xr_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xr_empty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&s_full[b]), 1);
+      mbar_init(smem_u32(&k_full[b]), NUM_EPI_WARPS);
+      mbar_init(smem_u32(&k_empty[b]), 1);
+    }
+    mbar_init(smem_u32(o_full), 1);
+    mbar_init(smem_u32(o_empty), NUM_EPI_WARPS);
+    mbar_init(smem_u32(xr_full), 1);
+    mbar_init(smem_u32(xr_empty), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int n_items = a.row_tiles * a.splits;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      uint32_t s = 0, ph = 0, itc = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++itc) {
+        const int rt = it / a.splits, sp = it - rt * a.splits;
+        const int ct0 = sp * a.tiles_per_split;
+        const int ct1 = min(a.col_tiles, ct0 + a.tiles_per_split);
+        mbar_wait(smem_u32(xr_empty), (itc & 1) ^ 1);
+        mbar_expect_tx(smem_u32(xr_full), row_bytes);
+        bulk_g2s(smem_u32(xr_s), a.row_img + (int64_t)rt * (row_bytes / 4), row_bytes, smem_u32(xr_full));
+        const float* cimg = a.col_img + (int64_t)ct0 * (col_bytes / 4);
+        const uint8_t* vimg = reinterpret_cast<const uint8_t*>(a.v_img) + (int64_t)ct0 * v_bytes;
+        for (int ct = ct0; ct < ct1; ++ct) {
+          mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+          uint8_t* st = stages + s * stage_bytes;
+          mbar_expect_tx(smem_u32(&full[s]), stage_bytes);
+          bulk_g2s(smem_u32(st), cimg, col_bytes, smem_u32(&full[s]));
+          bulk_g2s(smem_u32(st + col_bytes), vimg, v_bytes, smem_u32(&full[s]));
+          cimg += col_bytes / 4;
+          vimg += v_bytes;
+          if (++s == (uint32_t)NS) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    const uint32_t idesc_d = make_idesc(BM, BN);
+    const uint32_t idesc_c = idesc_f16(BM, NW);
+    const uint32_t lbo_a = (BM / 8) * 128, lbo_b = (BN / 8) * 128, lbo_v = (2 * NW / 8) * 128;
+    const uint32_t a_half16 = (BM * DK * 4) >> 4, b_half16 = (BN * DK * 4) >> 4;
+    const uint32_t v2_16 = ((NW / 8) * 128) >> 4;   // V2 rows start NW/8 core rows down
+    const int ksteps = DK / 8;
+    const uint64_t da0 = make_desc(smem_u32(xr_s), lbo_a, 128);
+    const uint64_t db0 = make_desc(smem_u32(stages), lbo_b, 128);
+    const uint64_t dv0 = make_desc(smem_u32(stages + col_bytes), lbo_v, 128);
+    const uint32_t stage16 = stage_bytes >> 4;
+    const uint32_t kstep_a16 = (2 * lbo_a) >> 4, kstep_b16 = (2 * lbo_b) >> 4, kstep_v16 = (2 * lbo_v) >> 4;
+    const bool leader = elect_one();
+    uint32_t ds = 0, dph = 0, cs = 0, sbn = 0, kb = 0, kph = 0, oph = 0;
+    uint32_t itc = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++itc) {
+      const int sp = it % a.splits;
+      const int ct0 = sp * a.tiles_per_split;
+      const int ct1 = min(a.col_tiles, ct0 + a.tiles_per_split);
+      const int J = ct1 - ct0;
+      mbar_wait(smem_u32(xr_full), itc & 1);
+      tc_fence_after();
+      auto dist = [&]() {
+        mbar_wait(smem_u32(&full[ds]), dph);
+        tc_fence_after();
+        const uint32_t d_tm = tmem + TMS(sbn);
+        const uint64_t db = db0 + (uint64_t)(ds * stage16);
+        if (leader) {
+#pragma unroll
+          for (int pass = 0; pass < 3; ++pass) {
+            const uint64_t a_p = da0 + (pass == 0 ? a_half16 : 0u);
+            const uint64_t b_p = db + (pass == 1 ? b_half16 : 0u);
+            for (int ks = 0; ks < ksteps; ++ks)
+              mma_ss(d_tm, a_p + (uint64_t)(ks * kstep_a16), b_p + (uint64_t)(ks * kstep_b16), idesc_d,
+                     (pass | ks) != 0);
+          }
+          tc_commit(smem_u32(&s_full[sbn]));
+        }
+        __syncwarp();
+        if (++ds == (uint32_t)NS) { ds = 0; dph ^= 1; }
+        sbn ^= 1;
+      };
+      dist();
+      for (int jj = 0; jj < J; ++jj) {
+        if (jj + 1 < J) dist();   // S buffer of tile jj+1 was read by the epilogue of tile jj-1 (k_full seen)
+        mbar_wait(smem_u32(&k_full[kb]), kph);
+        tc_fence_after();
+        const bool chunk_start = (jj % CH) == 0;
+        if (chunk_start) {   // the previous chunk's O has been folded
+          mbar_wait(smem_u32(o_empty), oph ^ 1);
+          tc_fence_after();
+        }
+        const uint64_t vb = dv0 + (uint64_t)(cs * stage16);
+        const uint32_t k1 = tmem + TMK1(kb), k2 = tmem + TMK2(kb);
+        if (leader) {
+          // O += K1.V1 + K1.V2 + K2.V1  (K = 64 = 4 x 16, N = NW)
+#pragma unroll
+          for (int ks = 0; ks < BN / 16; ++ks)
+            mma16_ts(tmem + TMO, k1 + ks * 8, vb + (uint64_t)(ks * kstep_v16), idesc_c, !(chunk_start && ks == 0));
+#pragma unroll
+          for (int ks = 0; ks < BN / 16; ++ks)
+            mma16_ts(tmem + TMO, k1 + ks * 8, vb + (uint64_t)(v2_16 + ks * kstep_v16), idesc_c, 1);
+#pragma unroll
+          for (int ks = 0; ks < BN / 16; ++ks)
+            mma16_ts(tmem + TMO, k2 + ks * 8, vb + (uint64_t)(ks * kstep_v16), idesc_c, 1);
+          tc_commit(smem_u32(&empty[cs]));
+          tc_commit(smem_u32(&k_empty[kb]));
+          if ((jj % CH) == CH - 1 || jj == J - 1) tc_commit(smem_u32(o_full));
+        }
+        __syncwarp();
+        if ((jj % CH) == CH - 1 || jj == J - 1) oph ^= 1;
+        if (++cs == (uint32_t)NS) cs = 0;
+        if (++kb == 2) { kb = 0; kph ^= 1; }
+      }
+      if (leader) tc_commit(smem_u32(xr_empty));
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue (8 warps) =====================
+    const int q = warp & 3;
+    const int half = (warp - 4) >> 2;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    uint32_t sb = 0, sph = 0, kb = 0, kph = 0, oph = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int rt = it / a.splits, sp = it - rt * a.splits;
+      const int ct0 = sp * a.tiles_per_split;
+      const int ct1 = min(a.col_tiles, ct0 + a.tiles_per_split);
+      const int J = ct1 - ct0;
+      const int64_t row = (int64_t)rt * BM + q * 32 + lane;
+      const int64_t diag_col = (a.self_offset >= 0 && row < a.n_rows) ? row + a.self_offset : -1000;
+      float* dst = a.accw + (int64_t)sp * a.NW * a.rows_pad + row;   // column c at dst[c * rows_pad]
+      for (int jj = 0; jj < J; ++jj) {
+        mbar_wait(smem_u32(&s_full[sb]), sph);
+        tc_fence_after();
+        uint32_t v[32];
+        tmem_ld32(tmem + lane_base + TMS(sb) + half * 32, v);
+        tmem_wait_ld();
+        const int64_t e_diag = diag_col - ((int64_t)(ct0 + jj) * BN + half * 32);
+        if (__any_sync(0xffffffffu, e_diag >= 0 && e_diag < 32)) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (e == e_diag) v[e] = 0u;   // same point on both sides: r2 = 0 exactly
+        }
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          float sv = __uint_as_float(v[e]);
+          float kap;
+          if (FAM == GP_FAMILY_RBF) {
+            kap = ex2_approx(sv > 0.f ? 0.f : sv);
+          } else {
+            float u = sqrt_approx(sv < 0.f ? 0.f : sv);
+            float ex = ex2_approx(u * -kLog2e);
+            kap = fmaf(u, ex, ex);
+          }
+          v[e] = __float_as_uint(kap);
+        }
+        mbar_wait(smem_u32(&k_empty[kb]), kph ^ 1);   // K[kb] was read two tiles ago
+        tc_fence_after();
+#pragma unroll
+        for (int s16 = 0; s16 < 2; ++s16) {
+          uint32_t p1[8], p2[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            split_pair(__uint_as_float(v[16 * s16 + 2 * k]), __uint_as_float(v[16 * s16 + 2 * k + 1]), p1[k], p2[k]);
+          tmem_st8(tmem + lane_base + TMK1(kb) + half * 16 + 8 * s16, p1);
+          tmem_st8(tmem + lane_base + TMK2(kb) + half * 16 + 8 * s16, p2);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&k_full[kb]));
+        if (++sb == 2) { sb = 0; sph ^= 1; }
+        if (++kb == 2) { kb = 0; kph ^= 1; }
+        if ((jj % CH) == CH - 1 || jj == J - 1) {
+          // fold the chunk: this warp's lane quarter, alternate 16-column blocks per half
+          mbar_wait(smem_u32(o_full), oph);
+          oph ^= 1;
+          tc_fence_after();
+          const bool first = jj < CH;
+          // column-major destination: a warp's 32 lanes are 32 consecutive rows (coalesced)
+          for (int c0 = half * 16; c0 < NW; c0 += 32) {
+            uint32_t o[16];
+            tmem_ld16(tmem + lane_base + TMO + c0, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              float* p = dst + (int64_t)(c0 + c) * a.rows_pad;
+              const float r = __uint_as_float(o[c]);
+              *p = first ? r : *p + r;
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(o_empty));
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// out[i, c] = s2 2^-s_c sum_splits accw[sp][c][i] (+ noise V[i + diag_offset, c])
+__global__ void kv_wide_finalize(const float* __restrict__ accw, int splits, int NW, int64_t rows_pad,
+                                 int64_t nr, int t, const float* __restrict__ inv_vscale, float* out, int64_t ldo,
+                                 float s2, float noise, const float* __restrict__ V, int64_t ldv,
+                                 int64_t diag_offset) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nr * t) return;
+  const int c = (int)(idx / nr);
+  const int64_t i = idx - (int64_t)c * nr;   // consecutive threads: consecutive rows (coalesced reads)
+  float acc = 0.f;
+  for (int sp = 0; sp < splits; ++sp) acc += accw[((int64_t)sp * NW + c) * rows_pad + i];
+  float r = s2 * acc * inv_vscale[c];
+  if (diag_offset >= 0) r = fmaf(noise, V[(i + diag_offset) * ldv + c], r);
+  out[i * ldo + c] = r;
+}
+
+struct Plan {
+  int DK, NW, row_tiles, col_tiles, splits, tiles_per_split, nstages;
+  int64_t rows_pad;
+  size_t row_img_bytes, col_img_bytes, v_img_bytes, split_bytes, smem;
+};
+
+static Plan make_plan(const gp_kv_desc* d, int t) {
+  Plan p;
+  p.DK = (d->d + 2 + 7) / 8 * 8;
+  p.NW = (t + 15) / 16 * 16;
+  p.row_tiles = (int)((d->n_rows + BM - 1) / BM);
+  p.col_tiles = (int)((d->n_cols + BN - 1) / BN);
+  // column splits depend on the column count only for the square training
+  // operator (bitwise-identical rows under any row sharding)
+  int64_t hint_rows = (d->diag_offset >= 0 || d->Xr == d->Xc) ? d->n_cols : d->n_rows;
+  int64_t hint_tiles = (hint_rows + BM - 1) / BM;
+  int64_t target = 2LL * num_sms();
+  int64_t s = (target + hint_tiles - 1) / hint_tiles;
+  s = std::max<int64_t>(1, std::min<int64_t>({s, 64, (int64_t)p.col_tiles}));
+  p.tiles_per_split = (int)((p.col_tiles + s - 1) / s);
+  p.splits = (p.col_tiles + p.tiles_per_split - 1) / p.tiles_per_split;
+  p.row_img_bytes = (size_t)p.row_tiles * 2 * BM * p.DK * 4;
+  p.col_img_bytes = (size_t)p.col_tiles * 2 * BN * p.DK * 4;
+  p.v_img_bytes = (size_t)p.col_tiles * 2 * p.NW * BN * 2;
+  p.rows_pad = (int64_t)p.row_tiles * BM;
+  p.split_bytes = (size_t)p.splits * p.NW * p.rows_pad * 4 + 256 * sizeof(double) + 2 * TMAX * sizeof(float);
+  const size_t row_b = 2u * BM * p.DK * 4, stage_b = 2u * BN * p.DK * 4 + 2u * p.NW * BN * 2;
+  const size_t budget = 224 * 1024 - row_b - 256;
+  p.nstages = (int)std::min<size_t>(4, budget / stage_b);
+  p.smem = row_b + p.nstages * stage_b + 256;
+  return p;
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace tw
+
+bool kv_wide_supported(const gp_kv_desc* d, int t) {
+  if (t <= 16 || t > tw::TMAX) return false;
+  if (d->d < 1 || d->d + 2 > 32) return false;
+  return tw::make_plan(d, t).nstages >= 2;
+}
+
+size_t kv_wide_workspace(const gp_kv_desc* d, int t) {
+  if (!kv_wide_supported(d, t)) return 0;
+  tw::Plan p = tw::make_plan(d, t);
+  using tw::align256;
+  return align256(p.row_img_bytes) + align256(p.col_img_bytes) + align256(p.v_img_bytes) + align256(p.split_bytes);
+}
+
+int kv_wide(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out, int64_t ldo, void* ws,
+            size_t ws_bytes, cudaStream_t st) {
+  using namespace tw;
+  Plan p = make_plan(desc, t);
+  size_t need = kv_wide_workspace(desc, t);
+  GP_REQUIRE(ws != nullptr && ws_bytes >= need, "gp_kv(wide): workspace of %zu bytes required, %zu given", need,
+             ws_bytes);
+  char* w = static_cast<char*>(ws);
+  float* row_img = reinterpret_cast<float*>(w); w += align256(p.row_img_bytes);
+  float* col_img = reinterpret_cast<float*>(w); w += align256(p.col_img_bytes);
+  __half* v_img = reinterpret_cast<__half*>(w); w += align256(p.v_img_bytes);
+  double* mean = reinterpret_cast<double*>(w); w += 256 * sizeof(double);
+  float* vscale = reinterpret_cast<float*>(w); w += TMAX * sizeof(float);
+  float* inv_vscale = reinterpret_cast<float*>(w); w += TMAX * sizeof(float);
+  float* accw = reinterpret_cast<float*>(w);
+  const double c = desc->family == GP_FAMILY_RBF ? 1.4426950408889634 : -6.0;
+  if (int rc = tc::distance_images(desc->Xr, desc->ldr, desc->n_rows, desc->Xc, desc->ldc, desc->n_cols, desc->d,
+                                   p.DK, BM, BN, c, mean, row_img, col_img, st))
+    return rc;
+  if (int rc = tc::v_colscale(V, ldv, desc->n_cols, t, vscale, inv_vscale, st)) return rc;
+  if (int rc = tc::v_images16_wide(V, ldv, t, p.NW, desc->n_cols, vscale, v_img, p.col_tiles, st)) return rc;
+  Args a;
+  a.row_img = row_img; a.col_img = col_img; a.v_img = v_img; a.inv_vscale = inv_vscale;
+  a.DK = p.DK; a.NW = p.NW;
+  a.n_rows = desc->n_rows; a.n_cols = desc->n_cols;
+  a.row_tiles = p.row_tiles; a.col_tiles = p.col_tiles; a.splits = p.splits;
+  a.tiles_per_split = p.tiles_per_split; a.nstages = p.nstages; a.t = t;
+  a.s2 = (float)desc->outputscale; a.noise = (float)desc->noise; a.diag_offset = desc->diag_offset;
+  a.self_offset = desc->self_offset;
+  a.accw = accw; a.rows_pad = p.rows_pad;
+  int items = p.row_tiles * p.splits;
+  int grid = std::min(items, num_sms());
+  auto kern = desc->family == GP_FAMILY_RBF ? kv_wide_kernel<GP_FAMILY_RBF> : kv_wide_kernel<GP_FAMILY_MATERN32>;
+  GP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+  kern<<<grid, NTHREADS, p.smem, st>>>(a);
+  GP_LAUNCH_CHECK();
+  const int64_t tot = desc->n_rows * (int64_t)t;
+  kv_wide_finalize<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(accw, p.splits, p.NW, p.rows_pad, desc->n_rows, t,
+                                                                  inv_vscale, out, ldo, a.s2, a.noise, V, ldv,
+                                                                  desc->diag_offset);
+  GP_LAUNCH_CHECK();
+  return GP_OK;
+}
+
+}  // namespace gp

@@ -209,8 +209,10 @@ def test_tc_row_shards_bitwise_equal_full():
         assert np.array_equal(parts, full), shards
 
 
-@pytest.mark.parametrize("t", [1, 3, 11, 16])
+@pytest.mark.parametrize("t", [1, 3, 11, 16, 17, 40, 256])
 def test_tc_widths_and_families(t):
+    """t <= 16: row-tiled tcgen05 kernel; 16 < t <= 256: the wide-RHS kernel
+    (variance solves batch 256 test points, predictor.py:135-182)."""
     rng = np.random.default_rng(t)
     for fam in ("rbf", "matern32"):
         for d in (1, 3, 8, 30):
@@ -220,5 +222,35 @@ def test_tc_widths_and_families(t):
             ls = np.linspace(0.75, 1.5, d) * np.sqrt(d)
             m = gp.KernelModel(fam, 1.3, ls, 0.2)
             ref = O.kernel_mvm(O.make_hp(fam, 1.3, ls, 0.2), X, V)
-            got = _kv(m, X, V, algo=2)
+            got = _kv(m, X, V, algo=2 if t <= 16 else 0)
             assert colrel(got, ref) <= KV_RTOL, (fam, d, t, colrel(got, ref))
+
+
+def test_wide_rhs_scaled_columns_and_cross_blocks():
+    """Wide kernel with columns of very different magnitude (per-column fp16
+    scaling) and on cross blocks (test rows x training columns)."""
+    rng = np.random.default_rng(7)
+    n, d, t = 3000, 8, 100
+    X = rng.standard_normal((n, d))
+    V = rng.standard_normal((n, t)) * np.geomspace(1e-6, 1e6, t)
+    ls = np.linspace(0.75, 1.5, d) * np.sqrt(d)
+    m = gp.KernelModel("matern32", 1.1, ls, 0.3)
+    hp = O.make_hp("matern32", 1.1, ls, 0.3)
+    assert colrel(_kv(m, X, V, algo=0), O.kernel_mvm(hp, X, V)) <= KV_RTOL
+    Xt = rng.standard_normal((300, d))
+    got = _kv(m, Xt, V, algo=0, Xc=X)
+    ref = O.kernel_block(hp, Xt, X) @ V
+    assert colrel(got, ref) <= KV_RTOL
+
+
+def test_symmetric_kernel_matches_row_tiled_and_is_deterministic():
+    """algo 3 (each unordered pair once, 64-bit fixed-point accumulation):
+    same values as the row-tiled kernel within fp32 round-off, bitwise
+    reproducible run to run."""
+    w = syn.WORKLOADS["C2"]
+    X = syn.whitened_inputs(20_000, w.d, 0)
+    V = syn.rhs_block(20_000, 11, 2)
+    sym = _kv_rows(w, X, V, 0, 20_000, algo=3)
+    tc = _kv_rows(w, X, V, 0, 20_000, algo=2)
+    assert colrel(sym, tc) <= 1e-5
+    assert np.array_equal(sym, _kv_rows(w, X, V, 0, 20_000, algo=3))
