@@ -8,8 +8,9 @@
 // than SFU-bound: per 128 x 64 tile, O += K1.V1 + K1.V2 + K2.V1 (kind::f16,
 // 2-term fp16 splits of K and of the column-scaled V, fp32 accumulation in
 // TMEM), 12 MMAs of N = t_pad. O (t_pad TMEM columns) accumulates over CH
-// column tiles and is then folded into the fp32 destination by the epilogue
-// warps (plain read-modify-write: each CTA owns its rows of its column split),
+// column tiles and is then folded into an fp32 accumulator in global memory by
+// TMA bulk reduce-adds (cp.reduce.async.bulk, 2 KB per warp block, issued in a
+// fixed order per element: deterministic),
 // bounding the length of any TMEM accumulation chain (long TMEM accumulation
 // loses precision, measured in kv_tc.cu).
 //
@@ -47,6 +48,24 @@ struct Args {
   int64_t rows_pad;
 };
 
+// accumulator layout (fp32): [split][row tile][lane quarter q][column][32 rows],
+// so one epilogue warp's 32 rows x 16 columns block is 2 KB contiguous and is
+// folded with a single TMA bulk reduce-add (cp.reduce.async.bulk .add.f32)
+__host__ __device__ __forceinline__ int64_t accw_index(int64_t sp, int64_t rt, int row_tiles, int q, int NW, int col,
+                                                       int l) {
+  return ((((sp * row_tiles + rt) * 4 + q) * NW + col) * 32) + l;
+}
+constexpr uint32_t STAGE_FOLD_BYTES = 32u * 16u * 4u;   // one warp's 32 x 16 fp32 block
+
+__device__ __forceinline__ void bulk_reduce_add_f32(const void* gdst, uint32_t ssrc, uint32_t bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(gdst), "r"(ssrc),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // TMEM: S 2 x 64 | K1 32 + K2 32 (x2 buffers) | O NW (<= 256)
 __device__ __forceinline__ uint32_t TMS(uint32_t b) { return b * 64; }
 __device__ __forceinline__ uint32_t TMK1(uint32_t b) { return 128 + b * 64; }
@@ -75,6 +94,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
   uint64_t* xr_full = o_empty + 1;
   uint64_t* xr_empty = xr_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xr_empty + 1);
+  float* fold_s = reinterpret_cast<float*>(smem + row_bytes + NS * stage_bytes + 256);   // [8 warps][2][32 x 16]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -219,7 +239,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
       const int J = ct1 - ct0;
       const int64_t row = (int64_t)rt * BM + q * 32 + lane;
       const int64_t diag_col = (a.self_offset >= 0 && row < a.n_rows) ? row + a.self_offset : -1000;
-      float* dst = a.accw + (int64_t)sp * a.NW * a.rows_pad + row;   // column c at dst[c * rows_pad]
+      float* dst = a.accw + accw_index(sp, rt, a.row_tiles, q, NW, 0, 0);   // this warp's [col][32] slab
       for (int jj = 0; jj < J; ++jj) {
         mbar_wait(smem_u32(&s_full[sb]), sph);
         tc_fence_after();
@@ -267,17 +287,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
           mbar_wait(smem_u32(o_full), oph);
           oph ^= 1;
           tc_fence_after();
-          const bool first = jj < CH;
-          // column-major destination: a warp's 32 lanes are 32 consecutive rows (coalesced)
-          for (int c0 = half * 16; c0 < NW; c0 += 32) {
+          // the previous fold's bulk reductions into this slab must be complete
+          // (keeps the per-element addition order fixed: deterministic)
+          if (lane == 0) bulk_wait_all();
+          __syncwarp();
+          float* stg0 = fold_s + (warp - 4) * 2 * (32 * 16);
+          int buf = 0;
+          for (int c0 = half * 16; c0 < NW; c0 += 32, buf ^= 1) {
             uint32_t o[16];
             tmem_ld16(tmem + lane_base + TMO + c0, o);
+            if (lane == 0) bulk_wait_read1();   // staging buffer `buf` free again
+            __syncwarp();
             tmem_wait_ld();
+            float* stg = stg0 + buf * (32 * 16);
 #pragma unroll
-            for (int c = 0; c < 16; ++c) {
-              float* p = dst + (int64_t)(c0 + c) * a.rows_pad;
-              const float r = __uint_as_float(o[c]);
-              *p = first ? r : *p + r;
+            for (int c = 0; c < 16; ++c) stg[c * 32 + lane] = __uint_as_float(o[c]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              bulk_reduce_add_f32(dst + (int64_t)c0 * 32, smem_u32(stg), STAGE_FOLD_BYTES);
+              bulk_commit();
             }
           }
           tc_fence_before();
@@ -288,6 +317,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
     }
   }
 
+  if (warp >= 4 && lane == 0) bulk_wait_all();
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -297,7 +327,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
 }
 
 // out[i, c] = s2 2^-s_c sum_splits accw[sp][c][i] (+ noise V[i + diag_offset, c])
-__global__ void kv_wide_finalize(const float* __restrict__ accw, int splits, int NW, int64_t rows_pad,
+__global__ void kv_wide_finalize(const float* __restrict__ accw, int splits, int NW, int row_tiles,
                                  int64_t nr, int t, const float* __restrict__ inv_vscale, float* out, int64_t ldo,
                                  float s2, float noise, const float* __restrict__ V, int64_t ldv,
                                  int64_t diag_offset) {
@@ -305,8 +335,10 @@ __global__ void kv_wide_finalize(const float* __restrict__ accw, int splits, int
   if (idx >= nr * t) return;
   const int c = (int)(idx / nr);
   const int64_t i = idx - (int64_t)c * nr;   // consecutive threads: consecutive rows (coalesced reads)
+  const int64_t rt = i / 128;
+  const int q = (int)((i / 32) & 3), l = (int)(i & 31);
   float acc = 0.f;
-  for (int sp = 0; sp < splits; ++sp) acc += accw[((int64_t)sp * NW + c) * rows_pad + i];
+  for (int sp = 0; sp < splits; ++sp) acc += accw[accw_index(sp, rt, row_tiles, q, NW, c, l)];
   float r = s2 * acc * inv_vscale[c];
   if (diag_offset >= 0) r = fmaf(noise, V[(i + diag_offset) * ldv + c], r);
   out[i * ldo + c] = r;
@@ -339,9 +371,10 @@ static Plan make_plan(const gp_kv_desc* d, int t) {
   p.rows_pad = (int64_t)p.row_tiles * BM;
   p.split_bytes = (size_t)p.splits * p.NW * p.rows_pad * 4 + 256 * sizeof(double) + 2 * TMAX * sizeof(float);
   const size_t row_b = 2u * BM * p.DK * 4, stage_b = 2u * BN * p.DK * 4 + 2u * p.NW * BN * 2;
-  const size_t budget = 224 * 1024 - row_b - 256;
+  const size_t fold_b = NUM_EPI_WARPS * 2 * STAGE_FOLD_BYTES;
+  const size_t budget = 224 * 1024 - row_b - 256 - fold_b;
   p.nstages = (int)std::min<size_t>(4, budget / stage_b);
-  p.smem = row_b + p.nstages * stage_b + 256;
+  p.smem = row_b + p.nstages * stage_b + 256 + fold_b;
   return p;
 }
 
@@ -392,6 +425,7 @@ int kv_wide(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* o
   a.s2 = (float)desc->outputscale; a.noise = (float)desc->noise; a.diag_offset = desc->diag_offset;
   a.self_offset = desc->self_offset;
   a.accw = accw; a.rows_pad = p.rows_pad;
+  GP_CUDA_TRY(cudaMemsetAsync(accw, 0, (size_t)p.splits * p.NW * p.rows_pad * 4, st));
   int items = p.row_tiles * p.splits;
   int grid = std::min(items, num_sms());
   auto kern = desc->family == GP_FAMILY_RBF ? kv_wide_kernel<GP_FAMILY_RBF> : kv_wide_kernel<GP_FAMILY_MATERN32>;
@@ -399,7 +433,7 @@ int kv_wide(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* o
   kern<<<grid, NTHREADS, p.smem, st>>>(a);
   GP_LAUNCH_CHECK();
   const int64_t tot = desc->n_rows * (int64_t)t;
-  kv_wide_finalize<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(accw, p.splits, p.NW, p.rows_pad, desc->n_rows, t,
+  kv_wide_finalize<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(accw, p.splits, p.NW, p.row_tiles, desc->n_rows, t,
                                                                   inv_vscale, out, ldo, a.s2, a.noise, V, ldv,
                                                                   desc->diag_offset);
   GP_LAUNCH_CHECK();
