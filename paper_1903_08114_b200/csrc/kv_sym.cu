@@ -52,7 +52,11 @@ constexpr int BN = 64;    // columns per tile (UMMA M of the mirror product)
 constexpr int TN = 16;    // right-hand sides
 // warp roles: 0 TMA, 1 MMA, 2 TMEM allocator, 3 idle, 4-11 kappa (S -> K),
 // 12-15 transpose (kappa^T -> TMEM, row image), 16-19 drain (O_I, O_J)
+// 8 kappa warps measured faster than 16 (with 16 the MMA-issuing warp shares
+// its scheduler with 6 others and the issue chain stretches)
 constexpr int KAPPA_WARP0 = 4, NUM_KAPPA_WARPS = 8;
+constexpr int KC = 64 / (NUM_KAPPA_WARPS / 4);   // columns of a tile per kappa warp
+static_assert(KC == 16 || KC == 32, "kappa warps use 16- or 32-column TMEM loads");
 constexpr int TRANS_WARP0 = KAPPA_WARP0 + NUM_KAPPA_WARPS;
 constexpr int DRAIN_WARP0 = TRANS_WARP0 + 4;
 constexpr int NTHREADS = 32 * (DRAIN_WARP0 + 4);
@@ -63,6 +67,11 @@ constexpr int NTHREADS = 32 * (DRAIN_WARP0 + 4);
 // distinct banks per half-warp.
 constexpr int KT_LD = 136;
 constexpr uint32_t KT32_BYTES = 64u * KT_LD * 4u;
+// mirror-output accumulator of one item (block Q): [CB column tiles][64 rows][ACC_LD]
+// fp32, row stride 17 floats so the drain lanes (16 rows x 2 column halves) hit
+// distinct banks
+constexpr int ACC_LD = 17;
+constexpr uint32_t ACCQ_BYTES = 16u * 64u * ACC_LD * 4u;
 // V image of one 64-point tile: 32 x 64 fp16, rows 0-15 = V1, 16-31 = V2
 constexpr uint32_t V_TILE_BYTES = 2u * TN * BN * 2u;
 
@@ -72,7 +81,7 @@ struct Args {
   const __half* v_img;    // [col tiles][32 x 64] fp16
   int DK;
   int64_t n;
-  int row_tiles, col_tiles, splits, n_items;
+  int row_tiles, col_tiles, nblocks, n_items;
   int nstages;
   int t;
   const int* expo;                  // [TN] partials (in scaled units) summed as round(v 2^expo_c)
@@ -106,27 +115,42 @@ __device__ __forceinline__ uint32_t TMOJ(uint32_t b) { return 448 + 32 * b; }
 __device__ __forceinline__ void red_add_u64(unsigned long long* p, long long v) {
   asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-// row-tile items: item L = I * splits + sp covers column tiles
-// [2I + sp*C, min(col_tiles, 2I + (sp+1)*C)), C = ceil((col_tiles - 2I) / splits)
-struct Item {
-  int rt, ct0, ct1;
+// Block-pair items. Points are grouped in blocks of RB row tiles (1024
+// points = CB column tiles); item L is the block pair (P, Q), P <= Q, in
+// row-major upper-triangular order. Within an item, sub-item r is row tile
+// I = RB P + r against the column tiles of block Q (P < Q: all mirrored), or,
+// on a diagonal pair, against column tiles [2I, CB (P+1)) of which the first
+// two form the 128 x 128 diagonal block (direct only). The mirror outputs of
+// an item all land in block Q, so they accumulate in SMEM across the RB row
+// tiles and are reduced to global memory once per item (4x fewer fixed-point
+// reductions than one flush per tile).
+constexpr int RB = 8, CB = 2 * RB;
+struct Sub {
+  int rt, ct0, ct1, first_mirror;
 };
-__device__ __forceinline__ Item item_of(const Args& a, int L) {
-  Item it;
-  it.rt = L / a.splits;
-  const int sp = L - it.rt * a.splits;
-  const int lo = 2 * it.rt;
-  const int m = a.col_tiles - lo;
-  const int C = (m + a.splits - 1) / a.splits;
-  it.ct0 = lo + sp * C;
-  it.ct1 = min(a.col_tiles, it.ct0 + C);
-  return it;
+__device__ __forceinline__ void pair_of(int L, int NB, int& P, int& Q) {
+  // start(P) = P NB - P (P - 1) / 2 <= L < start(P + 1)
+  const double b2 = 2.0 * NB + 1.0;
+  int p = (int)floor((b2 - sqrt(b2 * b2 - 8.0 * (double)L)) * 0.5);
+  p = max(0, min(NB - 1, p));
+  auto start = [&](int x) { return (long long)x * NB - (long long)x * (x - 1) / 2; };
+  while (p > 0 && start(p) > L) --p;
+  while (p + 1 < NB && start(p + 1) <= L) ++p;
+  P = p;
+  Q = p + (int)(L - start(p));
 }
-// boustrophedon assignment of items to persistent CTAs: item sizes fall
-// linearly with the row tile, so alternating the direction each round
-// balances the per-CTA totals
-__device__ __forceinline__ int item_index(int r, int b, int G) {
-  return r * G + ((r & 1) ? (G - 1 - b) : b);
+__device__ __forceinline__ bool sub_of(const Args& a, int P, int Q, int r, Sub& s) {
+  s.rt = RB * P + r;
+  if (s.rt >= a.row_tiles) return false;
+  if (P < Q) {
+    s.ct0 = CB * Q;
+    s.first_mirror = 0;
+  } else {
+    s.ct0 = 2 * s.rt;
+    s.first_mirror = 2;
+  }
+  s.ct1 = min(a.col_tiles, CB * (Q + 1));
+  return s.ct1 > s.ct0;
 }
 
 // v * 2^E as a (truncated) signed 64-bit integer on the integer pipes (the
@@ -170,7 +194,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
   uint8_t* xr_s = smem + 2 * KT32_BYTES;                          // row image (TMA)
   uint8_t* vi_s = xr_s + row_bytes;                               // V image of the row tile
   uint8_t* stages = vi_s + 2 * v_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + NS * stage_bytes);
+  float* accq = reinterpret_cast<float*>(stages + NS * stage_bytes);   // mirror outputs of block Q
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(accq) + ACCQ_BYTES);
   uint64_t* full = bars;             // [NS]  TMA -> MMA
   uint64_t* empty = bars + NS;       // [NS]  MMA -> TMA
   uint64_t* s_full = bars + 2 * NS;  // [2]   distance tile landed in SK buffer b      (MMA -> kappa)
@@ -192,6 +217,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x < TN) expo_s[threadIdx.x] = a.expo[threadIdx.x];
+  for (int i = threadIdx.x; i < (int)(ACCQ_BYTES / 4); i += blockDim.x) accq[i] = 0.f;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
@@ -231,11 +257,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
     // ===================== TMA producer =====================
     if (lane == 0) {
       uint32_t s = 0, ph = 0, itc = 0;
-      for (int r = 0;; ++r) {
-        const int L = item_index(r, b, G);
-        if (L >= a.n_items) break;
-        const Item it = item_of(a, L);
-        if (it.ct1 <= it.ct0) continue;
+      for (int L = b; L < a.n_items; L += G) {
+        int P, Q;
+        pair_of(L, a.nblocks, P, Q);
+        for (int sr = 0; sr < RB; ++sr) {
+        Sub it;
+        if (!sub_of(a, P, Q, sr, it)) continue;
         mbar_wait(smem_u32(xr_empty), (itc & 1) ^ 1);
         const int vt = min(2, a.col_tiles - 2 * it.rt);  // V tiles of this row tile
         mbar_expect_tx(smem_u32(xr_full), row_bytes + vt * v_bytes);
@@ -255,11 +282,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
           vimg += v_bytes / 2;
           if (++s == (uint32_t)NS) { s = 0; ph ^= 1; }
         }
+        }
       }
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    // per tile, in tensor-pipe order: direct(T), mirror(T), dist(T+2); the
+    // per tile, in tensor-pipe order: direct(T), dist(T+2), mirror(T); the
     // distance tile T+2 reuses the SK buffer of tile T once direct(T) is
     // complete (the pipe does not order one MMA's TMEM-A reads against a
     // later MMA's D writes, so that is an explicit k_empty wait)
@@ -281,13 +309,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
     uint32_t ds = 0, dph = 0, cs = 0, dbuf = 0, keph0 = 0, keph1 = 0, kfph0 = 0, kfph1 = 0;
     uint32_t ob = 0, oph = 0, ktph = 0, jb = 0, jph = 0;
     uint32_t itc = 0;
-    for (int r = 0;; ++r) {
-      const int L = item_index(r, b, G);
-      if (L >= a.n_items) break;
-      const Item it = item_of(a, L);
-      if (it.ct1 <= it.ct0) continue;
+    for (int L = b; L < a.n_items; L += G) {
+      int P, Q;
+      pair_of(L, a.nblocks, P, Q);
+      for (int sr = 0; sr < RB; ++sr) {
+      Sub it;
+      if (!sub_of(a, P, Q, sr, it)) continue;
       const int J = it.ct1 - it.ct0;
-      const int first_mirror = 2 * it.rt + 2 - it.ct0;   // tiles jj >= this are mirrored
+      const int first_mirror = it.first_mirror;   // tiles jj >= this are mirrored
       mbar_wait(smem_u32(xr_full), itc & 1);
       SYM_T(0, mbar_wait(smem_u32(xa_full), itc & 1));
       ++itc;
@@ -341,6 +370,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
         __syncwarp();
         ob ^= 1;
         if (ob == 0) oph ^= 1;
+        // the next distance tile goes out before the mirror product: it only
+        // depends on direct(jj) finishing with this SK buffer, while the mirror
+        // waits for the transpose warps
+        if (jj + 2 < J) dist();
         if (jj >= first_mirror) {
           // mirror (M = 64, K = 128 points of I = 8 x 16): lanes 0-15 O_J = KT1.[V1 | V2],
           // lanes 16-31 O_J[:, 0:16] = KT2.V1 (summed by the reader)
@@ -367,27 +400,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
           jb ^= 1;
           if (jb == 0) jph ^= 1;
         }
-        if (jj + 2 < J) dist();
         kbuf ^= 1;
         if (++cs == (uint32_t)NS) cs = 0;
       }
       if (leader) tc_commit(smem_u32(xr_empty));
       __syncwarp();
+      }
     }
   } else if (warp >= KAPPA_WARP0 && warp < TRANS_WARP0) {
-    // ===================== kappa warps (8): S -> K, kappa^T staging =====================
+    // ===================== kappa warps: S -> K, kappa^T staging =====================
+    // NUM_KAPPA_WARPS / 4 warps per TMEM lane quarter (SMSP), KC columns each
     const int q = warp & 3;                        // TMEM lane quarter
-    const int half = (warp - KAPPA_WARP0) >> 2;    // column half of the 64-col tile
+    const int slice = (warp - KAPPA_WARP0) >> 2;   // column slice of the 64-col tile
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const int i_loc = q * 32 + lane;
     uint32_t T = 0, m = 0;                         // tiles / mirrored tiles seen
-    for (int r = 0;; ++r) {
-      const int L = item_index(r, b, G);
-      if (L >= a.n_items) break;
-      const Item it = item_of(a, L);
-      if (it.ct1 <= it.ct0) continue;
+    for (int L = b; L < a.n_items; L += G) {
+      int P, Q;
+      pair_of(L, a.nblocks, P, Q);
+      for (int sr = 0; sr < RB; ++sr) {
+      Sub it;
+      if (!sub_of(a, P, Q, sr, it)) continue;
       const int J = it.ct1 - it.ct0;
-      const int first_mirror = 2 * it.rt + 2 - it.ct0;
+      const int first_mirror = it.first_mirror;
       const int64_t my_row = (int64_t)it.rt * BM + i_loc;
       for (int jj = 0; jj < J; ++jj, ++T) {
         const bool mirror = jj >= first_mirror;
@@ -396,19 +431,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
         tacc[7] += 1;
         tc_fence_after();
         const uint32_t sk = tmem + lane_base + TMSK(sb);
-        uint32_t v[32];
-        tmem_ld32(sk + half * 32, v);
+        uint32_t v[KC];
+        if constexpr (KC == 32) {
+          tmem_ld32(sk + slice * KC, v);
+        } else {
+          tmem_ld16(sk + slice * KC, reinterpret_cast<uint32_t (&)[16]>(v));
+        }
         tmem_wait_ld();
         if (!mirror) {
-          const int64_t e_diag = my_row - ((int64_t)(it.ct0 + jj) * BN + half * 32);
-          if (__any_sync(0xffffffffu, e_diag >= 0 && e_diag < 32)) {
+          const int64_t e_diag = my_row - ((int64_t)(it.ct0 + jj) * BN + slice * KC);
+          if (__any_sync(0xffffffffu, e_diag >= 0 && e_diag < KC)) {
 #pragma unroll
-            for (int e = 0; e < 32; ++e)
+            for (int e = 0; e < KC; ++e)
               if (e == e_diag) v[e] = 0u;   // same point on both sides: r2 = 0 exactly
           }
         }
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
+        for (int e = 0; e < KC; ++e) {
           float sv = __uint_as_float(v[e]);
           float kap;
           if (FAM == GP_FAMILY_RBF) {
@@ -421,13 +460,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
           v[e] = __float_as_uint(kap);
         }
 #pragma unroll
-        for (int s16 = 0; s16 < 2; ++s16) {
+        for (int g8 = 0; g8 < KC / 16; ++g8) {
           uint32_t p1[8], p2[8];
 #pragma unroll
           for (int k = 0; k < 8; ++k)
-            split_pair(__uint_as_float(v[16 * s16 + 2 * k]), __uint_as_float(v[16 * s16 + 2 * k + 1]), p1[k], p2[k]);
-          tmem_st8(sk + 64 + half * 16 + 8 * s16, p1);   // K over S, same buffer (own reads done)
-          tmem_st8(sk + 96 + half * 16 + 8 * s16, p2);
+            split_pair(__uint_as_float(v[16 * g8 + 2 * k]), __uint_as_float(v[16 * g8 + 2 * k + 1]), p1[k], p2[k]);
+          tmem_st8(sk + 64 + slice * (KC / 2) + 8 * g8, p1);   // K over S, same buffer (own reads done)
+          tmem_st8(sk + 96 + slice * (KC / 2) + 8 * g8, p2);
         }
         if (mirror) {
           // kappa^T (fp32) for the transpose warps
@@ -435,8 +474,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
           SYM_T(2, mbar_wait(smem_u32(&ts_empty[mb]), ((m >> 1) & 1) ^ 1));
           float* ktb = kt32 + mb * (64 * KT_LD);
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            ktb[(32 * half + e) * KT_LD + (i_loc ^ ((e & 1) << 1))] = __uint_as_float(v[e]);
+          for (int e = 0; e < KC; ++e)
+            ktb[(KC * slice + e) * KT_LD + (i_loc ^ ((e & 1) << 1))] = __uint_as_float(v[e]);
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&ts_full[mb]));
           ++m;
@@ -446,6 +485,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&k_full[sb]));
       }
+      }
     }
   } else if (warp >= TRANS_WARP0 && warp < DRAIN_WARP0) {
     // ===================== transpose warps (4): row image, K^T -> TMEM =====================
@@ -453,13 +493,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const int i_loc = q * 32 + lane;
     uint32_t itc = 0, m = 0, ktph = 0;
-    for (int r = 0;; ++r) {
-      const int L = item_index(r, b, G);
-      if (L >= a.n_items) break;
-      const Item it = item_of(a, L);
-      if (it.ct1 <= it.ct0) continue;
+    for (int L = b; L < a.n_items; L += G) {
+      int P, Q;
+      pair_of(L, a.nblocks, P, Q);
+      for (int sr = 0; sr < RB; ++sr) {
+      Sub it;
+      if (!sub_of(a, P, Q, sr, it)) continue;
       const int J = it.ct1 - it.ct0;
-      const int first_mirror = 2 * it.rt + 2 - it.ct0;
+      const int first_mirror = it.first_mirror;
       {
         // row image -> TMEM (A operand of the distance product)
         mbar_wait(smem_u32(xr_full), itc & 1);
@@ -508,6 +549,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(kt_full));
       }
+      }
     }
   } else if (warp >= DRAIN_WARP0) {
     // ===================== drain warps (4): O_I -> registers, O_J -> fixed point =====================
@@ -515,17 +557,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const int i_loc = q * 32 + lane;
     uint32_t ob = 0, oph = 0, jb = 0, jph = 0;
-    int ej[TN / 2];   // exponents of this lane's mirror columns (c0 = 0 or 8)
-#pragma unroll
-    for (int c = 0; c < TN / 2; ++c) ej[c] = expo_s[(lane < 16 ? 0 : TN / 2) + c];
     float acc[TN];
-    for (int r = 0;; ++r) {
-      const int L = item_index(r, b, G);
-      if (L >= a.n_items) break;
-      const Item it = item_of(a, L);
-      if (it.ct1 <= it.ct0) continue;
+    for (int L = b; L < a.n_items; L += G) {
+      int P, Q;
+      pair_of(L, a.nblocks, P, Q);
+      for (int sr = 0; sr < RB; ++sr) {
+      Sub it;
+      if (!sub_of(a, P, Q, sr, it)) continue;
       const int J = it.ct1 - it.ct0;
-      const int first_mirror = 2 * it.rt + 2 - it.ct0;
+      const int first_mirror = it.first_mirror;
       const int64_t my_row = (int64_t)it.rt * BM + i_loc;
 #pragma unroll
       for (int c = 0; c < TN; ++c) acc[c] = 0.f;
@@ -534,41 +574,53 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
           SYM_T(0, mbar_wait(smem_u32(&o_full[ob]), oph));
           tacc[7] += 1;
           tc_fence_after();
-          uint32_t o[32];
-          tmem_ld32(tmem + lane_base + TMO(ob), o);
-          tmem_wait_ld();
+          {
+            uint32_t o[16];
+            tmem_ld16(tmem + lane_base + TMO(ob), o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < TN; ++c) acc[c] += __uint_as_float(o[c]);
+            tmem_ld16(tmem + lane_base + TMO(ob) + TN, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < TN; ++c) acc[c] += __uint_as_float(o[c]);
+          }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&o_empty[ob]));
           ob ^= 1;
           if (ob == 0) oph ^= 1;
-#pragma unroll
-          for (int c = 0; c < TN; ++c) acc[c] += __uint_as_float(o[c]) + __uint_as_float(o[c + TN]);
         }
         if (jj >= first_mirror) {  // mirror product of tile jj -> fixed-point sums
           SYM_T(1, mbar_wait(smem_u32(&oj_full[jb]), jph));
           tc_fence_after();
-          uint32_t o[32];
-          tmem_ld32(tmem + lane_base + TMOJ(jb), o);   // lanes 0-15: [1.V1 | 1.V2], 16-31: [2.V1 | -]
-          tmem_wait_ld();
+          // lanes 0-15: [1.V1 | 1.V2], 16-31: [2.V1 | -]
+          float v[TN];
+          {
+            uint32_t o[16];
+            tmem_ld16(tmem + lane_base + TMOJ(jb), o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < TN; ++c) v[c] = __uint_as_float(o[c]);
+            tmem_ld16(tmem + lane_base + TMOJ(jb) + TN, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < TN; ++c) v[c] += lane < 16 ? __uint_as_float(o[c]) : 0.f;
+          }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&oj_empty[jb]));
           jb ^= 1;
           if (jb == 0) jph ^= 1;
-          float v[TN];
 #pragma unroll
-          for (int c = 0; c < TN; ++c) {
-            const float mine =
-                lane < 16 ? __uint_as_float(o[c]) + __uint_as_float(o[c + TN]) : __uint_as_float(o[c]);
-            v[c] = mine + __shfl_xor_sync(0xffffffffu, mine, 16);
-          }
-          const int64_t row = (int64_t)(it.ct0 + jj) * BN + q * 16 + (lane & 15);
-          if (row < a.n) {
-            const int c0 = lane < 16 ? 0 : TN / 2;
+          for (int c = 0; c < TN; ++c) v[c] += __shfl_xor_sync(0xffffffffu, v[c], 16);
+          // accumulate into the item's SMEM block (rows 16q + lane%16 of column tile J - CB Q:
+          // this warp owns them, so no cross-warp synchronisation)
+          {
+            const int cidx = it.ct0 + jj - CB * Q;
+            float* arow = accq + ((cidx * 64) + q * 16 + (lane & 15)) * ACC_LD + (lane < 16 ? 0 : TN / 2);
 #pragma unroll
-            for (int c = 0; c < TN / 2; ++c)
-              if (c0 + c < a.t) contribute(a, row, c0 + c, lane < 16 ? v[c] : v[c + TN / 2], ej[c]);
+            for (int c = 0; c < TN / 2; ++c) arow[c] += lane < 16 ? v[c] : v[c + TN / 2];
           }
         }
       }
@@ -577,6 +629,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
         for (int c = 0; c < TN; ++c)
           if (c < a.t) contribute(a, my_row, c, acc[c], expo_s[c]);
       }
+      }
+      // item done: reduce block Q's mirror outputs (this warp's 16 rows of
+      // each column tile) into the fixed-point accumulator, and clear them
+      __syncwarp();
+#pragma unroll 1
+      for (int k = 0; k < CB / 2; ++k) {
+        const int pidx = k * 32 + lane;           // (column tile, row) pair
+        const int cidx = pidx >> 4, jl = q * 16 + (pidx & 15);
+        float* arow = accq + (cidx * 64 + jl) * ACC_LD;
+        const int64_t row = (int64_t)(CB * Q + cidx) * BN + jl;
+#pragma unroll
+        for (int c = 0; c < TN; ++c) {
+          const float val = arow[c];
+          arow[c] = 0.f;
+          if (c < a.t && row < a.n && val != 0.f) contribute(a, row, c, val, expo_s[c]);
+        }
+      }
+      __syncwarp();
     }
   }
 
@@ -652,7 +722,7 @@ __global__ void sym_finalize_kernel(const unsigned long long* __restrict__ acc, 
 }
 
 struct Plan {
-  int DK, row_tiles, col_tiles, splits, n_items, nstages;
+  int DK, row_tiles, col_tiles, nblocks, n_items, nstages;
   int64_t acc_ld;
   size_t row_img_bytes, col_img_bytes, v_img_bytes, acc_bytes, bad_bytes, smem;
 };
@@ -662,16 +732,15 @@ static Plan make_plan(const gp_kv_desc* d) {
   p.DK = (d->d + 2 + 7) / 8 * 8;
   p.row_tiles = (int)((d->n_rows + BM - 1) / BM);
   p.col_tiles = (int)((d->n_cols + BN - 1) / BN);  // row tile I starts at column tile 2I
-  p.splits = std::max(1, std::min(64, (8 * num_sms() + p.row_tiles - 1) / p.row_tiles));
-  if (const char* e = getenv("GP_SYM_SPLITS")) p.splits = std::max(1, atoi(e));   // diagnostic
-  p.n_items = p.row_tiles * p.splits;
+  p.nblocks = (p.row_tiles + RB - 1) / RB;
+  p.n_items = p.nblocks * (p.nblocks + 1) / 2;
   p.acc_ld = (int64_t)p.row_tiles * BM;
   p.row_img_bytes = (size_t)p.row_tiles * 2 * BM * p.DK * 4;
   p.col_img_bytes = (size_t)p.col_tiles * 2 * BN * p.DK * 4;
   p.v_img_bytes = (size_t)p.col_tiles * V_TILE_BYTES;
   p.acc_bytes = (size_t)TN * p.acc_ld * 8;
   p.bad_bytes = (size_t)p.acc_ld * 4;
-  const size_t fixed = 2 * KT32_BYTES + 2u * BM * p.DK * 4 + 2 * V_TILE_BYTES + 640;
+  const size_t fixed = 2 * KT32_BYTES + 2u * BM * p.DK * 4 + 2 * V_TILE_BYTES + ACCQ_BYTES + 640;
   const size_t stage_b = 2u * BN * p.DK * 4 + V_TILE_BYTES;
   const size_t budget = 227 * 1024;
   p.nstages = fixed >= budget ? 0 : (int)std::min<size_t>(4, (budget - fixed) / stage_b);
@@ -732,7 +801,7 @@ int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* ou
   }
   Args a;
   a.row_img = row_img; a.col_img = col_img; a.v_img = v_img; a.DK = p.DK;
-  a.n = n; a.row_tiles = p.row_tiles; a.col_tiles = p.col_tiles; a.splits = p.splits; a.n_items = p.n_items;
+  a.n = n; a.row_tiles = p.row_tiles; a.col_tiles = p.col_tiles; a.nblocks = p.nblocks; a.n_items = p.n_items;
   a.nstages = p.nstages; a.t = t;
   a.expo = expo; a.acc = acc; a.acc_ld = p.acc_ld; a.bad = bad;
   a.prof = nullptr;
@@ -749,7 +818,7 @@ int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* ou
     GP_CUDA_TRY(cudaStreamSynchronize(st));
     GP_CUDA_TRY(cudaMemcpy(h.data(), a.prof, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
     cudaFree(a.prof);
-    for (int wi : {1, 4, 8, 12, 16}) {
+    for (int wi : {1, 4, 8, TRANS_WARP0, DRAIN_WARP0}) {
       double s[8] = {0};
       for (int cta = 0; cta < grid; ++cta)
         for (int k = 0; k < 8; ++k) s[k] += (double)h[((size_t)cta * (NTHREADS / 32) + wi) * 8 + k];

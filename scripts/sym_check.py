@@ -33,7 +33,7 @@ def small():
     rng = np.random.default_rng(0)
     worst = 0.0
     for n in (1, 5, 64, 127, 128, 129, 191, 256, 700, 3000):
-        for d in (1, 3, 11, 29):
+        for d in (1, 3, 11, 14):
             for fam in ("rbf", "matern32"):
                 for t in (1, 11, 16):
                     X = rng.standard_normal((n, d))
