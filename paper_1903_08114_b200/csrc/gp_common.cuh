@@ -44,6 +44,18 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// clamps that propagate NaN in one FMNMX.NAN (the reference raises on
+// non-finite kernel blocks, partition.py:231-236, so NaN must survive)
+__device__ __forceinline__ float max0_nan(float x) {
+  float y;
+  asm("max.NaN.f32 %0, %1, 0f00000000;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float min0_nan(float x) {
+  float y;
+  asm("min.NaN.f32 %0, %1, 0f00000000;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float sqrt_approx(float x) {
   float y;
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -451,9 +451,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
           float sv = __uint_as_float(v[e]);
           float kap;
           if (FAM == GP_FAMILY_RBF) {
-            kap = ex2_approx(sv > 0.f ? 0.f : sv);  // S = -log2(e) r2 / 2
+            kap = ex2_approx(min0_nan(sv));  // S = -log2(e) r2 / 2
           } else {
-            float u = sqrt_approx(sv < 0.f ? 0.f : sv);  // S = 3 r2, u = sqrt(3) r
+            float u = sqrt_approx(max0_nan(sv));  // S = 3 r2, u = sqrt(3) r
             float ex = ex2_approx(u * -kLog2e);
             kap = fmaf(u, ex, ex);
           }

@@ -406,9 +406,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
             // clamps written as selects so NaN inputs propagate (the
             // reference raises on non-finite blocks, partition.py:231-236)
             if (FAM == GP_FAMILY_RBF) {
-              kap = ex2_approx(sv > 0.f ? 0.f : sv);  // S = -log2(e) r2 / 2
+              kap = ex2_approx(min0_nan(sv));  // S = -log2(e) r2 / 2
             } else {
-              float u = sqrt_approx(sv < 0.f ? 0.f : sv);  // S = 3 r2, u = sqrt(3) r
+              float u = sqrt_approx(max0_nan(sv));  // S = 3 r2, u = sqrt(3) r
               float ex = ex2_approx(u * -kLog2e);
               kap = fmaf(u, ex, ex);                       // (1 + sqrt3 r) e^{-sqrt3 r}
             }

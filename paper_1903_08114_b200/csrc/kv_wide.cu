@@ -257,9 +257,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
           float sv = __uint_as_float(v[e]);
           float kap;
           if (FAM == GP_FAMILY_RBF) {
-            kap = ex2_approx(sv > 0.f ? 0.f : sv);
+            kap = ex2_approx(min0_nan(sv));
           } else {
-            float u = sqrt_approx(sv < 0.f ? 0.f : sv);
+            float u = sqrt_approx(max0_nan(sv));
             float ex = ex2_approx(u * -kLog2e);
             kap = fmaf(u, ex, ex);
           }

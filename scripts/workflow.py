@@ -42,6 +42,16 @@ def main():
                 workload=key, n=w.n, d=w.d)
     print(json.dumps({"stage": "mll_result", "value": res.value, "iterations": res.diagnostics.iterations,
                       "gradients": {k: float(v) for k, v in res.gradients.items()}}), flush=True)
+    if "--train" in sys.argv:
+        from paper_1903_08114_b200 import trainer as tr
+        cfgt = tr.TrainConfig(protocol="pretrain-finetune", family=w.family, ard=w.ard,
+                              cg=likelihood.CgConfig(tolerance=1.0, probes=10, precond_rank=w.rank))
+        mdl, trace = timed("train(pretrain-finetune: 10k-subset L-BFGS 10 + Adam 10, full Adam 3)",
+                           lambda: tr.train(X, y, cfgt))
+        for r in trace.records:
+            print(json.dumps({"stage": "train_step", "phase": r.phase, "step": r.step, "mll": r.mll,
+                              "seconds": round(r.seconds, 3), "cg_iterations": r.cg_iterations}), flush=True)
+        model = mdl
     if "--skip-cache" in sys.argv:
         return
     cache = timed("build_cache(tol=1e-3)", lambda: predictor.build_cache(model, X, y, precond_rank=w.rank))
