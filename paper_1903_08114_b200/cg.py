@@ -379,14 +379,19 @@ def mbcg_solve(mvm, request: SolveRequest) -> SolveReport:
                        solutions_device=U)
 
 
-def slq_logdet(report, preconditioner: PreconditionerCache | None = None, columns=None) -> float:
+def slq_logdet(report, preconditioner: PreconditionerCache | None = None, columns=None,
+               n_total: int | None = None) -> float:
     """n * mean_j sum_m (V_0m)^2 log(lambda_m) (+ logdet P) over probe
-    columns (cg.py:182-218; the weight is n, as in the reference code)."""
+    columns (cg.py:182-218; the weight is n, as in the reference code).
+    `n_total` overrides n for a row-sharded solve (the report holds this
+    rank's rows only)."""
     tris = report.tridiagonals if not isinstance(report, DeviceSolve) else report.tridiagonals()
     cols = list(range(len(tris)) if columns is None else columns)
     if not cols:
         raise ValueError("at least one probe column is required")
     n = (report.solutions.shape[0] if isinstance(report, SolveReport) else report.U.shape[0])
+    if n_total is not None:
+        n = int(n_total)
     total = 0.0
     for j in cols:
         Tj = tris[j]

@@ -637,7 +637,7 @@ static Plan make_plan(const gp_kv_desc* d, int t) {
   p.col_tiles = (int)((d->n_cols + BN - 1) / BN);
   // column splits depend on the column count only for the square training
   // operator (bitwise-identical rows under any row sharding)
-  int64_t hint_rows = (d->diag_offset >= 0 || d->Xr == d->Xc) ? d->n_cols : d->n_rows;
+  int64_t hint_rows = (d->diag_offset >= 0 || d->self_offset >= 0 || d->Xr == d->Xc) ? d->n_cols : d->n_rows;
   int64_t hint_tiles = (hint_rows + BM - 1) / BM;
   int64_t target = 2LL * num_sms();
   int64_t s = (target + hint_tiles - 1) / hint_tiles;

@@ -1,0 +1,119 @@
+"""Row-sharded MLL + gradients and predictive mean across GPUs (one process
+per GPU, torch.distributed) — SURVEY §8(e).
+
+Rank r owns rows [row0, row1) of K̂ and of every CG block; X, y, the probe
+block Z and the rank-k preconditioner are replicated (O(nd + nk) per GPU, as
+in the paper). Exchanges:
+
+* mBCG: all-gather of the fp32 search directions and all-reduce of the fp64
+  reduction payload each iteration (cg.MbcgRun with a TorchComm);
+* MLL: all-reduce of the local y·a partial; the SLQ log-determinant comes
+  from the all-reduced alpha/beta histories, identical on every rank;
+* gradients: all-gather of the representer weights a (8 n bytes), then each
+  rank runs the fused gradient pass on its rows against all columns and the
+  1 + n_l + 2 partial sums are all-reduced (likelihood.py:166-216);
+* predictive mean: each rank contracts K(X*, X_local) a_local and the m test
+  outputs are all-reduced (predictor.py:113-132).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _device as D
+from . import _ops
+from . import precond as _pc
+from .cg import FusedOperator, mbcg_device, slq_logdet
+from .distributed import TorchComm
+from .errors import NumericError
+from .kernels import KernelModel
+from .likelihood import (LOG_TWO_PI, CgConfig, MLLDiagnostics, MLLResult, _grad_forms_raw,
+                         assemble_gradients, build_kernel_preconditioner, draw_probes_device)
+
+
+def _local_gradient_operands(a_loc, S_loc, W_loc, a_full, W_full, cache, r0, r1):
+    """Y rows of this shard and R over all rows for the fused gradient pass
+    (same identity as likelihood.gradient_operands)."""
+    T = D.torch()
+    t = W_loc.shape[1]
+    if cache is not None:
+        Yc = [0.5 * a_loc[:, None], -(S_loc - W_loc) / (2.0 * t)]
+        Rc = [a_full[:, None], W_full]
+        if cache.rank:
+            L = cache.factor_device
+            Yc.append(_ops.lowrank_mul(L[r0:r1].contiguous(), cache.binv_device) / (2.0 * cache.noise))
+            Rc.append(L)
+    else:
+        Yc = [0.5 * a_loc[:, None], -S_loc / (2.0 * t)]
+        Rc = [a_full[:, None], W_full]
+    Y = T.cat(Yc, dim=1).to(T.float32).contiguous()
+    R = T.cat(Rc, dim=1).to(T.float32).contiguous()
+    return Y, R
+
+
+def mll_value_and_grad_sharded(model: KernelModel, X, y, cg_config: CgConfig, probe_seed: int,
+                               comm: TorchComm) -> MLLResult:
+    """mll_value_and_grad (likelihood.py:104-163) with K̂ rows sharded over
+    the ranks of `comm`; every rank returns the same result."""
+    T = D.torch()
+    ps = D.points(X)
+    n = ps.n
+    if comm.n_total != n:
+        raise ValueError("communicator was built for a different training size")
+    yd = D.to_device(y)
+    if tuple(yd.shape) != (n,):
+        raise ValueError(f"y has shape {tuple(yd.shape)}, expected ({n},)")
+    model.scale_for(ps.d)
+    r0, r1 = comm.row0, comm.row1
+    t = cg_config.probes
+    yc = yd - model.mean
+    cache = build_kernel_preconditioner(model, ps, cg_config.precond_rank)   # identical on every rank
+    Z = draw_probes_device(n, t, probe_seed, cache)                          # identical on every rank
+    Xs32, _ = ps.scaled(model.scale_for(ps.d))
+    kv = _ops.FusedKernelOperator(model.family_code, ps.d, Xs32[r0:r1], Xs32, model.outputscale, 0.0,
+                                  -1, self_offset=r0)
+    op = FusedOperator(kv, model.noise, n)
+    B = T.cat([yc[:, None], Z], dim=1)[r0:r1].contiguous()
+    sol = mbcg_device(op, B, cg_config.tolerance, cg_config.max_iters, cache, comm=comm, row_offset=r0)
+    a_loc = sol.U[:, 0].contiguous()
+    S_loc = sol.U[:, 1:].contiguous()
+    logdet = slq_logdet(sol, cache, columns=range(1, t + 1), n_total=n)
+    red = T.stack([_ops.coldot(yc[r0:r1, None].contiguous(), a_loc[:, None])[0], a_loc.sum()])
+    comm.allreduce_(red)
+    quad, asum = (float(v) for v in D.to_host(red))
+    value = -0.5 * quad - 0.5 * logdet - 0.5 * n * LOG_TWO_PI
+    W_full = _pc.precond_apply_device(cache, Z) if cache is not None else Z
+    W_loc = W_full[r0:r1].contiguous()
+    a_full = T.zeros(comm.rows_per_rank * comm.world, dtype=T.float64, device=a_loc.device)
+    a_pad = T.zeros(comm.rows_per_rank, dtype=T.float64, device=a_loc.device)
+    a_pad[: r1 - r0] = a_loc
+    comm.allgather_rows(a_pad, a_full)
+    a_full = a_full[:n].contiguous()
+    Y, R = _local_gradient_operands(a_loc, S_loc, W_loc, a_full, W_full, cache, r0, r1)
+    raw = _grad_forms_raw(model, ps.d, Xs32[r0:r1], Xs32, Y, R, self_offset=r0)
+    gradients = assemble_gradients(model, raw, a_loc, S_loc, W_loc, cache, n,
+                                   reduce=lambda v: comm.allreduce_(v.contiguous()))
+    gradients["mean"] = asum
+    if not np.isfinite(value) or any(not np.isfinite(g) for g in gradients.values()):
+        raise NumericError("non-finite likelihood value or gradient")
+    diag = MLLDiagnostics(probe_seed=probe_seed, iterations=sol.iterations, final_residuals=sol.rel,
+                          converged=bool(sol.converged.all()), logdet_estimate=logdet, quad_term=quad,
+                          precond_rank=cache.rank if cache is not None else 0)
+    return MLLResult(value=value, gradients=gradients, diagnostics=diag)
+
+
+def predict_mean_sharded(model: KernelModel, X_train, weights, X_test, comm: TorchComm) -> np.ndarray:
+    """mu + K(X*, X) a with the training columns sharded: each rank contracts
+    its columns, the m outputs are all-reduced (predictor.py:113-132)."""
+    T = D.torch()
+    tr = D.points(X_train)
+    te = D.points(np.atleast_2d(X_test) if not D.is_tensor(X_test) else X_test)
+    r0, r1 = comm.row0, comm.row1
+    ls = model.scale_for(tr.d)
+    Xr32, _ = te.scaled(ls)
+    Xc32, _ = tr.scaled(ls)
+    w = D.to_device(weights)[r0:r1, None].to(T.float32).contiguous()
+    kv = _ops.FusedKernelOperator(model.family_code, tr.d, Xr32, Xc32[r0:r1], model.outputscale, 0.0, -1)
+    part = kv.apply32(w, 1)[:, 0].to(T.float64).contiguous()
+    comm.allreduce_(part)
+    return model.mean + D.to_host(part)
