@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", default="M1e6")
-    ap.add_argument("--n", type=int, default=0, help="override n (testing only)")
+    ap.add_argument("--points", type=int, default=0, help="override n (testing only)")
     ap.add_argument("--algo", type=int, default=0, help="0 auto, 1 SIMT, 2 tcgen05")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -182,7 +182,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     import numpy as np
-    w, n, X, y = workload_inputs(args.workload, args.n)
+    w, n, X, y = workload_inputs(args.workload, args.points)
     ls = w.lengthscales()
     state = None
     vals = []
@@ -241,7 +241,7 @@ def run_ours(args):
 
     lib = _lib.lib()
     peaks, peak_kind = load_peaks()
-    w, n, X, y = workload_inputs(args.workload, args.n)
+    w, n, X, y = workload_inputs(args.workload, args.points)
     ls = w.lengthscales()
     model = gp.KernelModel(w.family, 1.0, ls, 0.1)
     comm = TorchComm(n) if world > 1 else None
@@ -320,7 +320,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": iters_per_s, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32 K·V (fp32 accumulate) / f64 CG state",
             "data": "synthetic: seeded whitened U[0,1]^11 inputs, RFF target, probes ~ N(0, P)",
             "config": {"workload": f"{w.name}: n={n} d={w.d} {w.family} ARD mBCG iteration, "
