@@ -89,7 +89,6 @@ struct Args {
   int64_t acc_ld;
   int* bad;                         // [acc_ld] non-finite partial seen for the row
   long long* prof;                  // optional per-warp phase cycle counters (GP_SYM_PROF=1)
-  int skip;                         // diagnostic: bit 0 skips mirror MMAs, bit 1 direct, bit 2 dist
 };
 
 // phase timing for the GP_SYM_PROF diagnostic (no effect when a.prof == nullptr)
@@ -169,15 +168,6 @@ __device__ __forceinline__ void contribute(const Args& a, int64_t row, int c, fl
     a.bad[row] = 1;
     return;
   }
-  if (a.skip & 8) {   // diagnostic: conversion only
-    if (fixed_point(v, E) == 0x7fffffffffffffffLL) a.bad[row] = 2;
-    return;
-  }
-  if (a.skip & 16) {  // diagnostic: RED without the conversion
-    red_add_u64(a.acc + (int64_t)c * a.acc_ld + row, (long long)__float_as_uint(v));
-    return;
-  }
-  if (a.skip & 32) return;
   red_add_u64(a.acc + (int64_t)c * a.acc_ld + row, fixed_point(v, E));
 }
 
@@ -805,7 +795,6 @@ int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* ou
   a.nstages = p.nstages; a.t = t;
   a.expo = expo; a.acc = acc; a.acc_ld = p.acc_ld; a.bad = bad;
   a.prof = nullptr;
-  a.skip = getenv("GP_SYM_SKIP") ? atoi(getenv("GP_SYM_SKIP")) : 0;
   int grid = std::min(p.n_items, num_sms());
   auto kern = desc->family == GP_FAMILY_RBF ? kv_sym_kernel<GP_FAMILY_RBF> : kv_sym_kernel<GP_FAMILY_MATERN32>;
   GP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));

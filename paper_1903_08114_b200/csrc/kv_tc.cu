@@ -75,7 +75,6 @@ struct Args {
   int chunk;              // column tiles per O flush
   int lookahead;          // distance MMAs issued this many tiles ahead (<= nstages - 1)
   long long* prof;        // optional per-warp wait counters (GP_TC_PROF=1, diagnostic)
-  int skip;               // diagnostic (GP_TC_SKIP): 1 contraction MMAs, 2 distance MMAs, 4 kappa math
 };
 
 #define TC_T(slot, ...)                                   \
@@ -275,7 +274,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
         tc_fence_after();
         const uint32_t d_tm = tmem + TMS(sb_next);
         const uint64_t db = db0 + (uint64_t)(ds * stage16);
-        if (leader && !(a.skip & 2)) {
+        if (leader) {
 #pragma unroll
           for (int pass = 0; pass < 3; ++pass) {
             const uint64_t a_p = da0 + (pass == 0 ? a_half16 : 0u);
@@ -305,7 +304,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
         const uint64_t vb = dv0 + (uint64_t)(cs * stage16);
         const uint32_t o_tm = tmem + TMO(oc);
         const uint32_t khi = tmem + TMKH(kb), klo = tmem + TMKL(kb);
-        if (leader && !(a.skip & 1)) {
+        if (leader) {
           // O = K_hi.[V_hi | V_lo];  O[:, 0:16] += K_lo.V_hi  (fresh accumulator every tile)
           if constexpr (KV_F16) {
 #pragma unroll
@@ -387,8 +386,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
         // this warp's 32 columns in one TMEM load (one round trip per tile)
         const int c0 = half * 32;
         uint32_t v[32];
-        tmem_ld32(tmem + lane_base + TMS(sb) + c0, v);
-        tmem_wait_ld();
+        TC_T(3, tmem_ld32(tmem + lane_base + TMS(sb) + c0, v); tmem_wait_ld());
         {
           const int64_t e_diag = diag_col - ((int64_t)(ct0 + jj) * BN + c0);
           // self-diagonal entry (same point on both sides): r2 = 0 exactly
@@ -398,7 +396,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
               if (k == e_diag) v[k] = 0u;
           }
         }
-        if (!(a.skip & 4)) {
+        const long long tk0 = a.prof ? clock64() : 0;
+        {
 #pragma unroll
           for (int k = 0; k < 32; ++k) {
             float sv = __uint_as_float(v[k]);
@@ -415,6 +414,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
             v[k] = __float_as_uint(kap);
           }
         }
+        if (a.prof) { v[0] |= (uint32_t)(clock64() == 0); tacc[4] += clock64() - tk0; }
         // K[g] was last read by this group's previous contraction
         TC_T(1, mbar_wait(smem_u32(&k_empty[g]), (kuse & 1) ^ 1));
         ++kuse;
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
             tmem_st16(tmem + lane_base + TMKL(g) + c0 + 16 * s16, lo);
           }
         }
-        tmem_wait_st();
+        TC_T(5, tmem_wait_st());
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&k_full[g]));
@@ -721,7 +721,6 @@ int kv_tc(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out
   auto kern = desc->family == GP_FAMILY_RBF ? kv_tc_kernel<GP_FAMILY_RBF> : kv_tc_kernel<GP_FAMILY_MATERN32>;
   GP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   a.prof = nullptr;
-  a.skip = getenv("GP_TC_SKIP") ? atoi(getenv("GP_TC_SKIP")) : 0;
   const char* pe = getenv("GP_TC_PROF");
   if (pe && *pe == '1') GP_CUDA_TRY(cudaMalloc(&a.prof, (size_t)grid * (NTHREADS / 32) * 8 * sizeof(long long)));
   kern<<<grid, NTHREADS, p.smem, st>>>(a);
