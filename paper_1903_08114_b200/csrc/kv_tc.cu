@@ -152,12 +152,16 @@ __global__ void points_image_kernel(const float* __restrict__ X, int64_t ldx, in
 //   done reading K), o_full/o_empty[2], xr_full/xr_empty (row image).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t TMS(uint32_t b) { return b * 64; }           // 0, 64, 128
-// K buffer b: tf32 hi [192 + 128b, +64) | lo [+64, +128); fp16 pairs K1 [.., +32) | K2 [+32, +64)
-__device__ __forceinline__ uint32_t TMKH(uint32_t b) { return 192 + b * 128; }   // 192, 320
-__device__ __forceinline__ uint32_t TMKL(uint32_t b) { return (KV_F16 ? 224 : 256) + b * 128; }
-__device__ __forceinline__ uint32_t TMO(uint32_t c) { return 448 + c * 32; }     // 448, 480
+// TMEM layouts (columns):            S            K (x2)       O (x2)     row image
+//   SS distance (3 S buffers):   [0, 192)     192 + 128b   [448, 512)   -
+//   TS distance (2 S buffers):   [0, 128)     [128, 256)   [256, 320)   [320, 320 + 2 DK)
+// K buffer b, fp16 pairs: K1 [tm_k + 64b, +32) | K2 [+32, +64); tf32 (SS only): hi 64 | lo 64
+#define TMKH(b) ((TS ? 128u : 192u) + (uint32_t)(b) * (TS ? 64u : 128u))
+#define TMKL(b) (TMKH(b) + (KV_F16 ? 32u : 64u))
+#define TMO(c) ((TS ? 256u : 448u) + (uint32_t)(c) * 32u)
+#define TMXA 320u
 
-template <int FAM>
+template <int FAM, bool TS>
 __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int DK = a.DK;
@@ -178,7 +182,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
   uint64_t* o_empty = o_full + 2;    // [2]
   uint64_t* xr_full = o_empty + 2;   // [1]
   uint64_t* xr_empty = xr_full + 1;  // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xr_empty + 1);
+  uint64_t* xa_full = xr_empty + 1;  // [1] row image copied into TMEM (TS mode)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xa_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -195,6 +200,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
     }
     mbar_init(smem_u32(xr_full), 1);
     mbar_init(smem_u32(xr_empty), 1);
+    mbar_init(smem_u32(xa_full), 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -268,6 +274,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
       const int ct1 = min(a.col_tiles, ct0 + a.tiles_per_split);
       const int J = ct1 - ct0;
       mbar_wait(smem_u32(xr_full), itc & 1);
+      if (TS) mbar_wait(smem_u32(xa_full), itc & 1);
       tc_fence_after();
       auto dist = [&]() {
         TC_T(0, mbar_wait(smem_u32(&full[ds]), dph));
@@ -275,13 +282,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
         const uint32_t d_tm = tmem + TMS(sb_next);
         const uint64_t db = db0 + (uint64_t)(ds * stage16);
         if (leader) {
+          if (TS) {
 #pragma unroll
-          for (int pass = 0; pass < 3; ++pass) {
-            const uint64_t a_p = da0 + (pass == 0 ? a_half16 : 0u);
-            const uint64_t b_p = db + (pass == 1 ? b_half16 : 0u);
-            for (int ks = 0; ks < ksteps; ++ks)
-              mma_ss(d_tm, a_p + (uint64_t)(ks * kstep_a16), b_p + (uint64_t)(ks * kstep_b16), idesc_d,
-                     (pass | ks) != 0);
+            for (int pass = 0; pass < 3; ++pass) {
+              const uint32_t a_t = tmem + TMXA + (pass == 0 ? (uint32_t)DK : 0u);
+              const uint64_t b_p = db + (pass == 1 ? b_half16 : 0u);
+              for (int ks = 0; ks < ksteps; ++ks)
+                mma_ts(d_tm, a_t + ks * 8, b_p + (uint64_t)(ks * kstep_b16), idesc_d, (pass | ks) != 0);
+            }
+          } else {
+#pragma unroll
+            for (int pass = 0; pass < 3; ++pass) {
+              const uint64_t a_p = da0 + (pass == 0 ? a_half16 : 0u);
+              const uint64_t b_p = db + (pass == 1 ? b_half16 : 0u);
+              for (int ks = 0; ks < ksteps; ++ks)
+                mma_ss(d_tm, a_p + (uint64_t)(ks * kstep_a16), b_p + (uint64_t)(ks * kstep_b16), idesc_d,
+                       (pass | ks) != 0);
+            }
           }
         }
         if (leader) {
@@ -289,7 +306,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
         }
         __syncwarp();
         if (++ds == (uint32_t)NS) { ds = 0; dph ^= 1; }
-        if (++sb_next == 3) sb_next = 0;
+        if (++sb_next == (TS ? 2u : 3u)) sb_next = 0;
       };
       for (int jj = 0; jj < LA && jj < J; ++jj) dist();
       for (int jj = 0; jj < J; ++jj) {
@@ -368,18 +385,38 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
       if (lane == 0) mbar_arrive(smem_u32(&o_empty[g]));
       pending = 0;
     };
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    uint32_t itc = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++itc) {
       const int rt = it / a.splits, sp = it - rt * a.splits;
       const int ct0 = sp * a.tiles_per_split;
       const int ct1 = min(a.col_tiles, ct0 + a.tiles_per_split);
       const int J = ct1 - ct0;
       const int64_t my_row = (int64_t)rt * BM + q * 32 + lane;
       const int64_t diag_col = (a.self_offset >= 0 && my_row < a.n_rows) ? my_row + a.self_offset : -1000;
+      if (TS && g == 0 && half == 0) {
+        // TS mode: row image hi | lo -> TMEM (A operand of the distance product).
+        // xr_full of this item implies the previous item's MMAs completed.
+        mbar_wait(smem_u32(xr_full), itc & 1);
+        const float* xr = reinterpret_cast<const float*>(xr_s);
+        const int i_loc = q * 32 + lane;
+        for (int part = 0; part < 2; ++part)
+          for (int k0 = 0; k0 < DK; k0 += 8) {
+            uint32_t w[8];
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+              w[kk] = __float_as_uint(xr[part * BM * DK + canon(i_loc, k0 + kk, BM)]);
+            tmem_st8(tmem + lane_base + TMXA + part * DK + k0, w);
+          }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(xa_full));
+      }
 #pragma unroll
       for (int c = 0; c < TN; ++c) acc[c] = 0.f;
       for (int jj = 0; jj < J; ++jj, ++T) {
         if ((int)(T & 1) != g) continue;
-        const uint32_t sb = T % 3, sph = (T / 3) & 1;
+        const uint32_t sb = T % (TS ? 2u : 3u), sph = (T / (TS ? 2u : 3u)) & 1;
         TC_T(0, mbar_wait(smem_u32(&s_full[sb]), sph));
         tacc[7] += 1;
         tc_fence_after();
@@ -709,7 +746,9 @@ int kv_tc(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out
   a.s2 = (float)desc->outputscale; a.noise = (float)desc->noise; a.diag_offset = desc->diag_offset;
   a.self_offset = desc->self_offset;
   a.V = V; a.ldv = ldv;
-  a.lookahead = std::min(2, p.nstages - 1);
+  // large d: row image TMEM-resident (TS distance MMA, 2 S buffers, look-ahead 1)
+  const bool ts = KV_F16 && p.DK >= 48;
+  a.lookahead = ts ? 1 : std::min(2, p.nstages - 1);
   a.chunk = CHUNK;
   if (p.splits > 1) {
     a.out = split_ws; a.ldo = t; a.split_stride = desc->n_rows * (int64_t)t;
@@ -718,7 +757,9 @@ int kv_tc(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out
   }
   int items = p.row_tiles * p.splits;
   int grid = std::min(items, num_sms());
-  auto kern = desc->family == GP_FAMILY_RBF ? kv_tc_kernel<GP_FAMILY_RBF> : kv_tc_kernel<GP_FAMILY_MATERN32>;
+  auto kern = desc->family == GP_FAMILY_RBF ? (ts ? kv_tc_kernel<GP_FAMILY_RBF, true> : kv_tc_kernel<GP_FAMILY_RBF, false>)
+                                            : (ts ? kv_tc_kernel<GP_FAMILY_MATERN32, true>
+                                                  : kv_tc_kernel<GP_FAMILY_MATERN32, false>);
   GP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   a.prof = nullptr;
   const char* pe = getenv("GP_TC_PROF");
