@@ -1,36 +1,41 @@
 // Symmetric tcgen05 K·V kernel for the square training operator (sm_100a).
 //
 // out = s2 * kappa(X, X) V (+ noise V), evaluating every unordered pair of
-// points ONCE: K is symmetric, so the tile K_IJ (row tile I of 128 points,
-// column tile J of 64 points strictly above the 128 x 128 diagonal block)
-// serves both
-//     out_I += K_IJ   V_J      (direct:  A = K   from TMEM, M = 128)
-//     out_J += K_IJ^T V_I      (mirror:  A = K^T from TMEM, M = 64)
+// points ONCE. K is symmetric, so the tile K_IJ (row tile I, column tile J,
+// 128 points each, I < J) serves both
+//     out_I += K_IJ   V_J      (direct:  A = K   from TMEM,        M = 128 rows i)
+//     out_J += K_IJ^T V_I      (mirror:  A = K^T from SMEM, MN-major, M = 128 rows j)
 // which halves the transcendental (SFU) work that bounds the kernel at CG
-// width. Diagonal blocks are evaluated in full, direct only.
+// width. Diagonal tiles (I = J) are evaluated in full and
+// used once (direct only).
 //
-// Per tile, on the tensor core (one elected thread issues, TMEM accumulators):
-//   S = A_I . B_J^T        3xTF32 (kind::tf32), A = row image in TMEM
-//   O_I = K . V_J          2-term fp16 split of K and of V (kind::f16, K = 16
-//   O_J = K^T . V_I        per instruction): K1.[V1|V2] (N = 32) + K2.V1
-// The fp16 split (K = K1 + K2 with K1 = K truncated to 11 bits, V scaled per
-// column by 2^s into fp16 range) is as accurate as 3xTF32 but needs half the
-// MMA instructions; the kernel is bound by MMA issue (~30 cycles per small-N
-// tcgen05.mma, measured) and the SFU, so instruction count is what matters.
+// The transpose costs nothing extra: each kappa lane (point i) writes its 8
+// consecutive K_ij (fp16 pairs along j) as one 16-byte store, which is
+// exactly a row of a core matrix of the MN-major (M = j contiguous) canonical
+// layout the tensor core reads K^T from. The same fp16 values go to TMEM in
+// place over S for the direct product.
 //
-// The mirror product needs K^T with j in TMEM lanes while the distance tile
-// lands with i in lanes, so each mirrored tile is transposed through a
-// double-buffered fp32 SMEM tile (producers: one 4-byte store per entry;
-// consumers: 8-byte pair loads, fp16 split, 16x256b TMEM stores with K1 in
-// lanes 0-15 and K2 in lanes 16-31 of each sub-partition, the M = 64 layout).
+// Per tile, on the tensor core (one elected thread issues):
+//   S = A_I . B_J^T                 3xTF32, A (row image) in TMEM, N = 128
+//   O_I[r] += K1.V1 + K2.V1 + K1.V2 (kind::f16, A = K from TMEM, N = 16 each)
+//   O_J[c] += K1^T.[V1|V2] + K2^T.V1 (kind::f16, A = K^T from SMEM)
+// with the fp16 split K = K1 + K2 (K1 = K truncated to 11 bits) and V scaled
+// per column by 2^s into fp16 range (V = V1 + V2): as accurate as 3xTF32.
 //
-// Contributions to one output row come from many CTAs, so they are summed in
-// 64-bit FIXED POINT (red.global.add.u64, per-column scale 2^E_c chosen from
-// ||V_c||_1 so no partial can overflow): integer addition is associative, so
-// the result is bitwise reproducible run to run and independent of the CTA
-// schedule, like the reference's partition-count independence
-// (test_partition.py:92-102). Quantisation error per partial is
-// <= ||V_c||_1 2^-61 (~1e-13 relative at n = 10^6), far below fp32 round-off.
+// Work items are 4 x 4 blocks of tiles (block pairs P <= Q, row-major
+// upper-triangular order, round-robin over persistent CTAs). O_I[0..3] and
+// O_J[0..3] accumulate in TMEM over an item (4 tiles of K each, short enough
+// for the tensor core's fp32 accumulation) and are drained once per item:
+// O_I into an SMEM fp32 accumulator that is carried across consecutive items
+// of the same row block, O_J straight into the global sums. Contributions to
+// one output row come from many CTAs, so they are summed in 64-bit FIXED POINT
+// (red.global.add.u64, per-column scale 2^E_c chosen from ||V_c||_1 so no
+// partial can overflow): integer addition is associative, so the result is
+// bitwise reproducible run to run and independent of the CTA schedule, like
+// the reference's partition-count independence (test_partition.py:92-102).
+//
+// Warp roles: 0 TMA producer, 1 MMA issuer, 2-5 drain (+ row image -> TMEM,
+// warp 2 allocates TMEM), 6-21 kappa (S -> K, 32 rows x 32 columns each).
 //
 // Reference semantics: kernels.py:225-244 (kappa), :293-316 (rows of K̂ incl.
 // the sigma^2 diagonal), partition.py:224-241 (row-block products).
@@ -39,6 +44,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -47,43 +53,32 @@ namespace tcs {
 
 using namespace gp::tc;
 
-constexpr int BM = 128;   // rows per tile (UMMA M of the direct product)
-constexpr int BN = 64;    // columns per tile (UMMA M of the mirror product)
+constexpr int BT = 128;   // points per tile, both sides (UMMA M of both products)
 constexpr int TN = 16;    // right-hand sides
-// warp roles: 0 TMA, 1 MMA, 2 TMEM allocator, 3 idle, 4-11 kappa (S -> K),
-// 12-15 transpose (kappa^T -> TMEM, row image), 16-19 drain (O_I, O_J)
-// 8 kappa warps measured faster than 16 (with 16 the MMA-issuing warp shares
-// its scheduler with 6 others and the issue chain stretches)
-constexpr int KAPPA_WARP0 = 4, NUM_KAPPA_WARPS = 8;
-constexpr int KC = 64 / (NUM_KAPPA_WARPS / 4);   // columns of a tile per kappa warp
-static_assert(KC == 16 || KC == 32, "kappa warps use 16- or 32-column TMEM loads");
-constexpr int TRANS_WARP0 = KAPPA_WARP0 + NUM_KAPPA_WARPS;
-constexpr int DRAIN_WARP0 = TRANS_WARP0 + 4;
-constexpr int NTHREADS = 32 * (DRAIN_WARP0 + 4);
-// fp32 kappa^T staging tile in SMEM (double buffered): element (j, i) at
-// j * KT_LD + (i ^ 2(j & 1)). Producers (lane = i) store conflict-free; the
-// 136-float row stride plus the pair swizzle makes the consumers' 8-byte
-// loads (16x256b fragment: rows j = lane/4, column pairs 4(lane%4)) hit 32
-// distinct banks per half-warp.
-constexpr int KT_LD = 136;
-constexpr uint32_t KT32_BYTES = 64u * KT_LD * 4u;
-// mirror-output accumulator of one item (block Q): [CB column tiles][64 rows][ACC_LD]
-// fp32, row stride 17 floats so the drain lanes (16 rows x 2 column halves) hit
-// distinct banks
-constexpr int ACC_LD = 17;
-constexpr uint32_t ACCQ_BYTES = 16u * 64u * ACC_LD * 4u;
-// V image of one 64-point tile: 32 x 64 fp16, rows 0-15 = V1, 16-31 = V2
-constexpr uint32_t V_TILE_BYTES = 2u * TN * BN * 2u;
+constexpr int RB = 4;     // tiles per block side: an item is a 4 x 4 block of tiles
+constexpr int DRAIN_WARP0 = 2, KAPPA_WARP0 = 6, NUM_KAPPA_WARPS = 16;
+constexpr int NTHREADS = 32 * (KAPPA_WARP0 + NUM_KAPPA_WARPS);
+constexpr uint32_t KS_HALF = BT * BT * 2;            // K1 (or K2) of one tile, fp16 MN-major
+constexpr uint32_t KS_BYTES = 2 * KS_HALF;
+constexpr uint32_t V_TILE_BYTES = 2u * TN * BT * 2u;  // [V1 | V2] of one tile, 32 x 128 fp16
+constexpr uint32_t ACCI_BYTES = RB * BT * TN * 4u;    // O_I carried over items of one row block
+constexpr uint32_t BAR_BYTES = 1024;
+
+// TMEM columns (512): S/K buffers 2 x 128 | O_I 4 x 16 | O_J 4 x 32 | row image 2 DK
+// S (fp32) lands in [128b, 128b + 128); the kappa warps overwrite it in place
+// with K1 | K2 (fp16 pairs along j): kstep ks (16 points) at 16 ks (K1), 16 ks + 8 (K2)
+__device__ __forceinline__ uint32_t TSK(uint32_t b) { return 128u * b; }
+__device__ __forceinline__ uint32_t TOI(int r) { return 256u + 16u * (uint32_t)r; }
+__device__ __forceinline__ uint32_t TOJ(int c) { return 320u + 32u * (uint32_t)c; }
+constexpr uint32_t TXA = 448;
 
 struct Args {
-  const float* row_img;   // [row tiles][2][BM*DK] tf32 hi|lo
-  const float* col_img;   // [col tiles][2][BN*DK]
-  const __half* v_img;    // [col tiles][32 x 64] fp16
+  const float* row_img;   // [tiles][2][BT*DK] tf32 hi|lo (A of the distance product)
+  const float* col_img;   // [tiles][2][BT*DK]
+  const __half* v_img;    // [tiles][32 x 128] fp16 [V1 | V2]
   int DK;
   int64_t n;
-  int row_tiles, col_tiles, nblocks, n_items;
-  int nstages;
-  int t;
+  int tiles, nblocks, n_items, nsc, nsv, t;
   const int* expo;                  // [TN] partials (in scaled units) summed as round(v 2^expo_c)
   unsigned long long* acc;          // [TN][acc_ld] fixed-point sums (column-major)
   int64_t acc_ld;
@@ -91,7 +86,6 @@ struct Args {
   long long* prof;                  // optional per-warp phase cycle counters (GP_SYM_PROF=1)
 };
 
-// phase timing for the GP_SYM_PROF diagnostic (no effect when a.prof == nullptr)
 #define SYM_T(slot, ...)                                  \
   do {                                                    \
     const long long _t0 = a.prof ? clock64() : 0;         \
@@ -99,36 +93,17 @@ struct Args {
     if (a.prof) tacc[slot] += clock64() - _t0;            \
   } while (0)
 
-// TMEM columns (512):
-//   SK 2 x 128: S (fp32) lands in [0, 64) of buffer b; the epilogue writes
-//     K1 | K2 (fp16 pairs along j) into [64, 96) | [96, 128)
-//   K^T 64 (fp16 pairs along i; M = 64 layout: K1 in lanes 0-15, K2 in lanes
-//     16-31 of each sub-partition) | row image hi|lo 2 x DK (<= 64)
-//   O_I 2 x 32 = [K1 V1 + K2 V1 | K1 V2]
-//   O_J 2 x 32 (lanes 0-15 [KT1 V1 | KT1 V2], lanes 16-31 [KT2 V1 | -])
-__device__ __forceinline__ uint32_t TMSK(uint32_t b) { return b * 128; }
-constexpr uint32_t TMKT = 256, TMXA = 320;
-__device__ __forceinline__ uint32_t TMO(uint32_t b) { return 384 + 32 * b; }
-__device__ __forceinline__ uint32_t TMOJ(uint32_t b) { return 448 + 32 * b; }
-
 __device__ __forceinline__ void red_add_u64(unsigned long long* p, long long v) {
   asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-// Block-pair items. Points are grouped in blocks of RB row tiles (1024
-// points = CB column tiles); item L is the block pair (P, Q), P <= Q, in
-// row-major upper-triangular order. Within an item, sub-item r is row tile
-// I = RB P + r against the column tiles of block Q (P < Q: all mirrored), or,
-// on a diagonal pair, against column tiles [2I, CB (P+1)) of which the first
-// two form the 128 x 128 diagonal block (direct only). The mirror outputs of
-// an item all land in block Q, so they accumulate in SMEM across the RB row
-// tiles and are reduced to global memory once per item (4x fewer fixed-point
-// reductions than one flush per tile).
-constexpr int RB = 8, CB = 2 * RB;
-struct Sub {
-  int rt, ct0, ct1, first_mirror;
-};
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(x), "r"(y), "r"(z), "r"(w)
+               : "memory");
+}
+
+// item L -> block pair (P, Q), P <= Q, in row-major upper-triangular order:
+// start(P) = P NB - P (P - 1) / 2 <= L < start(P + 1)
 __device__ __forceinline__ void pair_of(int L, int NB, int& P, int& Q) {
-  // start(P) = P NB - P (P - 1) / 2 <= L < start(P + 1)
   const double b2 = 2.0 * NB + 1.0;
   int p = (int)floor((b2 - sqrt(b2 * b2 - 8.0 * (double)L)) * 0.5);
   p = max(0, min(NB - 1, p));
@@ -138,19 +113,43 @@ __device__ __forceinline__ void pair_of(int L, int NB, int& P, int& Q) {
   P = p;
   Q = p + (int)(L - start(p));
 }
-__device__ __forceinline__ bool sub_of(const Args& a, int P, int Q, int r, Sub& s) {
-  s.rt = RB * P + r;
-  if (s.rt >= a.row_tiles) return false;
-  if (P < Q) {
-    s.ct0 = CB * Q;
-    s.first_mirror = 0;
-  } else {
-    s.ct0 = 2 * s.rt;
-    s.first_mirror = 2;
+
+// The tile sequence of one CTA (every role walks the same sequence): items
+// L = blockIdx.x + k gridDim.x; within an item, rows r then columns c, with
+// c >= r on a diagonal item (P = Q), whose tile (r, r) is a diagonal tile.
+struct TileSeq {
+  int NB, tiles, n_items, G;
+  int L, P, Q, r, c, rows_in, cols_in;
+  bool ok;
+  __device__ void set_item() {
+    pair_of(L, NB, P, Q);
+    rows_in = min(RB, tiles - RB * P);
+    cols_in = min(RB, tiles - RB * Q);
+    r = 0;
+    c = c0();
   }
-  s.ct1 = min(a.col_tiles, CB * (Q + 1));
-  return s.ct1 > s.ct0;
-}
+  __device__ void begin(const Args& a) {
+    NB = a.nblocks; tiles = a.tiles; n_items = a.n_items; G = gridDim.x;
+    L = blockIdx.x;
+    ok = L < n_items;
+    if (ok) set_item();
+  }
+  __device__ int c0() const { return P == Q ? r : 0; }
+  __device__ void next() {
+    if (++c < cols_in) return;
+    if (++r < rows_in) { c = c0(); return; }
+    L += G;
+    ok = L < n_items;
+    if (ok) set_item();
+  }
+  __device__ bool first_in_row() const { return c == c0(); }
+  __device__ bool last_in_row() const { return c == cols_in - 1; }
+  __device__ bool first_in_item() const { return r == 0 && c == c0(); }
+  __device__ bool last_in_item() const { return last_in_row() && r == rows_in - 1; }
+  __device__ bool mirror() const { return !(P == Q && c == r); }
+  __device__ int I() const { return RB * P + r; }
+  __device__ int J() const { return RB * Q + c; }
+};
 
 // v * 2^E as a (truncated) signed 64-bit integer on the integer pipes (the
 // F2I.S64 conversion would run on the XU pipe the kappa epilogue saturates).
@@ -175,63 +174,63 @@ template <int FAM>
 __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int DK = a.DK;
-  const uint32_t row_bytes = 2u * BM * DK * 4u;
-  const uint32_t col_bytes = 2u * BN * DK * 4u;
-  const uint32_t v_bytes = V_TILE_BYTES;
-  const uint32_t stage_bytes = col_bytes + v_bytes;
-  const int NS = a.nstages;
-  float* kt32 = reinterpret_cast<float*>(smem);                   // [2][64][KT_LD] fp32 kappa^T
-  uint8_t* xr_s = smem + 2 * KT32_BYTES;                          // row image (TMA)
-  uint8_t* vi_s = xr_s + row_bytes;                               // V image of the row tile
-  uint8_t* stages = vi_s + 2 * v_bytes;
-  float* accq = reinterpret_cast<float*>(stages + NS * stage_bytes);   // mirror outputs of block Q
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(accq) + ACCQ_BYTES);
-  uint64_t* full = bars;             // [NS]  TMA -> MMA
-  uint64_t* empty = bars + NS;       // [NS]  MMA -> TMA
-  uint64_t* s_full = bars + 2 * NS;  // [2]   distance tile landed in SK buffer b      (MMA -> kappa)
-  uint64_t* k_empty = s_full + 2;    // [2]   direct product done reading SK buffer b  (MMA -> MMA)
-  uint64_t* k_full = k_empty + 2;    // [2]   K written over S in SK buffer b          (kappa -> MMA)
-  uint64_t* o_full = k_full + 2;     // [2]   direct product done                      (MMA -> drain)
-  uint64_t* o_empty = o_full + 2;    // [2]   O_I read                                 (drain -> MMA)
-  uint64_t* oj_full = o_empty + 2;   // [2]   mirror product done                      (MMA -> drain)
-  uint64_t* oj_empty = oj_full + 2;  // [2]   O_J read                                 (drain -> MMA)
-  uint64_t* ts_full = oj_empty + 2;  // [2]   kappa^T staged in SMEM buffer            (kappa -> transpose)
-  uint64_t* ts_empty = ts_full + 2;  // [2]   SMEM buffer consumed                     (transpose -> kappa)
-  uint64_t* kt_full = ts_empty + 2;  // K^T written to TMEM                            (transpose -> MMA)
-  uint64_t* kt_empty = kt_full + 1;  // mirror product done reading K^T                (MMA -> transpose)
-  uint64_t* xr_full = kt_empty + 1;  // row image + V_I landed                         (TMA -> MMA, transpose)
-  uint64_t* xr_empty = xr_full + 1;  // item's products done with them                 (MMA -> TMA)
-  uint64_t* xa_full = xr_empty + 1;  // row image copied into TMEM                     (transpose -> MMA)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xa_full + 1);
+  const uint32_t img_bytes = 2u * BT * DK * 4u;       // row or column image of one tile (hi | lo)
+  const int NSC = a.nsc, NSV = a.nsv;
+  uint8_t* ks = smem;                                  // K1 | K2 of the current tile (mirror A operand)
+  uint8_t* xr_s = ks + KS_BYTES;                       // row image (TMA, copied into TMEM)
+  uint8_t* vi_s = xr_s + img_bytes;                    // V_I, double buffered by row
+  uint8_t* cring = vi_s + 2 * V_TILE_BYTES;            // [NSC] column images
+  uint8_t* vring = cring + NSC * img_bytes;            // [NSV] V_J images
+  float* acci = reinterpret_cast<float*>(vring + NSV * V_TILE_BYTES);   // [RB][BT][TN]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(acci) + ACCI_BYTES);
+  uint64_t* cfull = bars;               // [NSC] column image landed           TMA -> MMA
+  uint64_t* cempty = cfull + NSC;       // [NSC] distance product done         MMA -> TMA
+  uint64_t* vfull = cempty + NSC;       // [NSV] V_J landed                    TMA -> MMA
+  uint64_t* vempty = vfull + NSV;       // [NSV] direct product done           MMA -> TMA
+  uint64_t* vi_full = vempty + NSV;     // [2]   V_I landed                    TMA -> MMA
+  uint64_t* vi_empty = vi_full + 2;     // [2]   mirrors of the row done       MMA -> TMA
+  uint64_t* s_full = vi_empty + 2;      // [2]   S in TMEM buffer b            MMA -> kappa
+  uint64_t* k_full = s_full + 2;        // [2]   K written (TMEM + SMEM)       kappa -> MMA
+  uint64_t* sk_empty = k_full + 2;      // [2]   products done with buffer b   MMA -> MMA
+  uint64_t* ks_empty = sk_empty + 2;    //       products done with the SMEM K MMA -> kappa
+  uint64_t* xr_full = ks_empty + 1;     //       row image landed              TMA -> drain
+  uint64_t* xr_empty = xr_full + 1;     //       row image consumed            drain -> TMA
+  uint64_t* xa_full = xr_empty + 1;     //       row image in TMEM             drain -> MMA
+  uint64_t* xa_empty = xa_full + 1;     //       distance products of the row done  MMA -> drain
+  uint64_t* acc_full = xa_empty + 1;    //       item's products done          MMA -> drain
+  uint64_t* acc_empty = acc_full + 1;   //       O_I / O_J read                drain -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
   int* expo_s = reinterpret_cast<int*>(tmem_slot + 4);   // [TN] fixed-point exponents
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x < TN) expo_s[threadIdx.x] = a.expo[threadIdx.x];
-  for (int i = threadIdx.x; i < (int)(ACCQ_BYTES / 4); i += blockDim.x) accq[i] = 0.f;
+  for (int i = threadIdx.x; i < (int)(ACCI_BYTES / 4); i += blockDim.x) acci[i] = 0.f;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), 1);
+    for (int s = 0; s < NSC; ++s) {
+      mbar_init(smem_u32(&cfull[s]), 1);
+      mbar_init(smem_u32(&cempty[s]), 1);
+    }
+    for (int s = 0; s < NSV; ++s) {
+      mbar_init(smem_u32(&vfull[s]), 1);
+      mbar_init(smem_u32(&vempty[s]), 1);
     }
     for (int q = 0; q < 2; ++q) {
+      mbar_init(smem_u32(&vi_full[q]), 1);
+      mbar_init(smem_u32(&vi_empty[q]), 1);
       mbar_init(smem_u32(&s_full[q]), 1);
-      mbar_init(smem_u32(&k_empty[q]), 1);
       mbar_init(smem_u32(&k_full[q]), NUM_KAPPA_WARPS);
-      mbar_init(smem_u32(&o_full[q]), 1);
-      mbar_init(smem_u32(&o_empty[q]), 4);
-      mbar_init(smem_u32(&oj_full[q]), 1);
-      mbar_init(smem_u32(&oj_empty[q]), 4);
-      mbar_init(smem_u32(&ts_full[q]), NUM_KAPPA_WARPS);
-      mbar_init(smem_u32(&ts_empty[q]), 4);
+      mbar_init(smem_u32(&sk_empty[q]), 1);
     }
-    mbar_init(smem_u32(kt_full), 4);
-    mbar_init(smem_u32(kt_empty), 1);
+    mbar_init(smem_u32(ks_empty), 1);
     mbar_init(smem_u32(xr_full), 1);
-    mbar_init(smem_u32(xr_empty), 1);
+    mbar_init(smem_u32(xr_empty), 4);
     mbar_init(smem_u32(xa_full), 4);
+    mbar_init(smem_u32(xa_empty), 1);
+    mbar_init(smem_u32(acc_full), 1);
+    mbar_init(smem_u32(acc_empty), 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 2) {
+  if (warp == DRAIN_WARP0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -239,404 +238,295 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int G = gridDim.x, b = blockIdx.x;
   long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const long long t_start = clock64();
 
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
-      uint32_t s = 0, ph = 0, itc = 0;
-      for (int L = b; L < a.n_items; L += G) {
-        int P, Q;
-        pair_of(L, a.nblocks, P, Q);
-        for (int sr = 0; sr < RB; ++sr) {
-        Sub it;
-        if (!sub_of(a, P, Q, sr, it)) continue;
-        mbar_wait(smem_u32(xr_empty), (itc & 1) ^ 1);
-        const int vt = min(2, a.col_tiles - 2 * it.rt);  // V tiles of this row tile
-        mbar_expect_tx(smem_u32(xr_full), row_bytes + vt * v_bytes);
-        bulk_g2s(smem_u32(xr_s), a.row_img + (int64_t)it.rt * (row_bytes / 4), row_bytes, smem_u32(xr_full));
-        bulk_g2s(smem_u32(vi_s), a.v_img + (int64_t)(2 * it.rt) * (v_bytes / 2), vt * v_bytes,
-                 smem_u32(xr_full));
-        ++itc;
-        const float* cimg = a.col_img + (int64_t)it.ct0 * (col_bytes / 4);
-        const __half* vimg = a.v_img + (int64_t)it.ct0 * (v_bytes / 2);
-        for (int ct = it.ct0; ct < it.ct1; ++ct) {
-          mbar_wait(smem_u32(&empty[s]), ph ^ 1);
-          uint8_t* st = stages + s * stage_bytes;
-          mbar_expect_tx(smem_u32(&full[s]), stage_bytes);
-          bulk_g2s(smem_u32(st), cimg, col_bytes, smem_u32(&full[s]));
-          bulk_g2s(smem_u32(st + col_bytes), vimg, v_bytes, smem_u32(&full[s]));
-          cimg += col_bytes / 4;
-          vimg += v_bytes / 2;
-          if (++s == (uint32_t)NS) { s = 0; ph ^= 1; }
+      TileSeq it;
+      it.begin(a);
+      uint32_t cs = 0, cph = 0, vs = 0, vph = 0, R = 0;
+      const uint32_t img_f = img_bytes / 4, vt_h = V_TILE_BYTES / 2;
+      while (it.ok) {
+        if (it.first_in_row()) {
+          const int I = it.I();
+          if (R >= 1) mbar_wait(smem_u32(xr_empty), (R - 1) & 1);
+          mbar_expect_tx(smem_u32(xr_full), img_bytes);
+          bulk_g2s(smem_u32(xr_s), a.row_img + (int64_t)I * img_f, img_bytes, smem_u32(xr_full));
+          const uint32_t vb = R & 1, u = R >> 1;
+          if (u >= 1) mbar_wait(smem_u32(&vi_empty[vb]), (u - 1) & 1);
+          mbar_expect_tx(smem_u32(&vi_full[vb]), V_TILE_BYTES);
+          bulk_g2s(smem_u32(vi_s + vb * V_TILE_BYTES), a.v_img + (int64_t)I * vt_h, V_TILE_BYTES,
+                   smem_u32(&vi_full[vb]));
+          ++R;
         }
-        }
+        const int J = it.J();
+        mbar_wait(smem_u32(&cempty[cs]), cph ^ 1);
+        mbar_expect_tx(smem_u32(&cfull[cs]), img_bytes);
+        bulk_g2s(smem_u32(cring + cs * img_bytes), a.col_img + (int64_t)J * img_f, img_bytes, smem_u32(&cfull[cs]));
+        if (++cs == (uint32_t)NSC) { cs = 0; cph ^= 1; }
+        mbar_wait(smem_u32(&vempty[vs]), vph ^ 1);
+        mbar_expect_tx(smem_u32(&vfull[vs]), V_TILE_BYTES);
+        bulk_g2s(smem_u32(vring + vs * V_TILE_BYTES), a.v_img + (int64_t)J * vt_h, V_TILE_BYTES,
+                 smem_u32(&vfull[vs]));
+        if (++vs == (uint32_t)NSV) { vs = 0; vph ^= 1; }
+        it.next();
       }
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    // per tile, in tensor-pipe order: direct(T), dist(T+2), mirror(T); the
-    // distance tile T+2 reuses the SK buffer of tile T once direct(T) is
-    // complete (the pipe does not order one MMA's TMEM-A reads against a
-    // later MMA's D writes, so that is an explicit k_empty wait)
-    const uint32_t idesc_d = make_idesc(BM, BN);
-    const uint32_t idesc_c32 = idesc_f16(BM, 2 * TN), idesc_c16 = idesc_f16(BM, TN);
-    const uint32_t idesc_m32 = idesc_f16(BN, 2 * TN), idesc_m16 = idesc_f16(BN, TN);
-    const uint32_t lbo_b = (BN / 8) * 128, lbo_v = (2 * TN / 8) * 128;
-    const uint32_t b_half16 = (BN * DK * 4) >> 4;
+    // per tile T: dist(T+1) (into the other S/K buffer, once the products of
+    // T-1 are done with it), then direct(T) and mirror(T) once the kappa warps
+    // have written K(T)
+    const uint32_t idesc_d = make_idesc(BT, BT);
+    const uint32_t idesc_n16 = idesc_f16(BT, TN);
+    const uint32_t idesc_m32 = idesc_f16(BT, 2 * TN) | IDESC_A_MN_MAJOR;
+    const uint32_t idesc_m16 = idesc_f16(BT, TN) | IDESC_A_MN_MAJOR;
+    const uint32_t lbo_b = (BT / 8) * 128, lbo_v = (2 * TN / 8) * 128;
+    const uint32_t half16 = (BT * DK * 4) >> 4;
     const int ksteps = DK / 8;
-    const uint64_t db0 = make_desc(smem_u32(stages), lbo_b, 128);
-    const uint64_t dv0 = make_desc(smem_u32(stages + col_bytes), lbo_v, 128);
-    const uint64_t dvi = make_desc(smem_u32(vi_s), lbo_v, 128);
-    const uint32_t vtile16 = v_bytes >> 4;
-    const uint32_t stage16 = stage_bytes >> 4;
+    const uint64_t dc0 = make_desc(smem_u32(cring), lbo_b, 128);
+    const uint64_t dv0 = make_desc(smem_u32(vring), lbo_v, 128);
+    const uint64_t dvi0 = make_desc(smem_u32(vi_s), lbo_v, 128);
+    // K^T, MN-major: core matrix = 8 points i x 8 points j (16 B rows along j);
+    // LBO = 128 B between i-groups (the K direction), SBO = 2 KB between j-groups
+    const uint64_t dks = make_desc(smem_u32(ks), 128, 2048);
+    const uint32_t img16 = img_bytes >> 4, vt16 = V_TILE_BYTES >> 4;
     const uint32_t kstep_b16 = (2 * lbo_b) >> 4, kstep_v16 = (2 * lbo_v) >> 4;
-    const uint32_t xa_hi = tmem + TMXA, xa_lo = tmem + TMXA + (uint32_t)DK;
-    const uint32_t kt1 = tmem + TMKT, kt2 = tmem + (16u << 16) + TMKT;
+    const uint32_t v2_16 = 256 >> 4;              // rows 16-31 of the V image (V2)
+    const uint32_t ks2_16 = KS_HALF >> 4;          // K2 half of the SMEM K
     const bool leader = elect_one();
-    uint32_t ds = 0, dph = 0, cs = 0, dbuf = 0, keph0 = 0, keph1 = 0, kfph0 = 0, kfph1 = 0;
-    uint32_t ob = 0, oph = 0, ktph = 0, jb = 0, jph = 0;
-    uint32_t itc = 0;
-    for (int L = b; L < a.n_items; L += G) {
-      int P, Q;
-      pair_of(L, a.nblocks, P, Q);
-      for (int sr = 0; sr < RB; ++sr) {
-      Sub it;
-      if (!sub_of(a, P, Q, sr, it)) continue;
-      const int J = it.ct1 - it.ct0;
-      const int first_mirror = it.first_mirror;   // tiles jj >= this are mirrored
-      mbar_wait(smem_u32(xr_full), itc & 1);
-      SYM_T(0, mbar_wait(smem_u32(xa_full), itc & 1));
-      ++itc;
+    uint32_t cs = 0, cph = 0, vs = 0, vph = 0, R = 0, K = 0, T = 0;
+    int rowc = -1;
+    TileSeq it;
+    it.begin(a);
+    auto dist = [&](const TileSeq& tt, uint32_t Tn) {
+      const uint32_t b = Tn & 1;
+      if (Tn >= 2) SYM_T(0, mbar_wait(smem_u32(&sk_empty[b]), ((Tn >> 1) - 1) & 1));
+      if (tt.first_in_row()) {
+        SYM_T(1, mbar_wait(smem_u32(xa_full), R & 1));
+        ++R;
+      }
+      SYM_T(2, mbar_wait(smem_u32(&cfull[cs]), cph));
       tc_fence_after();
-      auto dist = [&]() {   // S = A.B^T into SK[dbuf], A (row image) from TMEM, 3xTF32
-        uint32_t& keph = dbuf ? keph1 : keph0;
-        SYM_T(5, mbar_wait(smem_u32(&k_empty[dbuf]), keph ^ 1));
-        keph ^= 1;
-        SYM_T(5, mbar_wait(smem_u32(&full[ds]), dph));
-        tc_fence_after();
-        const uint32_t d_tm = tmem + TMSK(dbuf);
-        const uint64_t db = db0 + (uint64_t)(ds * stage16);
-        if (leader) {
+      if (leader) {
+        const uint32_t d_tm = tmem + TSK(b);
+        const uint64_t db = dc0 + (uint64_t)(cs * img16);
 #pragma unroll
-          for (int pass = 0; pass < 3; ++pass) {
-            const uint32_t a_p = pass == 0 ? xa_lo : xa_hi;
-            const uint64_t b_p = db + (pass == 1 ? b_half16 : 0u);
-            for (int ks = 0; ks < ksteps; ++ks)
-              mma_ts(d_tm, a_p + ks * 8, b_p + (uint64_t)(ks * kstep_b16), idesc_d, (pass | ks) != 0);
-          }
-          tc_commit(smem_u32(&s_full[dbuf]));
+        for (int pass = 0; pass < 3; ++pass) {
+          const uint32_t a_t = tmem + TXA + (pass == 0 ? (uint32_t)DK : 0u);
+          const uint64_t b_p = db + (pass == 1 ? half16 : 0u);
+          for (int k = 0; k < ksteps; ++k)
+            mma_ts(d_tm, a_t + k * 8, b_p + (uint64_t)(k * kstep_b16), idesc_d, (pass | k) != 0);
         }
-        __syncwarp();
-        if (++ds == (uint32_t)NS) { ds = 0; dph ^= 1; }
-        dbuf ^= 1;
-      };
-      uint32_t kbuf = dbuf;   // SK buffer of tile 0
-      dist();
-      if (J > 1) dist();
-      for (int jj = 0; jj < J; ++jj) {
-        uint32_t& kfph = kbuf ? kfph1 : kfph0;
-        SYM_T(1, mbar_wait(smem_u32(&k_full[kbuf]), kfph));
-        kfph ^= 1;
-        tc_fence_after();
-        SYM_T(2, mbar_wait(smem_u32(&o_empty[ob]), oph ^ 1));
-        tc_fence_after();
-        const uint64_t vb = dv0 + (uint64_t)(cs * stage16);
-        const uint32_t k1 = tmem + TMSK(kbuf) + 64, k2 = k1 + 32;
-        if (leader) {
-          // direct: O_I[:, 0:32] = K1.[V1 | V2];  O_I[:, 0:16] += K2.V1  (K = 64 = 4 x 16)
-#pragma unroll
-          for (int ks = 0; ks < BN / 16; ++ks)
-            mma16_ts(tmem + TMO(ob), k1 + ks * 8, vb + (uint64_t)(ks * kstep_v16), idesc_c32, ks != 0);
-#pragma unroll
-          for (int ks = 0; ks < BN / 16; ++ks)
-            mma16_ts(tmem + TMO(ob), k2 + ks * 8, vb + (uint64_t)(ks * kstep_v16), idesc_c16, 1);
-          tc_commit(smem_u32(&empty[cs]));
-          tc_commit(smem_u32(&o_full[ob]));
-          tc_commit(smem_u32(&k_empty[kbuf]));
-        }
-        __syncwarp();
-        ob ^= 1;
-        if (ob == 0) oph ^= 1;
-        // the next distance tile goes out before the mirror product: it only
-        // depends on direct(jj) finishing with this SK buffer, while the mirror
-        // waits for the transpose warps
-        if (jj + 2 < J) dist();
-        if (jj >= first_mirror) {
-          // mirror (M = 64, K = 128 points of I = 8 x 16): lanes 0-15 O_J = KT1.[V1 | V2],
-          // lanes 16-31 O_J[:, 0:16] = KT2.V1 (summed by the reader)
-          SYM_T(3, mbar_wait(smem_u32(kt_full), ktph));
-          tc_fence_after();
-          ktph ^= 1;
-          SYM_T(4, mbar_wait(smem_u32(&oj_empty[jb]), jph ^ 1));
-          tc_fence_after();
-          tacc[7] += 1;
-          const uint32_t oj1 = tmem + TMOJ(jb), oj2 = tmem + (16u << 16) + TMOJ(jb);
-          if (leader) {
-#pragma unroll
-            for (int ks = 0; ks < BM / 16; ++ks)
-              mma16_ts(oj1, kt1 + ks * 8, dvi + (uint64_t)((ks >> 2) * vtile16 + (ks & 3) * kstep_v16),
-                       idesc_m32, ks != 0);
-#pragma unroll
-            for (int ks = 0; ks < BM / 16; ++ks)
-              mma16_ts(oj2, kt2 + ks * 8, dvi + (uint64_t)((ks >> 2) * vtile16 + (ks & 3) * kstep_v16),
-                       idesc_m16, ks != 0);
-            tc_commit(smem_u32(kt_empty));
-            tc_commit(smem_u32(&oj_full[jb]));
-          }
-          __syncwarp();
-          jb ^= 1;
-          if (jb == 0) jph ^= 1;
-        }
-        kbuf ^= 1;
-        if (++cs == (uint32_t)NS) cs = 0;
+        tc_commit(smem_u32(&s_full[b]));
+        tc_commit(smem_u32(&cempty[cs]));
+        if (tt.last_in_row()) tc_commit(smem_u32(xa_empty));
       }
-      if (leader) tc_commit(smem_u32(xr_empty));
       __syncwarp();
+      if (++cs == (uint32_t)NSC) { cs = 0; cph ^= 1; }
+    };
+    if (it.ok) dist(it, 0);
+    while (it.ok) {
+      TileSeq nx = it;
+      nx.next();
+      if (nx.ok) dist(nx, T + 1);
+      const uint32_t b = T & 1;
+      if (it.first_in_row()) ++rowc;
+      if (it.first_in_item() && K >= 1) SYM_T(3, mbar_wait(smem_u32(acc_empty), (K - 1) & 1));
+      SYM_T(4, mbar_wait(smem_u32(&k_full[b]), (T >> 1) & 1));
+      tacc[7] += 1;
+      SYM_T(5, mbar_wait(smem_u32(&vfull[vs]), vph));
+      const bool mir = it.mirror();
+      if (mir) SYM_T(5, mbar_wait(smem_u32(&vi_full[rowc & 1]), (rowc >> 1) & 1));
+      tc_fence_after();
+      if (leader) {
+        const uint32_t oi = tmem + TOI(it.r), sk = tmem + TSK(b);
+        const uint64_t vb = dv0 + (uint64_t)(vs * vt16);
+        const uint32_t fresh = it.first_in_row() ? 1u : 0u;
+#pragma unroll
+        for (int k = 0; k < BT / 16; ++k)   // O_I (+)= K1 . V1
+          mma16_ts(oi, sk + 16 * k, vb + (uint64_t)(k * kstep_v16), idesc_n16, !(fresh && k == 0));
+#pragma unroll
+        for (int k = 0; k < BT / 16; ++k)   // O_I += K2 . V1
+          mma16_ts(oi, sk + 16 * k + 8, vb + (uint64_t)(k * kstep_v16), idesc_n16, 1);
+#pragma unroll
+        for (int k = 0; k < BT / 16; ++k)   // O_I += K1 . V2
+          mma16_ts(oi, sk + 16 * k, vb + (uint64_t)(v2_16 + k * kstep_v16), idesc_n16, 1);
+        if (mir) {
+          const uint32_t oj = tmem + TOJ(it.c);
+          const uint64_t vib = dvi0 + (uint64_t)((rowc & 1) * vt16);
+          const uint32_t jfresh = it.r == 0 ? 1u : 0u;
+#pragma unroll
+          for (int k = 0; k < BT / 16; ++k)   // O_J (+)= K1^T . [V1 | V2]
+            mma16_ss(oj, dks + (uint64_t)(16 * k), vib + (uint64_t)(k * kstep_v16), idesc_m32, !(jfresh && k == 0));
+#pragma unroll
+          for (int k = 0; k < BT / 16; ++k)   // O_J[:, 0:16] += K2^T . V1
+            mma16_ss(oj, dks + (uint64_t)(ks2_16 + 16 * k), vib + (uint64_t)(k * kstep_v16), idesc_m16, 1);
+        }
+        tc_commit(smem_u32(&vempty[vs]));
+        tc_commit(smem_u32(&sk_empty[b]));
+        tc_commit(smem_u32(ks_empty));
+        if (it.last_in_row()) tc_commit(smem_u32(&vi_empty[rowc & 1]));
+        if (it.last_in_item()) tc_commit(smem_u32(acc_full));
       }
+      __syncwarp();
+      if (++vs == (uint32_t)NSV) { vs = 0; vph ^= 1; }
+      if (it.last_in_item()) ++K;
+      it = nx;
+      ++T;
     }
-  } else if (warp >= KAPPA_WARP0 && warp < TRANS_WARP0) {
-    // ===================== kappa warps: S -> K, kappa^T staging =====================
-    // NUM_KAPPA_WARPS / 4 warps per TMEM lane quarter (SMSP), KC columns each
+  } else if (warp >= KAPPA_WARP0) {
+    // ===================== kappa warps: S -> K =====================
+    const int e = warp - KAPPA_WARP0;
     const int q = warp & 3;                        // TMEM lane quarter
-    const int slice = (warp - KAPPA_WARP0) >> 2;   // column slice of the 64-col tile
+    const int ch = e >> 2;                         // 32-column chunk of the tile
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const int i_loc = q * 32 + lane;
-    uint32_t T = 0, m = 0;                         // tiles / mirrored tiles seen
-    for (int L = b; L < a.n_items; L += G) {
-      int P, Q;
-      pair_of(L, a.nblocks, P, Q);
-      for (int sr = 0; sr < RB; ++sr) {
-      Sub it;
-      if (!sub_of(a, P, Q, sr, it)) continue;
-      const int J = it.ct1 - it.ct0;
-      const int first_mirror = it.first_mirror;
-      const int64_t my_row = (int64_t)it.rt * BM + i_loc;
-      for (int jj = 0; jj < J; ++jj, ++T) {
-        const bool mirror = jj >= first_mirror;
-        const uint32_t sb = T & 1;
-        SYM_T(0, mbar_wait(smem_u32(&s_full[sb]), (T >> 1) & 1));
-        tacc[7] += 1;
-        tc_fence_after();
-        const uint32_t sk = tmem + lane_base + TMSK(sb);
-        uint32_t v[KC];
-        if constexpr (KC == 32) {
-          tmem_ld32(sk + slice * KC, v);
+    const uint32_t ks_row = smem_u32(ks) + 16u * (uint32_t)i_loc + (uint32_t)(4 * ch) * 2048u;
+    TileSeq it;
+    it.begin(a);
+    uint32_t T = 0;
+    while (it.ok) {
+      const uint32_t b = T & 1;
+      SYM_T(0, mbar_wait(smem_u32(&s_full[b]), (T >> 1) & 1));
+      tacc[7] += 1;
+      tc_fence_after();
+      const uint32_t sk = tmem + lane_base + TSK(b) + 32u * ch;
+      uint32_t v[32];
+      SYM_T(1, tmem_ld32(sk, v); tmem_wait_ld());
+      const bool mir = it.mirror();
+      if (!mir) {
+        // diagonal tile: the same point on both sides has r2 = 0 exactly
+        const int e_diag = i_loc - 32 * ch;
+        if (__any_sync(0xffffffffu, e_diag >= 0 && e_diag < 32)) {
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            if (k == e_diag) v[k] = 0u;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const float sv = __uint_as_float(v[k]);
+        float kap;
+        // clamps written as selects so NaN inputs propagate
+        if (FAM == GP_FAMILY_RBF) {
+          kap = ex2_approx(min0_nan(sv));          // S = -log2(e) r2 / 2
         } else {
-          tmem_ld16(sk + slice * KC, reinterpret_cast<uint32_t (&)[16]>(v));
+          const float u = sqrt_approx(max0_nan(sv));   // S = 3 r2, u = sqrt(3) r
+          const float ex = ex2_approx(u * -kLog2e);
+          kap = fmaf(u, ex, ex);                   // (1 + sqrt3 r) e^{-sqrt3 r}
         }
+        v[k] = __float_as_uint(kap);
+      }
+      uint32_t p1[16], p2[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) split_pair(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]), p1[k], p2[k]);
+      // in place over this warp's own S columns: kstep 2ch at [32ch, +16), 2ch+1 at [32ch+16, +16)
+      tmem_st8(sk, p1);
+      tmem_st8(sk + 8, p2);
+      tmem_st8(sk + 16, p1 + 8);
+      tmem_st8(sk + 24, p2 + 8);
+      if (mir) {
+        // K^T operand: 8 consecutive j of point i = one 16-byte core-matrix row
+        if (T >= 1) SYM_T(2, mbar_wait(smem_u32(ks_empty), (T - 1) & 1));
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          sts128(ks_row + m * 2048u, p1[4 * m], p1[4 * m + 1], p1[4 * m + 2], p1[4 * m + 3]);
+          sts128(ks_row + KS_HALF + m * 2048u, p2[4 * m], p2[4 * m + 1], p2[4 * m + 2], p2[4 * m + 3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      }
+      SYM_T(3, tmem_wait_st());
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&k_full[b]));
+      it.next();
+      ++T;
+    }
+  } else {
+    // ===================== drain warps (4): row image -> TMEM, O_I / O_J -> sums =====================
+    const int q = warp & 3;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const int i_loc = q * 32 + lane;
+    uint32_t R = 0, K = 0;
+    auto copy_row = [&]() {
+      SYM_T(0, mbar_wait(smem_u32(xr_full), R & 1));
+      if (R >= 1) SYM_T(1, mbar_wait(smem_u32(xa_empty), (R - 1) & 1));
+      tc_fence_after();
+      const float* xr = reinterpret_cast<const float*>(xr_s);
+      for (int part = 0; part < 2; ++part)
+        for (int k0 = 0; k0 < DK; k0 += 8) {
+          uint32_t w[8];
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) w[kk] = __float_as_uint(xr[part * BT * DK + canon(i_loc, k0 + kk, BT)]);
+          tmem_st8(tmem + lane_base + TXA + part * DK + k0, w);
+        }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(smem_u32(xa_full));
+        mbar_arrive(smem_u32(xr_empty));
+      }
+      ++R;
+    };
+    int L = blockIdx.x;
+    const int G = gridDim.x, NB = a.nblocks;
+    if (L < a.n_items) copy_row();
+    while (L < a.n_items) {
+      int P, Q;
+      pair_of(L, NB, P, Q);
+      const int rows_in = min(RB, a.tiles - RB * P), cols_in = min(RB, a.tiles - RB * Q);
+      for (int r = 1; r < rows_in; ++r) copy_row();
+      const int Ln = L + G;
+      int Pn = -1, Qn = -1;
+      if (Ln < a.n_items) {
+        pair_of(Ln, NB, Pn, Qn);
+        copy_row();   // the next item's first row is needed before this item drains
+      }
+      SYM_T(2, mbar_wait(smem_u32(acc_full), K & 1));
+      tacc[7] += 1;
+      tc_fence_after();
+      for (int r = 0; r < rows_in; ++r) {
+        uint32_t o[16];
+        tmem_ld16(tmem + lane_base + TOI(r), o);
         tmem_wait_ld();
-        if (!mirror) {
-          const int64_t e_diag = my_row - ((int64_t)(it.ct0 + jj) * BN + slice * KC);
-          if (__any_sync(0xffffffffu, e_diag >= 0 && e_diag < KC)) {
+        float* ar = acci + (r * BT + i_loc) * TN;
 #pragma unroll
-            for (int e = 0; e < KC; ++e)
-              if (e == e_diag) v[e] = 0u;   // same point on both sides: r2 = 0 exactly
-          }
-        }
-#pragma unroll
-        for (int e = 0; e < KC; ++e) {
-          float sv = __uint_as_float(v[e]);
-          float kap;
-          if (FAM == GP_FAMILY_RBF) {
-            kap = ex2_approx(min0_nan(sv));  // S = -log2(e) r2 / 2
-          } else {
-            float u = sqrt_approx(max0_nan(sv));  // S = 3 r2, u = sqrt(3) r
-            float ex = ex2_approx(u * -kLog2e);
-            kap = fmaf(u, ex, ex);
-          }
-          v[e] = __float_as_uint(kap);
-        }
-#pragma unroll
-        for (int g8 = 0; g8 < KC / 16; ++g8) {
-          uint32_t p1[8], p2[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
-            split_pair(__uint_as_float(v[16 * g8 + 2 * k]), __uint_as_float(v[16 * g8 + 2 * k + 1]), p1[k], p2[k]);
-          tmem_st8(sk + 64 + slice * (KC / 2) + 8 * g8, p1);   // K over S, same buffer (own reads done)
-          tmem_st8(sk + 96 + slice * (KC / 2) + 8 * g8, p2);
-        }
-        if (mirror) {
-          // kappa^T (fp32) for the transpose warps
-          const uint32_t mb = m & 1;
-          SYM_T(2, mbar_wait(smem_u32(&ts_empty[mb]), ((m >> 1) & 1) ^ 1));
-          float* ktb = kt32 + mb * (64 * KT_LD);
-#pragma unroll
-          for (int e = 0; e < KC; ++e)
-            ktb[(KC * slice + e) * KT_LD + (i_loc ^ ((e & 1) << 1))] = __uint_as_float(v[e]);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&ts_full[mb]));
-          ++m;
-        }
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&k_full[sb]));
+        for (int c = 0; c < TN; ++c) ar[c] += __uint_as_float(o[c]);
       }
-      }
-    }
-  } else if (warp >= TRANS_WARP0 && warp < DRAIN_WARP0) {
-    // ===================== transpose warps (4): row image, K^T -> TMEM =====================
-    const int q = warp & 3;
-    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    const int i_loc = q * 32 + lane;
-    uint32_t itc = 0, m = 0, ktph = 0;
-    for (int L = b; L < a.n_items; L += G) {
-      int P, Q;
-      pair_of(L, a.nblocks, P, Q);
-      for (int sr = 0; sr < RB; ++sr) {
-      Sub it;
-      if (!sub_of(a, P, Q, sr, it)) continue;
-      const int J = it.ct1 - it.ct0;
-      const int first_mirror = it.first_mirror;
-      {
-        // row image -> TMEM (A operand of the distance product)
-        mbar_wait(smem_u32(xr_full), itc & 1);
-        const float* xr = reinterpret_cast<const float*>(xr_s);
-        for (int part = 0; part < 2; ++part)
-          for (int k0 = 0; k0 < DK; k0 += 8) {
-            uint32_t w[8];
+      for (int cc = (P == Q ? 1 : 0); cc < cols_in; ++cc) {
+        uint32_t o[32];
+        tmem_ld32(tmem + lane_base + TOJ(cc), o);
+        tmem_wait_ld();
+        const int64_t row = (int64_t)(RB * Q + cc) * BT + i_loc;
+        if (row < a.n) {
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
-              w[kk] = __float_as_uint(xr[part * BM * DK + canon(i_loc, k0 + kk, BM)]);
-            tmem_st8(tmem + lane_base + TMXA + part * DK + k0, w);
-          }
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(xa_full));
-        ++itc;
-      }
-      for (int jj = max(first_mirror, 0); jj < J; ++jj, ++m) {
-        const uint32_t mb = m & 1;
-        SYM_T(0, mbar_wait(smem_u32(&ts_full[mb]), (m >> 1) & 1));
-        tacc[7] += 1;
-        SYM_T(1, mbar_wait(smem_u32(kt_empty), ktph ^ 1));   // previous mirror product done with K^T
-        ktph ^= 1;
-        tc_fence_after();
-        const float* ktb = kt32 + mb * (64 * KT_LD);
-        // register r of the 16x256b.x4 fragment -> K^T row j = 16q + lane/4 + 8((r>>1)&1),
-        // points i = 64 part + 16(r>>2) + 4(lane%4) + 2(r&1) and i + 1
-#pragma unroll
-        for (int part = 0; part < 2; ++part) {
-          uint32_t w1[16], w2[16];
-#pragma unroll
-          for (int rr = 0; rr < 16; ++rr) {
-            const int j = 16 * q + (lane >> 2) + 8 * ((rr >> 1) & 1);
-            const int i = 64 * part + 16 * (rr >> 2) + 4 * (lane & 3) + 2 * (rr & 1);
-            const float2 x = *reinterpret_cast<const float2*>(&ktb[j * KT_LD + (i ^ ((j & 1) << 1))]);
-            split_pair(x.x, x.y, w1[rr], w2[rr]);
-          }
-          tmem_st16x256_x4(tmem + lane_base + TMKT + 32 * part, w1);
-          tmem_st16x256_x4(tmem + lane_base + (16u << 16) + TMKT + 32 * part, w2);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&ts_empty[mb]));   // SMEM reads done
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(kt_full));
-      }
-      }
-    }
-  } else if (warp >= DRAIN_WARP0) {
-    // ===================== drain warps (4): O_I -> registers, O_J -> fixed point =====================
-    const int q = warp & 3;
-    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    const int i_loc = q * 32 + lane;
-    uint32_t ob = 0, oph = 0, jb = 0, jph = 0;
-    float acc[TN];
-    for (int L = b; L < a.n_items; L += G) {
-      int P, Q;
-      pair_of(L, a.nblocks, P, Q);
-      for (int sr = 0; sr < RB; ++sr) {
-      Sub it;
-      if (!sub_of(a, P, Q, sr, it)) continue;
-      const int J = it.ct1 - it.ct0;
-      const int first_mirror = it.first_mirror;
-      const int64_t my_row = (int64_t)it.rt * BM + i_loc;
-#pragma unroll
-      for (int c = 0; c < TN; ++c) acc[c] = 0.f;
-      for (int jj = 0; jj < J; ++jj) {
-        {  // direct product of tile jj -> registers
-          SYM_T(0, mbar_wait(smem_u32(&o_full[ob]), oph));
-          tacc[7] += 1;
-          tc_fence_after();
-          {
-            uint32_t o[16];
-            tmem_ld16(tmem + lane_base + TMO(ob), o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int c = 0; c < TN; ++c) acc[c] += __uint_as_float(o[c]);
-            tmem_ld16(tmem + lane_base + TMO(ob) + TN, o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int c = 0; c < TN; ++c) acc[c] += __uint_as_float(o[c]);
-          }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&o_empty[ob]));
-          ob ^= 1;
-          if (ob == 0) oph ^= 1;
-        }
-        if (jj >= first_mirror) {  // mirror product of tile jj -> fixed-point sums
-          SYM_T(1, mbar_wait(smem_u32(&oj_full[jb]), jph));
-          tc_fence_after();
-          // lanes 0-15: [1.V1 | 1.V2], 16-31: [2.V1 | -]
-          float v[TN];
-          {
-            uint32_t o[16];
-            tmem_ld16(tmem + lane_base + TMOJ(jb), o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int c = 0; c < TN; ++c) v[c] = __uint_as_float(o[c]);
-            tmem_ld16(tmem + lane_base + TMOJ(jb) + TN, o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int c = 0; c < TN; ++c) v[c] += lane < 16 ? __uint_as_float(o[c]) : 0.f;
-          }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&oj_empty[jb]));
-          jb ^= 1;
-          if (jb == 0) jph ^= 1;
-#pragma unroll
-          for (int c = 0; c < TN; ++c) v[c] += __shfl_xor_sync(0xffffffffu, v[c], 16);
-          // accumulate into the item's SMEM block (rows 16q + lane%16 of column tile J - CB Q:
-          // this warp owns them, so no cross-warp synchronisation)
-          {
-            const int cidx = it.ct0 + jj - CB * Q;
-            float* arow = accq + ((cidx * 64) + q * 16 + (lane & 15)) * ACC_LD + (lane < 16 ? 0 : TN / 2);
-#pragma unroll
-            for (int c = 0; c < TN / 2; ++c) arow[c] += lane < 16 ? v[c] : v[c + TN / 2];
+          for (int c = 0; c < TN; ++c) {
+            if (c < a.t) contribute(a, row, c, __uint_as_float(o[c]) + __uint_as_float(o[c + TN]), expo_s[c]);
           }
         }
       }
-      if (my_row < a.n) {
-#pragma unroll
-        for (int c = 0; c < TN; ++c)
-          if (c < a.t) contribute(a, my_row, c, acc[c], expo_s[c]);
-      }
-      }
-      // item done: reduce block Q's mirror outputs (this warp's 16 rows of
-      // each column tile) into the fixed-point accumulator, and clear them
+      tc_fence_before();
       __syncwarp();
-#pragma unroll 1
-      for (int k = 0; k < CB / 2; ++k) {
-        const int pidx = k * 32 + lane;           // (column tile, row) pair
-        const int cidx = pidx >> 4, jl = q * 16 + (pidx & 15);
-        float* arow = accq + (cidx * 64 + jl) * ACC_LD;
-        const int64_t row = (int64_t)(CB * Q + cidx) * BN + jl;
+      if (lane == 0) mbar_arrive(smem_u32(acc_empty));
+      ++K;
+      if (Pn != P) {
+        // leaving row block P: its carried O_I partials go to the global sums
+        for (int r = 0; r < rows_in; ++r) {
+          const int64_t row = (int64_t)(RB * P + r) * BT + i_loc;
+          float* ar = acci + (r * BT + i_loc) * TN;
 #pragma unroll
-        for (int c = 0; c < TN; ++c) {
-          const float val = arow[c];
-          arow[c] = 0.f;
-          if (c < a.t && row < a.n && val != 0.f) contribute(a, row, c, val, expo_s[c]);
+          for (int c = 0; c < TN; ++c) {
+            const float v = ar[c];
+            ar[c] = 0.f;
+            if (c < a.t && row < a.n) contribute(a, row, c, v, expo_s[c]);
+          }
         }
       }
-      __syncwarp();
+      L = Ln;
     }
   }
 
@@ -646,7 +536,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == DRAIN_WARP0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
@@ -712,29 +602,30 @@ __global__ void sym_finalize_kernel(const unsigned long long* __restrict__ acc, 
 }
 
 struct Plan {
-  int DK, row_tiles, col_tiles, nblocks, n_items, nstages;
+  int DK, tiles, nblocks, n_items, nsc, nsv;
   int64_t acc_ld;
-  size_t row_img_bytes, col_img_bytes, v_img_bytes, acc_bytes, bad_bytes, smem;
+  size_t img_bytes_all, v_img_bytes, acc_bytes, bad_bytes, smem;
 };
 
 static Plan make_plan(const gp_kv_desc* d) {
   Plan p;
   p.DK = (d->d + 2 + 7) / 8 * 8;
-  p.row_tiles = (int)((d->n_rows + BM - 1) / BM);
-  p.col_tiles = (int)((d->n_cols + BN - 1) / BN);  // row tile I starts at column tile 2I
-  p.nblocks = (p.row_tiles + RB - 1) / RB;
+  p.tiles = (int)((d->n_rows + BT - 1) / BT);
+  p.nblocks = (p.tiles + RB - 1) / RB;
   p.n_items = p.nblocks * (p.nblocks + 1) / 2;
-  p.acc_ld = (int64_t)p.row_tiles * BM;
-  p.row_img_bytes = (size_t)p.row_tiles * 2 * BM * p.DK * 4;
-  p.col_img_bytes = (size_t)p.col_tiles * 2 * BN * p.DK * 4;
-  p.v_img_bytes = (size_t)p.col_tiles * V_TILE_BYTES;
+  p.acc_ld = (int64_t)p.tiles * BT;
+  const size_t img = 2u * BT * p.DK * 4u;
+  p.img_bytes_all = (size_t)p.tiles * img;
+  p.v_img_bytes = (size_t)p.tiles * V_TILE_BYTES;
   p.acc_bytes = (size_t)TN * p.acc_ld * 8;
   p.bad_bytes = (size_t)p.acc_ld * 4;
-  const size_t fixed = 2 * KT32_BYTES + 2u * BM * p.DK * 4 + 2 * V_TILE_BYTES + ACCQ_BYTES + 640;
-  const size_t stage_b = 2u * BN * p.DK * 4 + V_TILE_BYTES;
   const size_t budget = 227 * 1024;
-  p.nstages = fixed >= budget ? 0 : (int)std::min<size_t>(4, (budget - fixed) / stage_b);
-  p.smem = fixed + p.nstages * stage_b;
+  const size_t fixed = KS_BYTES + img + 2 * V_TILE_BYTES + ACCI_BYTES + BAR_BYTES;
+  p.nsc = 2;
+  p.nsv = 0;
+  for (int nv = 3; nv >= 2; --nv)
+    if (fixed + p.nsc * img + nv * V_TILE_BYTES <= budget) { p.nsv = nv; break; }
+  p.smem = fixed + p.nsc * img + p.nsv * V_TILE_BYTES;
   return p;
 }
 
@@ -749,15 +640,15 @@ bool kv_sym_supported(const gp_kv_desc* d, int t) {
   if (d->d < 1 || d->d + 2 > 32) return false;   // row image hi|lo must fit 64 TMEM columns
   if (d->Xr != d->Xc || d->ldr != d->ldc || d->n_rows != d->n_cols || d->n_rows < 1) return false;
   if (d->self_offset != 0 || (d->diag_offset != 0 && d->diag_offset >= 0)) return false;
-  return tcs::make_plan(d).nstages >= 3;
+  return tcs::make_plan(d).nsv >= 2;
 }
 
 size_t kv_sym_workspace(const gp_kv_desc* d, int t) {
   if (!kv_sym_supported(d, t)) return 0;
   tcs::Plan p = tcs::make_plan(d);
   using tcs::align256;
-  return align256(p.row_img_bytes) + align256(p.col_img_bytes) + align256(p.v_img_bytes) +
-         align256(p.acc_bytes) + align256(p.bad_bytes) + 256 * sizeof(double) + 3 * 64 * sizeof(double);
+  return 2 * align256(p.img_bytes_all) + align256(p.v_img_bytes) + align256(p.acc_bytes) +
+         align256(p.bad_bytes) + 256 * sizeof(double) + 3 * 64 * sizeof(double);
 }
 
 int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out, int64_t ldo, void* ws,
@@ -768,8 +659,8 @@ int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* ou
   GP_REQUIRE(ws != nullptr && ws_bytes >= need, "gp_kv(symmetric): workspace of %zu bytes required, %zu given",
              need, ws_bytes);
   char* w = static_cast<char*>(ws);
-  float* row_img = reinterpret_cast<float*>(w); w += align256(p.row_img_bytes);
-  float* col_img = reinterpret_cast<float*>(w); w += align256(p.col_img_bytes);
+  float* row_img = reinterpret_cast<float*>(w); w += align256(p.img_bytes_all);
+  float* col_img = reinterpret_cast<float*>(w); w += align256(p.img_bytes_all);
   __half* v_img = reinterpret_cast<__half*>(w); w += align256(p.v_img_bytes);
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(w); w += align256(p.acc_bytes);
   int* bad = reinterpret_cast<int*>(w); w += align256(p.bad_bytes);
@@ -783,16 +674,15 @@ int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* ou
   GP_CUDA_TRY(cudaMemsetAsync(bad, 0, p.bad_bytes, st));
   sym_scale_kernel<<<TN, 256, 0, st>>>(V, ldv, n, t, expo, vscale, inv_scale);
   GP_LAUNCH_CHECK();
-  if (int rc = tc::distance_images(desc->Xr, desc->ldr, n, desc->Xc, desc->ldc, n, desc->d, p.DK, BM, BN, c,
+  if (int rc = tc::distance_images(desc->Xr, desc->ldr, n, desc->Xc, desc->ldc, n, desc->d, p.DK, BT, BT, c,
                                    mean, row_img, col_img, st))
     return rc;
-  {
-    if (int rc = tc::v_images16(V, ldv, t, n, vscale, v_img, p.col_tiles, st)) return rc;
-  }
+  // the 128-point V image is two consecutive 64-point tile images
+  if (int rc = tc::v_images16(V, ldv, t, n, vscale, v_img, 2 * (int64_t)p.tiles, st)) return rc;
   Args a;
   a.row_img = row_img; a.col_img = col_img; a.v_img = v_img; a.DK = p.DK;
-  a.n = n; a.row_tiles = p.row_tiles; a.col_tiles = p.col_tiles; a.nblocks = p.nblocks; a.n_items = p.n_items;
-  a.nstages = p.nstages; a.t = t;
+  a.n = n; a.tiles = p.tiles; a.nblocks = p.nblocks; a.n_items = p.n_items;
+  a.nsc = p.nsc; a.nsv = p.nsv; a.t = t;
   a.expo = expo; a.acc = acc; a.acc_ld = p.acc_ld; a.bad = bad;
   a.prof = nullptr;
   int grid = std::min(p.n_items, num_sms());
@@ -802,12 +692,12 @@ int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* ou
   if (pe && *pe == '1') GP_CUDA_TRY(cudaMalloc(&a.prof, (size_t)grid * (NTHREADS / 32) * 8 * sizeof(long long)));
   kern<<<grid, NTHREADS, p.smem, st>>>(a);
   GP_LAUNCH_CHECK();
-  if (a.prof) {   // diagnostic only: per-role average cycles per tile, CTA-averaged
+  if (a.prof) {   // diagnostic only: per-role average cycles per event, CTA-averaged
     std::vector<long long> h((size_t)grid * (NTHREADS / 32) * 8);
     GP_CUDA_TRY(cudaStreamSynchronize(st));
     GP_CUDA_TRY(cudaMemcpy(h.data(), a.prof, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
     cudaFree(a.prof);
-    for (int wi : {1, 4, 8, TRANS_WARP0, DRAIN_WARP0}) {
+    for (int wi : {1, DRAIN_WARP0, KAPPA_WARP0, KAPPA_WARP0 + 15}) {
       double s[8] = {0};
       for (int cta = 0; cta < grid; ++cta)
         for (int k = 0; k < 8; ++k) s[k] += (double)h[((size_t)cta * (NTHREADS / 32) + wi) * 8 + k];
