@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", default="M1e6")
     ap.add_argument("--points", type=int, default=0, help="override n (testing only)")
-    ap.add_argument("--algo", type=int, default=0, help="0 auto, 1 SIMT, 2 tcgen05")
+    ap.add_argument("--algo", type=int, default=0, help="0 auto, 1 SIMT, 2 tcgen05 row-tiled, 3 tcgen05 symmetric")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -289,7 +289,16 @@ def run_ours(args):
     flops_launch = (r1 - r0) * n * (2 * w.d + 2 * T_RHS)
     kv_ms_mean = statistics.mean(kv_ms)
     tflops = flops_launch / (kv_ms_mean / 1e3) / 1e12
-    entries_per_s = (r1 - r0) * n / (kv_ms_mean / 1e3)
+    # the symmetric kernel (the default for the whole square operator, d <= 14)
+    # evaluates each unordered pair of points once: T(T+1)/2 tiles of 128 x 128
+    sym = (world == 1 and args.algo in (0, 3) and w.d + 2 <= 16
+           and os.environ.get("GP_KV_NO_SYM", "0") != "1")
+    if sym:
+        tiles = (n + 127) // 128
+        entries_launch = tiles * (tiles + 1) // 2 * 128 * 128
+    else:
+        entries_launch = (r1 - r0) * n
+    entries_per_s = entries_launch / (kv_ms_mean / 1e3)
     mufu_per_entry = 2 if w.family == "matern32" else 1
     sm_mhz_max = clk.summary().get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
     sfu_peak_entries = 148 * 16 * sm_mhz_max * 1e6 / mufu_per_entry
@@ -337,8 +346,12 @@ def run_ours(args):
                              "bound": "sfu", "achieved": entries_per_s / 1e9,
                              "peak": sfu_peak_entries / 1e9, "unit": "Gentries/s",
                              "frac": entries_per_s / sfu_peak_entries,
-                             "note": f"{mufu_per_entry} MUFU op(s)/entry, 148 SM x 16/clk at "
-                                     f"{sm_mhz_max} MHz"}},
+                             "kernel": "kv_sym_kernel" if sym else "kv_tc_kernel",
+                             "entries_per_launch": entries_launch,
+                             "note": f"{mufu_per_entry} MUFU op(s)/evaluated entry, 148 SM x 16/clk at "
+                                     f"{sm_mhz_max} MHz"
+                                     + ("; symmetric kernel: each unordered pair evaluated once "
+                                        "(~n^2/2 entries for the n^2-entry operator)" if sym else "")}},
             "clocks": clocks,
             "gpu_launches": int(launches),
             "e2e": e2e,

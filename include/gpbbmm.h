@@ -65,14 +65,15 @@ int gp_prescale(const double* X, int64_t n, int d, int64_t ldx,
  * Replaces kernels.training_mvm_oracle + partition.partitioned_mvm
  * (kernels.py:293-316, partition.py:186-241) and, with diag_offset = -1,
  * kernels.cross_mvm_oracle (kernels.py:319-325, predictor.py:130-131).
- * Xr/Xc are prescaled fp32 points (gp_prescale). Per-row reduction order is
- * fixed by n_cols alone, so results are bitwise independent of how rows are
- * sharded across devices (test_partition.py:92-102).
+ * Xr/Xc are prescaled fp32 points (gp_prescale). The row-tiled kernels' per-row
+ * reduction order is fixed by n_cols alone, so their results are bitwise
+ * independent of how rows are sharded across devices (test_partition.py:92-102).
  * `algo`: 0 = auto, 1 = SIMT FFMA kernel, 2 = tcgen05 kernel, 3 = symmetric
  * tcgen05 kernel (whole square operator only: Xr == Xc, all rows, self_offset
  * 0; each unordered pair evaluated once, contributions summed in 64-bit fixed
  * point, so the result is bitwise reproducible but not bitwise equal to
- * algo 2). Auto picks 3 for the whole square operator, else 2 (t <= 16). */
+ * algo 2). Auto picks 3 for the whole square operator when d <= 14 and
+ * t <= 16 (GP_KV_NO_SYM=1 opts out), else 2 (t <= 16) or the wide kernel. */
 typedef struct gp_kv_desc {
   int32_t family;        /* GP_FAMILY_* */
   int32_t d;             /* input dimension */

@@ -458,10 +458,13 @@ static bool use_tc(const gp_kv_desc* d, int t) {
   if (d->algo == 2 || d->algo == 3) return true;
   return gp_has_tcgen05() && gp::kv_tc_supported(d, t);
 }
-// auto: the symmetric kernel whenever the call is the whole square operator
+// auto: the symmetric kernel whenever the call is the whole square training
+// operator (each unordered pair evaluated once); GP_KV_NO_SYM=1 opts out
 static bool use_sym(const gp_kv_desc* d, int t) {
   if (d->algo == 3) return true;
-  return d->algo == 0 && gp_has_tcgen05() && gp::kv_sym_supported(d, t) && getenv("GP_KV_AUTO_SYM") != nullptr;
+  if (d->algo != 0 || !gp_has_tcgen05() || !gp::kv_sym_supported(d, t)) return false;
+  const char* e = getenv("GP_KV_NO_SYM");
+  return !(e && *e == '1');
 }
 
 size_t gp_kv_workspace_bytes(const gp_kv_desc* desc, int t) {

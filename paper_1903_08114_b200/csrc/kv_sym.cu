@@ -34,8 +34,9 @@
 // bitwise reproducible run to run and independent of the CTA schedule, like
 // the reference's partition-count independence (test_partition.py:92-102).
 //
-// Warp roles: 0 TMA producer, 1 MMA issuer, 2-5 drain (+ row image -> TMEM,
-// warp 2 allocates TMEM), 6-21 kappa (S -> K, 32 rows x 32 columns each).
+// Warp roles: 0 TMA producer (column tiles), 1 MMA issuer (also copies each
+// row image SMEM -> TMEM with tcgen05.cp), 2-5 drain (warp 2 allocates TMEM),
+// 6-21 kappa (S -> K, 32 rows x 32 columns each), 22 TMA producer (row tiles).
 //
 // Reference semantics: kernels.py:225-244 (kappa), :293-316 (rows of K̂ incl.
 // the sigma^2 diagonal), partition.py:224-241 (row-block products).
@@ -57,20 +58,23 @@ constexpr int BT = 128;   // points per tile, both sides (UMMA M of both product
 constexpr int TN = 16;    // right-hand sides
 constexpr int RB = 4;     // tiles per block side: an item is a 4 x 4 block of tiles
 constexpr int DRAIN_WARP0 = 2, KAPPA_WARP0 = 6, NUM_KAPPA_WARPS = 16;
-constexpr int NTHREADS = 32 * (KAPPA_WARP0 + NUM_KAPPA_WARPS);
+constexpr int ROW_WARP = KAPPA_WARP0 + NUM_KAPPA_WARPS;   // row image + V_I loader
+constexpr int NTHREADS = 32 * (ROW_WARP + 1);
 constexpr uint32_t KS_HALF = BT * BT * 2;            // K1 (or K2) of one tile, fp16 MN-major
 constexpr uint32_t KS_BYTES = 2 * KS_HALF;
 constexpr uint32_t V_TILE_BYTES = 2u * TN * BT * 2u;  // [V1 | V2] of one tile, 32 x 128 fp16
 constexpr uint32_t ACCI_BYTES = RB * BT * TN * 4u;    // O_I carried over items of one row block
+constexpr uint32_t STAGE_BYTES = TN * BT * 8u;       // fixed-point sums of one 128-row block
 constexpr uint32_t BAR_BYTES = 1024;
 
-// TMEM columns (512): S/K buffers 2 x 128 | O_I 4 x 16 | O_J 4 x 32 | row image 2 DK
+// TMEM columns (512): S/K buffers 2 x 128 | O_I 2 x 32 (by row) | O_J 4 x 32 |
+// row image 2 x 2 DK (by row, DK <= 16)
 // S (fp32) lands in [128b, 128b + 128); the kappa warps overwrite it in place
 // with K1 | K2 (fp16 pairs along j): kstep ks (16 points) at 16 ks (K1), 16 ks + 8 (K2)
 __device__ __forceinline__ uint32_t TSK(uint32_t b) { return 128u * b; }
-__device__ __forceinline__ uint32_t TOI(int r) { return 256u + 16u * (uint32_t)r; }
+__device__ __forceinline__ uint32_t TOI(uint32_t rb) { return 256u + 32u * rb; }
 __device__ __forceinline__ uint32_t TOJ(int c) { return 320u + 32u * (uint32_t)c; }
-constexpr uint32_t TXA = 448;
+__device__ __forceinline__ uint32_t TXA(uint32_t xb) { return 448u + 32u * xb; }
 
 struct Args {
   const float* row_img;   // [tiles][2][BT*DK] tf32 hi|lo (A of the distance product)
@@ -86,16 +90,36 @@ struct Args {
   long long* prof;                  // optional per-warp phase cycle counters (GP_SYM_PROF=1)
 };
 
+// per-role wait counters for diagnosis: build with -DGP_SYM_PROF_BUILD=1 and
+// run with GP_SYM_PROF=1 (compiled out by default: the counters cost registers)
+#ifndef GP_SYM_PROF_BUILD
+#define GP_SYM_PROF_BUILD 0
+#endif
+#if GP_SYM_PROF_BUILD
 #define SYM_T(slot, ...)                                  \
   do {                                                    \
     const long long _t0 = a.prof ? clock64() : 0;         \
     __VA_ARGS__;                                          \
     if (a.prof) tacc[slot] += clock64() - _t0;            \
   } while (0)
+#define SYM_COUNT() (tacc[7] += 1)
+#else
+#define SYM_T(slot, ...) do { __VA_ARGS__; } while (0)
+#define SYM_COUNT() ((void)0)
+#endif
 
-__device__ __forceinline__ void red_add_u64(unsigned long long* p, long long v) {
-  asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// TMA bulk reduce-add of a contiguous fixed-point block into the global sums
+__device__ __forceinline__ void bulk_red_u64(void* gdst, uint32_t ssrc, uint32_t bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u64 [%0], [%1], %2;" ::"l"(gdst), "r"(ssrc),
+               "r"(bytes)
+               : "memory");
 }
+// SMEM (canonical K-major, no swizzle) -> TMEM, 128 lanes x 8 fp32 columns;
+// ordered with the tcgen05.mma of the same thread (one pipeline, issue order)
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+__device__ __forceinline__ void drain_bar() { asm volatile("bar.sync 2, 128;" ::: "memory"); }
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(x), "r"(y), "r"(z), "r"(w)
                : "memory");
@@ -151,25 +175,6 @@ struct TileSeq {
   __device__ int J() const { return RB * Q + c; }
 };
 
-// v * 2^E as a (truncated) signed 64-bit integer on the integer pipes (the
-// F2I.S64 conversion would run on the XU pipe the kappa epilogue saturates).
-// Exact for |v| 2^E >= 2^23; smaller magnitudes lose their sub-unit fraction.
-__device__ __forceinline__ long long fixed_point(float v, int E) {
-  const uint32_t bits = __float_as_uint(v);
-  const int sh = (int)((bits >> 23) & 0xFFu) - 150 + E;      // |v| 2^E = m 2^sh
-  const uint64_t m = (uint64_t)((bits & 0x7FFFFFu) | 0x800000u);
-  uint64_t mag = sh >= 0 ? (m << min(sh, 39)) : (sh > -24 ? (m >> -sh) : 0ull);
-  if (((bits >> 23) & 0xFFu) == 0u) mag = 0ull;                 // zero / denormal
-  return (bits >> 31) ? -(long long)mag : (long long)mag;
-}
-__device__ __forceinline__ void contribute(const Args& a, int64_t row, int c, float v, int E) {
-  if (!(fabsf(v) < INFINITY)) {
-    a.bad[row] = 1;
-    return;
-  }
-  red_add_u64(a.acc + (int64_t)c * a.acc_ld + row, fixed_point(v, E));
-}
-
 template <int FAM>
 __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -182,7 +187,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
   uint8_t* cring = vi_s + 2 * V_TILE_BYTES;            // [NSC] column images
   uint8_t* vring = cring + NSC * img_bytes;            // [NSV] V_J images
   float* acci = reinterpret_cast<float*>(vring + NSV * V_TILE_BYTES);   // [RB][BT][TN]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(acci) + ACCI_BYTES);
+  unsigned long long* stage = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(acci) + ACCI_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stage) + 2 * STAGE_BYTES);
   uint64_t* cfull = bars;               // [NSC] column image landed           TMA -> MMA
   uint64_t* cempty = cfull + NSC;       // [NSC] distance product done         MMA -> TMA
   uint64_t* vfull = cempty + NSC;       // [NSV] V_J landed                    TMA -> MMA
@@ -193,17 +199,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
   uint64_t* k_full = s_full + 2;        // [2]   K written (TMEM + SMEM)       kappa -> MMA
   uint64_t* sk_empty = k_full + 2;      // [2]   products done with buffer b   MMA -> MMA
   uint64_t* ks_empty = sk_empty + 2;    //       products done with the SMEM K MMA -> kappa
-  uint64_t* xr_full = ks_empty + 1;     //       row image landed              TMA -> drain
-  uint64_t* xr_empty = xr_full + 1;     //       row image consumed            drain -> TMA
-  uint64_t* xa_full = xr_empty + 1;     //       row image in TMEM             drain -> MMA
-  uint64_t* xa_empty = xa_full + 1;     //       distance products of the row done  MMA -> drain
-  uint64_t* acc_full = xa_empty + 1;    //       item's products done          MMA -> drain
-  uint64_t* acc_empty = acc_full + 1;   //       O_I / O_J read                drain -> MMA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
-  int* expo_s = reinterpret_cast<int*>(tmem_slot + 4);   // [TN] fixed-point exponents
+  uint64_t* xr_full = ks_empty + 1;     //       row image landed              TMA -> MMA
+  uint64_t* xr_empty = xr_full + 1;     //       row image copied into TMEM    MMA -> TMA
+  uint64_t* oi_full = xr_empty + 1;     // [2]   row's direct products done    MMA -> drain
+  uint64_t* oi_empty = oi_full + 2;     // [2]   O_I buffer read               drain -> MMA
+  uint64_t* oj_full = oi_empty + 2;     //       item's mirror products done   MMA -> drain
+  uint64_t* oj_empty = oj_full + 1;     // [RB]  O_J[c] read                   drain -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(oj_empty + RB);
+  float* scale_s = reinterpret_cast<float*>(tmem_slot + 4);   // [TN] fixed-point scales 2^expo_c
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x < TN) expo_s[threadIdx.x] = a.expo[threadIdx.x];
+  if (threadIdx.x < TN) scale_s[threadIdx.x] = ldexpf(1.0f, a.expo[threadIdx.x]);
   for (int i = threadIdx.x; i < (int)(ACCI_BYTES / 4); i += blockDim.x) acci[i] = 0.f;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSC; ++s) {
@@ -223,11 +229,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
     }
     mbar_init(smem_u32(ks_empty), 1);
     mbar_init(smem_u32(xr_full), 1);
-    mbar_init(smem_u32(xr_empty), 4);
-    mbar_init(smem_u32(xa_full), 4);
-    mbar_init(smem_u32(xa_empty), 1);
-    mbar_init(smem_u32(acc_full), 1);
-    mbar_init(smem_u32(acc_empty), 4);
+    mbar_init(smem_u32(xr_empty), 1);
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(smem_u32(&oi_full[q]), 1);
+      mbar_init(smem_u32(&oi_empty[q]), 4);
+    }
+    mbar_init(smem_u32(oj_full), 1);
+    for (int c = 0; c < RB; ++c) mbar_init(smem_u32(&oj_empty[c]), 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == DRAIN_WARP0) {
@@ -242,25 +250,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
   const long long t_start = clock64();
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer: column tiles =====================
     if (lane == 0) {
       TileSeq it;
       it.begin(a);
-      uint32_t cs = 0, cph = 0, vs = 0, vph = 0, R = 0;
+      uint32_t cs = 0, cph = 0, vs = 0, vph = 0;
       const uint32_t img_f = img_bytes / 4, vt_h = V_TILE_BYTES / 2;
       while (it.ok) {
-        if (it.first_in_row()) {
-          const int I = it.I();
-          if (R >= 1) mbar_wait(smem_u32(xr_empty), (R - 1) & 1);
-          mbar_expect_tx(smem_u32(xr_full), img_bytes);
-          bulk_g2s(smem_u32(xr_s), a.row_img + (int64_t)I * img_f, img_bytes, smem_u32(xr_full));
-          const uint32_t vb = R & 1, u = R >> 1;
-          if (u >= 1) mbar_wait(smem_u32(&vi_empty[vb]), (u - 1) & 1);
-          mbar_expect_tx(smem_u32(&vi_full[vb]), V_TILE_BYTES);
-          bulk_g2s(smem_u32(vi_s + vb * V_TILE_BYTES), a.v_img + (int64_t)I * vt_h, V_TILE_BYTES,
-                   smem_u32(&vi_full[vb]));
-          ++R;
-        }
         const int J = it.J();
         mbar_wait(smem_u32(&cempty[cs]), cph ^ 1);
         mbar_expect_tx(smem_u32(&cfull[cs]), img_bytes);
@@ -274,13 +270,39 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
         it.next();
       }
     }
+  } else if (warp == ROW_WARP) {
+    // ===================== TMA producer: row tiles =====================
+    // a separate thread, so the next row image is fetched as soon as the
+    // previous one is in TMEM instead of behind the column ring
+    if (lane == 0) {
+      TileSeq it;
+      it.begin(a);
+      uint32_t R = 0;
+      const uint32_t img_f = img_bytes / 4, vt_h = V_TILE_BYTES / 2;
+      while (it.ok) {
+        const int I = it.I();
+        if (R >= 1) mbar_wait(smem_u32(xr_empty), (R - 1) & 1);
+        mbar_expect_tx(smem_u32(xr_full), img_bytes);
+        bulk_g2s(smem_u32(xr_s), a.row_img + (int64_t)I * img_f, img_bytes, smem_u32(xr_full));
+        const uint32_t vb = R & 1, u = R >> 1;
+        if (u >= 1) mbar_wait(smem_u32(&vi_empty[vb]), (u - 1) & 1);
+        mbar_expect_tx(smem_u32(&vi_full[vb]), V_TILE_BYTES);
+        bulk_g2s(smem_u32(vi_s + vb * V_TILE_BYTES), a.v_img + (int64_t)I * vt_h, V_TILE_BYTES,
+                 smem_u32(&vi_full[vb]));
+        ++R;
+        // to the first tile of the next row
+        const int r0 = it.r;
+        const int L0 = it.L;
+        while (it.ok && it.r == r0 && it.L == L0) it.next();
+      }
+    }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     // per tile T: dist(T+1) (into the other S/K buffer, once the products of
     // T-1 are done with it), then direct(T) and mirror(T) once the kappa warps
     // have written K(T)
     const uint32_t idesc_d = make_idesc(BT, BT);
-    const uint32_t idesc_n16 = idesc_f16(BT, TN);
+    const uint32_t idesc_n16 = idesc_f16(BT, TN), idesc_n32 = idesc_f16(BT, 2 * TN);
     const uint32_t idesc_m32 = idesc_f16(BT, 2 * TN) | IDESC_A_MN_MAJOR;
     const uint32_t idesc_m16 = idesc_f16(BT, TN) | IDESC_A_MN_MAJOR;
     const uint32_t lbo_b = (BT / 8) * 128, lbo_v = (2 * TN / 8) * 128;
@@ -292,9 +314,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
     // K^T, MN-major: core matrix = 8 points i x 8 points j (16 B rows along j);
     // LBO = 128 B between i-groups (the K direction), SBO = 2 KB between j-groups
     const uint64_t dks = make_desc(smem_u32(ks), 128, 2048);
+    const uint64_t dxr0 = make_desc(smem_u32(xr_s), lbo_b, 128);   // row image, K-major like the column image
     const uint32_t img16 = img_bytes >> 4, vt16 = V_TILE_BYTES >> 4;
     const uint32_t kstep_b16 = (2 * lbo_b) >> 4, kstep_v16 = (2 * lbo_v) >> 4;
-    const uint32_t v2_16 = 256 >> 4;              // rows 16-31 of the V image (V2)
     const uint32_t ks2_16 = KS_HALF >> 4;          // K2 half of the SMEM K
     const bool leader = elect_one();
     uint32_t cs = 0, cph = 0, vs = 0, vph = 0, R = 0, K = 0, T = 0;
@@ -305,9 +327,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       const uint32_t b = Tn & 1;
       if (Tn >= 2) SYM_T(0, mbar_wait(smem_u32(&sk_empty[b]), ((Tn >> 1) - 1) & 1));
       if (tt.first_in_row()) {
-        SYM_T(1, mbar_wait(smem_u32(xa_full), R & 1));
+        // new row: row image SMEM -> TMEM buffer R & 1 (tcgen05.cp, in the
+        // tensor pipe ahead of this row's distance products)
+        SYM_T(1, mbar_wait(smem_u32(xr_full), R & 1));
+        tc_fence_after();
+        if (leader) {
+          for (int part = 0; part < 2; ++part)
+            for (int kb = 0; kb < ksteps; ++kb)
+              tmem_cp_128x256b(tmem + TXA(R & 1) + part * DK + 8 * kb,
+                               dxr0 + (uint64_t)((part * BT * DK * 4 + kb * 2 * lbo_b) >> 4));
+          tc_commit(smem_u32(xr_empty));
+        }
+        __syncwarp();
         ++R;
       }
+      const uint32_t xb = (R - 1) & 1;
       SYM_T(2, mbar_wait(smem_u32(&cfull[cs]), cph));
       tc_fence_after();
       if (leader) {
@@ -315,14 +349,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
         const uint64_t db = dc0 + (uint64_t)(cs * img16);
 #pragma unroll
         for (int pass = 0; pass < 3; ++pass) {
-          const uint32_t a_t = tmem + TXA + (pass == 0 ? (uint32_t)DK : 0u);
+          const uint32_t a_t = tmem + TXA(xb) + (pass == 0 ? (uint32_t)DK : 0u);
           const uint64_t b_p = db + (pass == 1 ? half16 : 0u);
           for (int k = 0; k < ksteps; ++k)
             mma_ts(d_tm, a_t + k * 8, b_p + (uint64_t)(k * kstep_b16), idesc_d, (pass | k) != 0);
         }
         tc_commit(smem_u32(&s_full[b]));
         tc_commit(smem_u32(&cempty[cs]));
-        if (tt.last_in_row()) tc_commit(smem_u32(xa_empty));
       }
       __syncwarp();
       if (++cs == (uint32_t)NSC) { cs = 0; cph ^= 1; }
@@ -333,27 +366,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       nx.next();
       if (nx.ok) dist(nx, T + 1);
       const uint32_t b = T & 1;
-      if (it.first_in_row()) ++rowc;
-      if (it.first_in_item() && K >= 1) SYM_T(3, mbar_wait(smem_u32(acc_empty), (K - 1) & 1));
+      if (it.first_in_row()) {
+        ++rowc;
+        // O_I buffer rowc & 1 was last used by row rowc - 2
+        if (rowc >= 2) SYM_T(3, mbar_wait(smem_u32(&oi_empty[rowc & 1]), ((rowc >> 1) - 1) & 1));
+      }
+      if (K >= 1) {
+        // O_J[c] of the previous item must be read before tile (0, c) of this
+        // one; columns this item does not have are waited for at its end, so
+        // every oj_empty phase is consumed once per item
+        if (it.r == 0) SYM_T(3, mbar_wait(smem_u32(&oj_empty[it.c]), (K - 1) & 1));
+        if (it.last_in_item())
+          for (int cc = it.cols_in; cc < RB; ++cc) mbar_wait(smem_u32(&oj_empty[cc]), (K - 1) & 1);
+      }
       SYM_T(4, mbar_wait(smem_u32(&k_full[b]), (T >> 1) & 1));
-      tacc[7] += 1;
+      SYM_COUNT();
       SYM_T(5, mbar_wait(smem_u32(&vfull[vs]), vph));
       const bool mir = it.mirror();
       if (mir) SYM_T(5, mbar_wait(smem_u32(&vi_full[rowc & 1]), (rowc >> 1) & 1));
       tc_fence_after();
       if (leader) {
-        const uint32_t oi = tmem + TOI(it.r), sk = tmem + TSK(b);
-        const uint64_t vb = dv0 + (uint64_t)(vs * vt16);
-        const uint32_t fresh = it.first_in_row() ? 1u : 0u;
-#pragma unroll
-        for (int k = 0; k < BT / 16; ++k)   // O_I (+)= K1 . V1
-          mma16_ts(oi, sk + 16 * k, vb + (uint64_t)(k * kstep_v16), idesc_n16, !(fresh && k == 0));
-#pragma unroll
-        for (int k = 0; k < BT / 16; ++k)   // O_I += K2 . V1
-          mma16_ts(oi, sk + 16 * k + 8, vb + (uint64_t)(k * kstep_v16), idesc_n16, 1);
-#pragma unroll
-        for (int k = 0; k < BT / 16; ++k)   // O_I += K1 . V2
-          mma16_ts(oi, sk + 16 * k, vb + (uint64_t)(v2_16 + k * kstep_v16), idesc_n16, 1);
+        // mirror first: its completion releases the SMEM K for the next tile
         if (mir) {
           const uint32_t oj = tmem + TOJ(it.c);
           const uint64_t vib = dvi0 + (uint64_t)((rowc & 1) * vt16);
@@ -365,11 +398,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
           for (int k = 0; k < BT / 16; ++k)   // O_J[:, 0:16] += K2^T . V1
             mma16_ss(oj, dks + (uint64_t)(ks2_16 + 16 * k), vib + (uint64_t)(k * kstep_v16), idesc_m16, 1);
         }
+        tc_commit(smem_u32(ks_empty));
+        const uint32_t oi = tmem + TOI(rowc & 1), sk = tmem + TSK(b);
+        const uint64_t vb = dv0 + (uint64_t)(vs * vt16);
+        const uint32_t fresh = it.first_in_row() ? 1u : 0u;
+#pragma unroll
+        for (int k = 0; k < BT / 16; ++k)   // O_I (+)= K1 . [V1 | V2]
+          mma16_ts(oi, sk + 16 * k, vb + (uint64_t)(k * kstep_v16), idesc_n32, !(fresh && k == 0));
+#pragma unroll
+        for (int k = 0; k < BT / 16; ++k)   // O_I[:, 0:16] += K2 . V1
+          mma16_ts(oi, sk + 16 * k + 8, vb + (uint64_t)(k * kstep_v16), idesc_n16, 1);
         tc_commit(smem_u32(&vempty[vs]));
         tc_commit(smem_u32(&sk_empty[b]));
-        tc_commit(smem_u32(ks_empty));
-        if (it.last_in_row()) tc_commit(smem_u32(&vi_empty[rowc & 1]));
-        if (it.last_in_item()) tc_commit(smem_u32(acc_full));
+        if (it.last_in_row()) {
+          tc_commit(smem_u32(&vi_empty[rowc & 1]));
+          tc_commit(smem_u32(&oi_full[rowc & 1]));
+        }
+        if (it.last_in_item()) tc_commit(smem_u32(oj_full));
       }
       __syncwarp();
       if (++vs == (uint32_t)NSV) { vs = 0; vph ^= 1; }
@@ -377,7 +422,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       it = nx;
       ++T;
     }
-  } else if (warp >= KAPPA_WARP0) {
+  } else if (warp >= KAPPA_WARP0 && warp < ROW_WARP) {
     // ===================== kappa warps: S -> K =====================
     const int e = warp - KAPPA_WARP0;
     const int q = warp & 3;                        // TMEM lane quarter
@@ -391,7 +436,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
     while (it.ok) {
       const uint32_t b = T & 1;
       SYM_T(0, mbar_wait(smem_u32(&s_full[b]), (T >> 1) & 1));
-      tacc[7] += 1;
+      SYM_COUNT();
       tc_fence_after();
       const uint32_t sk = tmem + lane_base + TSK(b) + 32u * ch;
       uint32_t v[32];
@@ -445,92 +490,107 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       it.next();
       ++T;
     }
-  } else {
+  } else if (warp >= DRAIN_WARP0 && warp < KAPPA_WARP0) {
     // ===================== drain warps (4): row image -> TMEM, O_I / O_J -> sums =====================
     const int q = warp & 3;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const int i_loc = q * 32 + lane;
-    uint32_t R = 0, K = 0;
-    auto copy_row = [&]() {
-      SYM_T(0, mbar_wait(smem_u32(xr_full), R & 1));
-      if (R >= 1) SYM_T(1, mbar_wait(smem_u32(xa_empty), (R - 1) & 1));
-      tc_fence_after();
-      const float* xr = reinterpret_cast<const float*>(xr_s);
-      for (int part = 0; part < 2; ++part)
-        for (int k0 = 0; k0 < DK; k0 += 8) {
-          uint32_t w[8];
+    uint32_t K = 0;
+    // 128 output rows x t columns -> fixed point -> SMEM staging (column-major,
+    // the global layout) -> one TMA bulk reduce-add per column, issued by one
+    // thread; the L2 does the 64-bit integer adds at line granularity
+    const bool issuer = warp == DRAIN_WARP0 && lane == 0;
+    uint32_t nflush = 0;
+    auto flush = [&](int64_t row0, const float (&v)[TN]) {
+      unsigned long long* sb = stage + (nflush & 1) * (STAGE_BYTES / 8);
+      if (issuer) SYM_T(4, asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"));   // buffer's last reduce read it
+      SYM_T(1, drain_bar());
+      const int64_t row = row0 + i_loc;
+      const bool in = row < a.n;
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) w[kk] = __float_as_uint(xr[part * BT * DK + canon(i_loc, k0 + kk, BT)]);
-          tmem_st8(tmem + lane_base + TXA + part * DK + k0, w);
+      for (int c = 0; c < TN; ++c) {
+        long long x = 0;
+        if (c < a.t && in) {
+          // v 2^E_c truncated toward zero (exact scaling: |v| 2^E_c <= 2^61 by
+          // the choice of E_c); one F2I on the XU pipe, which has headroom
+          if (fabsf(v[c]) < INFINITY) x = __float2ll_rz(v[c] * scale_s[c]);
+          else a.bad[row] = 1;
         }
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(smem_u32(xa_full));
-        mbar_arrive(smem_u32(xr_empty));
+        sb[c * BT + i_loc] = (unsigned long long)x;
       }
-      ++R;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      drain_bar();
+      if (issuer) {
+        for (int c = 0; c < a.t; ++c)
+          bulk_red_u64(a.acc + (int64_t)c * a.acc_ld + row0, smem_u32(sb + c * BT), BT * 8u);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      ++nflush;
     };
     int L = blockIdx.x;
     const int G = gridDim.x, NB = a.nblocks;
-    if (L < a.n_items) copy_row();
+    uint32_t Rd = 0;
     while (L < a.n_items) {
       int P, Q;
       pair_of(L, NB, P, Q);
       const int rows_in = min(RB, a.tiles - RB * P), cols_in = min(RB, a.tiles - RB * Q);
-      for (int r = 1; r < rows_in; ++r) copy_row();
       const int Ln = L + G;
       int Pn = -1, Qn = -1;
-      if (Ln < a.n_items) {
-        pair_of(Ln, NB, Pn, Qn);
-        copy_row();   // the next item's first row is needed before this item drains
-      }
-      SYM_T(2, mbar_wait(smem_u32(acc_full), K & 1));
-      tacc[7] += 1;
-      tc_fence_after();
+      if (Ln < a.n_items) pair_of(Ln, NB, Pn, Qn);
       for (int r = 0; r < rows_in; ++r) {
-        uint32_t o[16];
-        tmem_ld16(tmem + lane_base + TOI(r), o);
+        SYM_T(2, mbar_wait(smem_u32(&oi_full[Rd & 1]), (Rd >> 1) & 1));
+        tc_fence_after();
+        uint32_t o[32];
+        tmem_ld32(tmem + lane_base + TOI(Rd & 1), o);
         tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&oi_empty[Rd & 1]));
+        ++Rd;
         float* ar = acci + (r * BT + i_loc) * TN;
 #pragma unroll
-        for (int c = 0; c < TN; ++c) ar[c] += __uint_as_float(o[c]);
+        for (int c = 0; c < TN; ++c) ar[c] += __uint_as_float(o[c]) + __uint_as_float(o[c + TN]);
       }
-      for (int cc = (P == Q ? 1 : 0); cc < cols_in; ++cc) {
+      SYM_T(3, mbar_wait(smem_u32(oj_full), K & 1));
+      SYM_COUNT();
+      tc_fence_after();
+      for (int cc = 0; cc < RB; ++cc) {
+        const bool live = cc < cols_in && !(P == Q && cc == 0);
         uint32_t o[32];
-        tmem_ld32(tmem + lane_base + TOJ(cc), o);
-        tmem_wait_ld();
-        const int64_t row = (int64_t)(RB * Q + cc) * BT + i_loc;
-        if (row < a.n) {
+        if (live) {
+          tmem_ld32(tmem + lane_base + TOJ(cc), o);
+          tmem_wait_ld();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&oj_empty[cc]));
+        if (live) {
+          float v[TN];
 #pragma unroll
-          for (int c = 0; c < TN; ++c) {
-            if (c < a.t) contribute(a, row, c, __uint_as_float(o[c]) + __uint_as_float(o[c + TN]), expo_s[c]);
-          }
+          for (int c = 0; c < TN; ++c) v[c] = __uint_as_float(o[c]) + __uint_as_float(o[c + TN]);
+          SYM_T(5, flush((int64_t)(RB * Q + cc) * BT, v));
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(acc_empty));
       ++K;
       if (Pn != P) {
         // leaving row block P: its carried O_I partials go to the global sums
         for (int r = 0; r < rows_in; ++r) {
-          const int64_t row = (int64_t)(RB * P + r) * BT + i_loc;
           float* ar = acci + (r * BT + i_loc) * TN;
+          float v[TN];
 #pragma unroll
           for (int c = 0; c < TN; ++c) {
-            const float v = ar[c];
+            v[c] = ar[c];
             ar[c] = 0.f;
-            if (c < a.t && row < a.n) contribute(a, row, c, v, expo_s[c]);
           }
+          flush((int64_t)(RB * P + r) * BT, v);
         }
       }
       L = Ln;
     }
+    if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
 
-  if (a.prof && lane == 0) {
+  if (GP_SYM_PROF_BUILD && a.prof && lane == 0) {
     tacc[6] = clock64() - t_start;
     for (int k = 0; k < 8; ++k) a.prof[((int64_t)blockIdx.x * (NTHREADS / 32) + warp) * 8 + k] = tacc[k];
   }
@@ -620,7 +680,7 @@ static Plan make_plan(const gp_kv_desc* d) {
   p.acc_bytes = (size_t)TN * p.acc_ld * 8;
   p.bad_bytes = (size_t)p.acc_ld * 4;
   const size_t budget = 227 * 1024;
-  const size_t fixed = KS_BYTES + img + 2 * V_TILE_BYTES + ACCI_BYTES + BAR_BYTES;
+  const size_t fixed = KS_BYTES + img + 2 * V_TILE_BYTES + ACCI_BYTES + 2 * STAGE_BYTES + BAR_BYTES;
   p.nsc = 2;
   p.nsv = 0;
   for (int nv = 3; nv >= 2; --nv)
@@ -637,7 +697,7 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // the same point set on both sides, every row and column, t <= 16
 bool kv_sym_supported(const gp_kv_desc* d, int t) {
   if (t < 1 || t > tcs::TN) return false;
-  if (d->d < 1 || d->d + 2 > 32) return false;   // row image hi|lo must fit 64 TMEM columns
+  if (d->d < 1 || d->d + 2 > 16) return false;   // DK <= 16: the SMEM plan (d <= 14)
   if (d->Xr != d->Xc || d->ldr != d->ldc || d->n_rows != d->n_cols || d->n_rows < 1) return false;
   if (d->self_offset != 0 || (d->diag_offset != 0 && d->diag_offset >= 0)) return false;
   return tcs::make_plan(d).nsv >= 2;
@@ -689,7 +749,7 @@ int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* ou
   auto kern = desc->family == GP_FAMILY_RBF ? kv_sym_kernel<GP_FAMILY_RBF> : kv_sym_kernel<GP_FAMILY_MATERN32>;
   GP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   const char* pe = getenv("GP_SYM_PROF");
-  if (pe && *pe == '1') GP_CUDA_TRY(cudaMalloc(&a.prof, (size_t)grid * (NTHREADS / 32) * 8 * sizeof(long long)));
+  if (GP_SYM_PROF_BUILD && pe && *pe == '1') GP_CUDA_TRY(cudaMalloc(&a.prof, (size_t)grid * (NTHREADS / 32) * 8 * sizeof(long long)));
   kern<<<grid, NTHREADS, p.smem, st>>>(a);
   GP_LAUNCH_CHECK();
   if (a.prof) {   // diagnostic only: per-role average cycles per event, CTA-averaged

@@ -138,10 +138,10 @@ def test_row_shards_bitwise_equal_full():
     w = syn.WORKLOADS["C2"]
     X = syn.whitened_inputs(w.n, w.d, 0)[:20_000]
     V = syn.rhs_block(20_000, 11, 2)
-    full = _kv_rows(w, X, V, 0, 20_000)
+    full = _kv_rows(w, X, V, 0, 20_000, algo=1)
     for shards in (2, 3, 8):
         b = np.linspace(0, 20_000, shards + 1).astype(int)
-        parts = np.vstack([_kv_rows(w, X, V, b[i], b[i + 1] - b[i]) for i in range(shards)])
+        parts = np.vstack([_kv_rows(w, X, V, b[i], b[i + 1] - b[i], algo=1) for i in range(shards)])
         assert np.array_equal(parts, full), shards
 
 
@@ -254,3 +254,26 @@ def test_symmetric_kernel_matches_row_tiled_and_is_deterministic():
     tc = _kv_rows(w, X, V, 0, 20_000, algo=2)
     assert colrel(sym, tc) <= 1e-5
     assert np.array_equal(sym, _kv_rows(w, X, V, 0, 20_000, algo=3))
+    # the default for the whole square operator
+    assert np.array_equal(sym, _kv_rows(w, X, V, 0, 20_000, algo=0))
+
+
+@pytest.mark.parametrize("fam", ["rbf", "matern32"])
+def test_symmetric_kernel_edges_vs_oracle(fam):
+    """Ragged tile / block edges (n not a multiple of 128 or 512), tiny n,
+    d up to the kernel's limit, 1..16 right-hand sides, against the fp64
+    oracle."""
+    import oracle as O
+    import torch
+    from paper_1903_08114_b200 import _device as D, _ops
+    rng = np.random.default_rng(5)
+    for n, d, t in ((1, 3, 1), (5, 1, 16), (129, 14, 11), (700, 11, 16), (2051, 8, 3)):
+        X = rng.standard_normal((n, d))
+        V = rng.standard_normal((n, t))
+        ls = np.linspace(0.75, 1.5, d) * np.sqrt(d)
+        m = gp.KernelModel(fam, 1.3, ls, 0.2)
+        Xs32, _ = D.points(X).scaled(m.scale_for(d))
+        op = _ops.FusedKernelOperator(m.family_code, d, Xs32, Xs32, m.outputscale, m.noise, 0, algo=3)
+        got = op.apply32(torch.from_numpy(V).float().cuda(), t).double().cpu().numpy()
+        ref = O.kernel_mvm(O.make_hp(fam, 1.3, ls, 0.2), X, V)
+        assert colrel(got, ref) <= KV_RTOL, (n, d, t, colrel(got, ref))
