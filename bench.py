@@ -50,11 +50,11 @@ def parse():
     return ap.parse_args()
 
 
-def load_traffic():
-    """dram bytes per K·V launch from the committed ncu --set full capture
-    (profiles/kv_tc_ncu_summary.json), scaled to this launch's rows x cols."""
+def load_traffic(kernel="kv_tc"):
+    """dram bytes per K·V launch from the committed ncu --set full capture of
+    that kernel (profiles/<kernel>_ncu_summary.json)."""
     try:
-        with open(os.path.join(HERE, "profiles", "kv_tc_ncu_summary.json")) as fh:
+        with open(os.path.join(HERE, "profiles", f"{kernel}_ncu_summary.json")) as fh:
             return json.load(fh)
     except OSError:
         return None
@@ -305,7 +305,7 @@ def run_ours(args):
     job_tflops = n * n * (2 * w.d + 2 * T_RHS) / (kv_ms_max / 1e3) / 1e12
 
     traffic = None
-    tsum = load_traffic()
+    tsum = load_traffic("kv_sym" if sym else "kv_tc")
     if tsum and tsum.get("n") == n and tsum.get("rows") == (r1 - r0):
         traffic = tsum["dram_bytes_per_launch"]
     e2e = None
