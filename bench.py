@@ -252,8 +252,7 @@ def run_ours(args):
     precond = build_kernel_preconditioner(model, ps, w.rank)  # redundant per rank
     Z = draw_probes_device(n, T_RHS - 1, 0, precond)
     B = torch.cat([D.to_device(y)[:, None], Z], dim=1)[r0:r1].contiguous()
-    kv = _ops.FusedKernelOperator(model.family_code, w.d, Xs32[r0:r1], Xs32, 1.0, 0.0, -1,
-                                  algo=args.algo, self_offset=r0)
+    kv = _ops.training_operator(model.family_code, w.d, Xs32, 1.0, 0.0, -1, comm, algo=args.algo)
     op = FusedOperator(kv, model.noise, n)
     total_steps = args.warmup + args.steps
     run = MbcgRun(op, B, 1e-300, total_steps, precond, comm, row_offset=r0)
@@ -291,11 +290,11 @@ def run_ours(args):
     tflops = flops_launch / (kv_ms_mean / 1e3) / 1e12
     # the symmetric kernel (the default for the whole square operator, d <= 14)
     # evaluates each unordered pair of points once: T(T+1)/2 tiles of 128 x 128
-    sym = (world == 1 and args.algo in (0, 3) and w.d + 2 <= 16
-           and os.environ.get("GP_KV_NO_SYM", "0") != "1")
+    sym = (args.algo in (0, 3) and w.d + 2 <= 16 and os.environ.get("GP_KV_NO_SYM", "0") != "1")
     if sym:
+        # this rank's share of the T(T+1)/2 tiles (items of 4 x 4 tiles dealt round-robin)
         tiles = (n + 127) // 128
-        entries_launch = tiles * (tiles + 1) // 2 * 128 * 128
+        entries_launch = tiles * (tiles + 1) // 2 * 128 * 128 // world
     else:
         entries_launch = (r1 - r0) * n
     entries_per_s = entries_launch / (kv_ms_mean / 1e3)
@@ -385,8 +384,7 @@ def e2e_run(args, w, n, X, y, model, comm, r0, r1):
     t0 = time.perf_counter()
     ps = D.PointSet(Xh)
     Xs32, _ = ps.scaled(model.lengthscales)
-    kv = _ops.FusedKernelOperator(model.family_code, w.d, Xs32[r0:r1], Xs32, 1.0, 0.0, -1,
-                                  algo=args.algo, self_offset=r0)
+    kv = _ops.training_operator(model.family_code, w.d, Xs32, 1.0, 0.0, -1, comm, algo=args.algo)
     run = MbcgRun(FusedOperator(kv, model.noise, n), D.to_device(Bh), 1e-300, steps, precond,
                   comm, row_offset=r0)
     for _ in range(steps):

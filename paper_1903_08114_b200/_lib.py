@@ -49,6 +49,12 @@ _SIGS = {
     "gp_prescale": (C.c_int, [c_p, c_i64, C.c_int, c_i64, c_p, C.c_int, c_p, c_i64, c_p, c_i64, c_p, c_p]),
     "gp_kv_workspace_bytes": (c_sz, [C.POINTER(KvDesc), C.c_int]),
     "gp_kv": (C.c_int, [C.POINTER(KvDesc), c_p, c_i64, C.c_int, c_p, c_i64, c_p, c_sz, c_p]),
+    "gp_kv_sym_supported": (C.c_int, [C.POINTER(KvDesc), C.c_int]),
+    "gp_kv_sym_acc_ld": (c_i64, [C.POINTER(KvDesc)]),
+    "gp_kv_sym_partial": (C.c_int, [C.POINTER(KvDesc), c_p, c_i64, C.c_int, C.c_int, C.c_int, c_p, c_p, c_p,
+                                    c_sz, c_p]),
+    "gp_kv_sym_finalize": (C.c_int, [C.POINTER(KvDesc), c_p, c_i64, C.c_int, c_p, c_p, c_i64, c_i64, c_p,
+                                     c_i64, c_p, c_sz, c_p]),
     "gp_kernel_block": (C.c_int, [C.c_int, C.c_int, c_p, c_i64, c_i64, c_p, c_i64, c_i64, c_f64,
                                   c_f64, c_i64, c_p, c_i64, c_p]),
     "gp_block_mvm": (C.c_int, [c_p, c_i64, c_i64, c_i64, c_p, c_i64, C.c_int, c_p, c_i64, c_p, c_p]),

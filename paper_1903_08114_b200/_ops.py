@@ -74,6 +74,80 @@ class FusedKernelOperator:
         return out32
 
 
+class SymShardedKernelOperator:
+    """Rows [comm.row0, comm.row1) of the whole square operator
+    s2*kappa(X, X) (+ noise I) with the symmetric kernel's work items split
+    across the ranks of `comm` (include/gpbbmm.h, gp_kv_sym_partial): each rank
+    forms the 64-bit fixed-point partial sums of its items for all n rows, the
+    integer sums are all-reduced (deterministic), and each rank finalises its
+    own rows — bitwise equal to the single-device gp_kv result. Every rank
+    then evaluates ~n^2/(2 world) kernel entries instead of n^2/world. Falls
+    back to the row-tiled kernel (`fallback`) for shapes the symmetric kernel
+    does not take (t > 16)."""
+
+    def __init__(self, family_code: int, d: int, X32_full, outputscale: float, noise: float,
+                 diag_offset: int, comm, fallback=None):
+        self.desc = _lib.KvDesc(family=family_code, d=d, Xr=_lib.ptr(X32_full), ldr=X32_full.stride(0),
+                                n_rows=X32_full.shape[0], Xc=_lib.ptr(X32_full), ldc=X32_full.stride(0),
+                                n_cols=X32_full.shape[0], outputscale=float(outputscale),
+                                noise=float(noise), diag_offset=int(diag_offset), algo=0, self_offset=0)
+        self._keep = (X32_full,)
+        self.comm = comm
+        self.row0, self.row1 = comm.row0, comm.row1
+        self.n_rows = self.row1 - self.row0
+        self.n_cols = X32_full.shape[0]
+        self.fallback = fallback
+        self._acc = None
+
+    def supported(self, t: int) -> bool:
+        return bool(_lib.lib().gp_kv_sym_supported(self.desc, t))
+
+    def apply32(self, V32_full, t: int, out32=None):
+        """out32[:, :t] = rows [row0, row1) of K V32_full[:n, :t]."""
+        if not self.supported(t):
+            if self.fallback is None:
+                raise ValueError(f"symmetric K·V does not take t={t} and no fallback operator was given")
+            return self.fallback.apply32(V32_full, t, out32)
+        T = _T()
+        L = _lib.lib()
+        if out32 is None:
+            out32 = T.empty((self.n_rows, t), dtype=T.float32, device=D.device())
+        ld = int(L.gp_kv_sym_acc_ld(self.desc))
+        if self._acc is None or self._acc[0].numel() < t * ld:
+            self._acc = (T.empty(t * ld, dtype=T.int64, device=D.device()),
+                         T.empty(ld, dtype=T.int32, device=D.device()))
+        acc, bad = self._acc[0][: t * ld], self._acc[1][:ld]
+        nbytes = L.gp_kv_workspace_bytes(self.desc, t)
+        ws = _ws.bytes("kv", nbytes)
+        _lib.check(L.gp_kv_sym_partial(self.desc, _lib.ptr(V32_full), V32_full.stride(0), t, self.comm.rank,
+                                       self.comm.world, _lib.ptr(acc), _lib.ptr(bad), _lib.ptr(ws), int(nbytes),
+                                       _st()), "gp_kv_sym_partial")
+        self.comm.allreduce_(acc)
+        self.comm.allreduce_(bad)
+        _lib.check(L.gp_kv_sym_finalize(self.desc, _lib.ptr(V32_full), V32_full.stride(0), t, _lib.ptr(acc),
+                                        _lib.ptr(bad), self.row0, self.row1, _lib.ptr(out32), out32.stride(0),
+                                        _lib.ptr(ws), int(nbytes), _st()), "gp_kv_sym_finalize")
+        return out32
+
+
+def training_operator(family_code: int, d: int, X32_full, outputscale: float, noise: float,
+                      diag_offset: int, comm=None, algo: int = 0):
+    """The K̂ operator a solver on this rank applies: the whole operator on one
+    device (gp_kv picks the symmetric kernel itself), or, across ranks, the
+    symmetric schedule split by work items with the row-tiled kernel as the
+    fallback for shapes it does not take."""
+    if comm is None or getattr(comm, "world", 1) == 1:
+        return FusedKernelOperator(family_code, d, X32_full, X32_full, outputscale, noise, diag_offset,
+                                   algo=algo, self_offset=0)
+    r0, r1 = comm.row0, comm.row1
+    rows = FusedKernelOperator(family_code, d, X32_full[r0:r1], X32_full, outputscale, noise,
+                               diag_offset + r0 if diag_offset >= 0 else -1, algo=algo, self_offset=r0)
+    if algo not in (0, 3):
+        return rows
+    return SymShardedKernelOperator(family_code, d, X32_full, outputscale, noise, diag_offset, comm,
+                                    fallback=rows)
+
+
 def coldot(A, B):
     """Per-column sum(A * B) of two (n, t) fp64 tensors -> (t,) fp64."""
     T = _T()

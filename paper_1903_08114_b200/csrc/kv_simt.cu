@@ -445,6 +445,12 @@ int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* ou
            void* ws, size_t ws_bytes, cudaStream_t st);
 size_t kv_sym_workspace(const gp_kv_desc* desc, int t);
 bool kv_sym_supported(const gp_kv_desc* desc, int t);
+int64_t kv_sym_acc_ld(const gp_kv_desc* desc);
+int kv_sym_partial(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, int part, int nparts,
+                   long long* acc, int* bad, void* ws, size_t ws_bytes, cudaStream_t st);
+int kv_sym_finalize(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, const long long* acc,
+                    const int* bad, int64_t row0, int64_t row1, float* out, int64_t ldo, void* ws, size_t ws_bytes,
+                    cudaStream_t st);
 int kv_wide(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out, int64_t ldo,
             void* ws, size_t ws_bytes, cudaStream_t st);
 size_t kv_wide_workspace(const gp_kv_desc* desc, int t);
@@ -508,6 +514,35 @@ int gp_kv(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out
     return gp::kv_tc(desc, V, ldv, t, out, ldo, workspace, workspace_bytes, st);
   }
   return gp::kv_simt(desc, V, ldv, t, out, ldo, workspace, workspace_bytes, st);
+}
+
+int gp_kv_sym_supported(const gp_kv_desc* desc, int t) {
+  return desc != nullptr && gp_has_tcgen05() && gp::kv_sym_supported(desc, t) ? 1 : 0;
+}
+
+int64_t gp_kv_sym_acc_ld(const gp_kv_desc* desc) {
+  return desc != nullptr && desc->n_rows > 0 ? gp::kv_sym_acc_ld(desc) : 0;
+}
+
+int gp_kv_sym_partial(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, int part, int nparts,
+                      int64_t* acc, int32_t* bad, void* workspace, size_t workspace_bytes, void* stream) {
+  GP_REQUIRE(desc != nullptr && V != nullptr && acc != nullptr && bad != nullptr, "gp_kv_sym_partial: null argument");
+  GP_REQUIRE(gp_has_tcgen05(), "gp_kv_sym_partial: tcgen05 kernel not compiled in");
+  GP_REQUIRE(t >= 1 && ldv >= t, "gp_kv_sym_partial: t=%d ldv=%lld", t, (long long)ldv);
+  return gp::kv_sym_partial(desc, V, ldv, t, part, nparts, reinterpret_cast<long long*>(acc),
+                            reinterpret_cast<int*>(bad), workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int gp_kv_sym_finalize(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, const int64_t* acc,
+                       const int32_t* bad, int64_t row0, int64_t row1, float* out, int64_t ldo, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+  GP_REQUIRE(desc != nullptr && V != nullptr && acc != nullptr && bad != nullptr && out != nullptr,
+             "gp_kv_sym_finalize: null argument");
+  GP_REQUIRE(t >= 1 && ldv >= t && ldo >= t, "gp_kv_sym_finalize: t=%d ldv=%lld ldo=%lld", t, (long long)ldv,
+             (long long)ldo);
+  return gp::kv_sym_finalize(desc, V, ldv, t, reinterpret_cast<const long long*>(acc),
+                             reinterpret_cast<const int*>(bad), row0, row1, out, ldo, workspace, workspace_bytes,
+                             (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -23,15 +23,15 @@
 // per column by 2^s into fp16 range (V = V1 + V2): as accurate as 3xTF32.
 //
 // Work items are 4 x 4 blocks of tiles (block pairs P <= Q, row-major
-// upper-triangular order, round-robin over persistent CTAs). O_I[0..3] and
-// O_J[0..3] accumulate in TMEM over an item (4 tiles of K each, short enough
-// for the tensor core's fp32 accumulation) and are drained once per item:
-// O_I into an SMEM fp32 accumulator that is carried across consecutive items
-// of the same row block, O_J straight into the global sums. Contributions to
-// one output row come from many CTAs, so they are summed in 64-bit FIXED POINT
-// (red.global.add.u64, per-column scale 2^E_c chosen from ||V_c||_1 so no
-// partial can overflow): integer addition is associative, so the result is
-// bitwise reproducible run to run and independent of the CTA schedule, like
+// upper-triangular order, round-robin over persistent CTAs; with item
+// sharding, rank `part` of `nparts` takes the items L = part (mod nparts)).
+// O_I (per item row) and O_J[0..3] accumulate in TMEM over 4 tiles of K,
+// short enough for the tensor core's fp32 accumulation, and every such
+// per-item partial leaves the SM as 64-bit FIXED POINT (per-column scale 2^E_c
+// chosen from ||V_c||_1 so no partial can overflow), added into the global
+// sums with TMA bulk reduce-adds. Integer addition is associative and the
+// partials depend only on the item, so the result is bitwise identical run to
+// run, for any CTA schedule and for any split of the items across GPUs, like
 // the reference's partition-count independence (test_partition.py:92-102).
 //
 // Warp roles: 0 TMA producer (column tiles), 1 MMA issuer (also copies each
@@ -63,8 +63,14 @@ constexpr int NTHREADS = 32 * (ROW_WARP + 1);
 constexpr uint32_t KS_HALF = BT * BT * 2;            // K1 (or K2) of one tile, fp16 MN-major
 constexpr uint32_t KS_BYTES = 2 * KS_HALF;
 constexpr uint32_t V_TILE_BYTES = 2u * TN * BT * 2u;  // [V1 | V2] of one tile, 32 x 128 fp16
-constexpr uint32_t ACCI_BYTES = RB * BT * TN * 4u;    // O_I carried over items of one row block
 constexpr uint32_t STAGE_BYTES = TN * BT * 8u;       // fixed-point sums of one 128-row block
+// Items are dealt to CTAs in chunks of ITEM_CHUNK consecutive items (mostly
+// the same row block P); the O_I partials of a chunk's items are summed in
+// SMEM (fp32) and leave the SM once per (chunk, row block). The grouping is a
+// function of the item index alone, so the fixed-point result does not
+// depend on the grid size or on how the chunks are split across devices.
+constexpr int ITEM_CHUNK = 4;
+constexpr uint32_t ACCI_BYTES = RB * BT * TN * 4u;
 constexpr uint32_t BAR_BYTES = 1024;
 
 // TMEM columns (512): S/K buffers 2 x 128 | O_I 2 x 32 (by row) | O_J 4 x 32 |
@@ -83,6 +89,7 @@ struct Args {
   int DK;
   int64_t n;
   int tiles, nblocks, n_items, nsc, nsv, t;
+  int part, nparts;                 // item sharding: this launch takes items L = part (mod nparts)
   const int* expo;                  // [TN] partials (in scaled units) summed as round(v 2^expo_c)
   unsigned long long* acc;          // [TN][acc_ld] fixed-point sums (column-major)
   int64_t acc_ld;
@@ -138,11 +145,12 @@ __device__ __forceinline__ void pair_of(int L, int NB, int& P, int& Q) {
   Q = p + (int)(L - start(p));
 }
 
-// The tile sequence of one CTA (every role walks the same sequence): items
-// L = blockIdx.x + k gridDim.x; within an item, rows r then columns c, with
+// The tile sequence of one CTA (every role walks the same sequence): chunks
+// k = part + nparts (blockIdx.x + j gridDim.x) of ITEM_CHUNK items each; within an item, rows r then columns c, with
 // c >= r on a diagonal item (P = Q), whose tile (r, r) is a diagonal tile.
 struct TileSeq {
-  int NB, tiles, n_items, G;
+  int NB, tiles, n_items, G;   // G = chunk stride (grid x parts)
+  int k, i;                    // chunk, item within the chunk
   int L, P, Q, r, c, rows_in, cols_in;
   bool ok;
   __device__ void set_item() {
@@ -153,8 +161,22 @@ struct TileSeq {
     c = c0();
   }
   __device__ void begin(const Args& a) {
-    NB = a.nblocks; tiles = a.tiles; n_items = a.n_items; G = gridDim.x;
-    L = blockIdx.x;
+    NB = a.nblocks; tiles = a.tiles; n_items = a.n_items; G = gridDim.x * a.nparts;
+    k = a.part + a.nparts * blockIdx.x;
+    i = 0;
+    L = ITEM_CHUNK * k;
+    ok = L < n_items;
+    if (ok) set_item();
+  }
+  // next item of this CTA's sequence (chunk by chunk)
+  __device__ void next_item() {
+    if (++i < ITEM_CHUNK && ITEM_CHUNK * k + i < n_items) {
+      ++L;
+    } else {
+      k += G;
+      i = 0;
+      L = ITEM_CHUNK * k;
+    }
     ok = L < n_items;
     if (ok) set_item();
   }
@@ -162,9 +184,7 @@ struct TileSeq {
   __device__ void next() {
     if (++c < cols_in) return;
     if (++r < rows_in) { c = c0(); return; }
-    L += G;
-    ok = L < n_items;
-    if (ok) set_item();
+    next_item();
   }
   __device__ bool first_in_row() const { return c == c0(); }
   __device__ bool last_in_row() const { return c == cols_in - 1; }
@@ -186,7 +206,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
   uint8_t* vi_s = xr_s + img_bytes;                    // V_I, double buffered by row
   uint8_t* cring = vi_s + 2 * V_TILE_BYTES;            // [NSC] column images
   uint8_t* vring = cring + NSC * img_bytes;            // [NSV] V_J images
-  float* acci = reinterpret_cast<float*>(vring + NSV * V_TILE_BYTES);   // [RB][BT][TN]
+  float* acci = reinterpret_cast<float*>(vring + NSV * V_TILE_BYTES);   // [RB][BT][TN], 16-B chunks swizzled
   unsigned long long* stage = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(acci) + ACCI_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stage) + 2 * STAGE_BYTES);
   uint64_t* cfull = bars;               // [NSC] column image landed           TMA -> MMA
@@ -209,8 +229,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
   float* scale_s = reinterpret_cast<float*>(tmem_slot + 4);   // [TN] fixed-point scales 2^expo_c
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int x = threadIdx.x; x < (int)(ACCI_BYTES / 4); x += blockDim.x) acci[x] = 0.f;
   if (threadIdx.x < TN) scale_s[threadIdx.x] = ldexpf(1.0f, a.expo[threadIdx.x]);
-  for (int i = threadIdx.x; i < (int)(ACCI_BYTES / 4); i += blockDim.x) acci[i] = 0.f;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSC; ++s) {
       mbar_init(smem_u32(&cfull[s]), 1);
@@ -527,16 +547,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       }
       ++nflush;
     };
-    int L = blockIdx.x;
-    const int G = gridDim.x, NB = a.nblocks;
+    // O_I partials of the current (chunk, row block), fp32; 16-byte chunks
+    // swizzled by row so the 128-bit accesses of a warp hit distinct banks
+    const int sw = (i_loc >> 1) & 3;
+    auto acci_row = [&](int r) { return reinterpret_cast<float4*>(acci + (r * BT + i_loc) * TN); };
+    auto flush_acci = [&](int P, int rows) {
+      for (int r = 0; r < rows; ++r) {
+        float4* ar = acci_row(r);
+        float v[TN];
+#pragma unroll
+        for (int j = 0; j < TN / 4; ++j) {
+          const float4 x = ar[j ^ sw];
+          v[4 * j] = x.x; v[4 * j + 1] = x.y; v[4 * j + 2] = x.z; v[4 * j + 3] = x.w;
+          ar[j ^ sw] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        SYM_T(5, flush((int64_t)(RB * P + r) * BT, v));
+      }
+    };
+    TileSeq itm;
+    itm.begin(a);
     uint32_t Rd = 0;
-    while (L < a.n_items) {
-      int P, Q;
-      pair_of(L, NB, P, Q);
-      const int rows_in = min(RB, a.tiles - RB * P), cols_in = min(RB, a.tiles - RB * Q);
-      const int Ln = L + G;
-      int Pn = -1, Qn = -1;
-      if (Ln < a.n_items) pair_of(Ln, NB, Pn, Qn);
+    while (itm.ok) {
+      const int P = itm.P, Q = itm.Q, rows_in = itm.rows_in, cols_in = itm.cols_in;
       for (int r = 0; r < rows_in; ++r) {
         SYM_T(2, mbar_wait(smem_u32(&oi_full[Rd & 1]), (Rd >> 1) & 1));
         tc_fence_after();
@@ -547,9 +579,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&oi_empty[Rd & 1]));
         ++Rd;
-        float* ar = acci + (r * BT + i_loc) * TN;
+        float4* ar = acci_row(r);
 #pragma unroll
-        for (int c = 0; c < TN; ++c) ar[c] += __uint_as_float(o[c]) + __uint_as_float(o[c + TN]);
+        for (int j = 0; j < TN / 4; ++j) {
+          float4 x = ar[j ^ sw];
+          x.x += __uint_as_float(o[4 * j]) + __uint_as_float(o[4 * j + TN]);
+          x.y += __uint_as_float(o[4 * j + 1]) + __uint_as_float(o[4 * j + 1 + TN]);
+          x.z += __uint_as_float(o[4 * j + 2]) + __uint_as_float(o[4 * j + 2 + TN]);
+          x.w += __uint_as_float(o[4 * j + 3]) + __uint_as_float(o[4 * j + 3 + TN]);
+          ar[j ^ sw] = x;
+        }
       }
       SYM_T(3, mbar_wait(smem_u32(oj_full), K & 1));
       SYM_COUNT();
@@ -572,20 +611,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
         }
       }
       ++K;
-      if (Pn != P) {
-        // leaving row block P: its carried O_I partials go to the global sums
-        for (int r = 0; r < rows_in; ++r) {
-          float* ar = acci + (r * BT + i_loc) * TN;
-          float v[TN];
-#pragma unroll
-          for (int c = 0; c < TN; ++c) {
-            v[c] = ar[c];
-            ar[c] = 0.f;
-          }
-          flush((int64_t)(RB * P + r) * BT, v);
-        }
-      }
-      L = Ln;
+      const int k_now = itm.k;
+      itm.next_item();
+      // leaving the chunk or the row block: the carried O_I partials go out
+      if (!itm.ok || itm.k != k_now || itm.P != P) flush_acci(P, rows_in);
     }
     if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
@@ -648,17 +677,18 @@ __global__ void sym_scale_kernel(const float* __restrict__ V, int64_t ldv, int64
 
 // out[i, c] = s2 * acc[c][i] 2^-E_c (+ noise V[i + diag_offset, c]); NaN where a
 // non-finite partial was seen (the host names the partition, partition.py:231-236)
-__global__ void sym_finalize_kernel(const unsigned long long* __restrict__ acc, int64_t acc_ld,
-                                    const int* __restrict__ bad, const double* __restrict__ inv_scale, int64_t n,
-                                    int t, float* out, int64_t ldo, double s2, double noise, const float* V,
-                                    int64_t ldv, int64_t diag_offset) {
+// rows [row0, row1) of the operator: out[i - row0, c]
+__global__ void sym_finalize_kernel(const long long* __restrict__ acc, int64_t acc_ld,
+                                    const int* __restrict__ bad, const double* __restrict__ inv_scale,
+                                    int64_t row0, int64_t row1, int t, float* out, int64_t ldo, double s2,
+                                    double noise, const float* V, int64_t ldv, int64_t diag_offset) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= n * t) return;
-  const int64_t i = idx / t;
-  const int c = (int)(idx - i * t);
-  double r = s2 * ((double)(long long)acc[(int64_t)c * acc_ld + i] * inv_scale[c]);
+  if (idx >= (row1 - row0) * t) return;
+  const int64_t i = row0 + idx / t;
+  const int c = (int)(idx % t);
+  double r = s2 * ((double)acc[(int64_t)c * acc_ld + i] * inv_scale[c]);
   if (diag_offset >= 0) r += noise * (double)V[(i + diag_offset) * ldv + c];
-  out[i * ldo + c] = bad[i] ? __int_as_float(0x7fc00000) : (float)r;
+  out[(i - row0) * ldo + c] = bad[i] ? __int_as_float(0x7fc00000) : (float)r;
 }
 
 struct Plan {
@@ -711,41 +741,63 @@ size_t kv_sym_workspace(const gp_kv_desc* d, int t) {
          align256(p.bad_bytes) + 256 * sizeof(double) + 3 * 64 * sizeof(double);
 }
 
-int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out, int64_t ldo, void* ws,
-           size_t ws_bytes, cudaStream_t st) {
+namespace tcs {
+struct WsView {
+  float* row_img; float* col_img; __half* v_img;
+  long long* acc; int* bad; double* mean; int* expo; float* vscale; double* inv_scale;
+};
+static WsView carve(const Plan& p, void* ws) {
+  WsView v;
+  char* w = static_cast<char*>(ws);
+  v.row_img = reinterpret_cast<float*>(w); w += align256(p.img_bytes_all);
+  v.col_img = reinterpret_cast<float*>(w); w += align256(p.img_bytes_all);
+  v.v_img = reinterpret_cast<__half*>(w); w += align256(p.v_img_bytes);
+  v.acc = reinterpret_cast<long long*>(w); w += align256(p.acc_bytes);
+  v.bad = reinterpret_cast<int*>(w); w += align256(p.bad_bytes);
+  v.mean = reinterpret_cast<double*>(w); w += 256 * sizeof(double);
+  v.expo = reinterpret_cast<int*>(w); w += 64 * sizeof(double);
+  v.vscale = reinterpret_cast<float*>(w); w += 64 * sizeof(double);
+  v.inv_scale = reinterpret_cast<double*>(w);
+  return v;
+}
+}  // namespace tcs
+
+int64_t kv_sym_acc_ld(const gp_kv_desc* desc) { return tcs::make_plan(desc).acc_ld; }
+
+// fixed-point sums (t x acc_ld, column-major) of the items L = part (mod
+// nparts) of the symmetric schedule, written into acc / bad (zeroed here);
+// partial sums of disjoint item sets add up (int64) to the full product
+int kv_sym_partial(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, int part, int nparts,
+                   long long* acc, int* bad, void* ws, size_t ws_bytes, cudaStream_t st) {
   using namespace tcs;
+  GP_REQUIRE(kv_sym_supported(desc, t), "gp_kv_sym: shape unsupported by the symmetric kernel");
+  GP_REQUIRE(nparts >= 1 && part >= 0 && part < nparts, "gp_kv_sym: part %d of %d", part, nparts);
   Plan p = make_plan(desc);
   size_t need = kv_sym_workspace(desc, t);
   GP_REQUIRE(ws != nullptr && ws_bytes >= need, "gp_kv(symmetric): workspace of %zu bytes required, %zu given",
              need, ws_bytes);
-  char* w = static_cast<char*>(ws);
-  float* row_img = reinterpret_cast<float*>(w); w += align256(p.img_bytes_all);
-  float* col_img = reinterpret_cast<float*>(w); w += align256(p.img_bytes_all);
-  __half* v_img = reinterpret_cast<__half*>(w); w += align256(p.v_img_bytes);
-  unsigned long long* acc = reinterpret_cast<unsigned long long*>(w); w += align256(p.acc_bytes);
-  int* bad = reinterpret_cast<int*>(w); w += align256(p.bad_bytes);
-  double* mean = reinterpret_cast<double*>(w); w += 256 * sizeof(double);
-  int* expo = reinterpret_cast<int*>(w); w += 64 * sizeof(double);
-  float* vscale = reinterpret_cast<float*>(w); w += 64 * sizeof(double);
-  double* inv_scale = reinterpret_cast<double*>(w);
+  WsView w = carve(p, ws);
   const int64_t n = desc->n_rows;
   const double c = desc->family == GP_FAMILY_RBF ? 1.4426950408889634 : -6.0;
   GP_CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)t * p.acc_ld * 8, st));
   GP_CUDA_TRY(cudaMemsetAsync(bad, 0, p.bad_bytes, st));
-  sym_scale_kernel<<<TN, 256, 0, st>>>(V, ldv, n, t, expo, vscale, inv_scale);
+  sym_scale_kernel<<<TN, 256, 0, st>>>(V, ldv, n, t, w.expo, w.vscale, w.inv_scale);
   GP_LAUNCH_CHECK();
   if (int rc = tc::distance_images(desc->Xr, desc->ldr, n, desc->Xc, desc->ldc, n, desc->d, p.DK, BT, BT, c,
-                                   mean, row_img, col_img, st))
+                                   w.mean, w.row_img, w.col_img, st))
     return rc;
   // the 128-point V image is two consecutive 64-point tile images
-  if (int rc = tc::v_images16(V, ldv, t, n, vscale, v_img, 2 * (int64_t)p.tiles, st)) return rc;
+  if (int rc = tc::v_images16(V, ldv, t, n, w.vscale, w.v_img, 2 * (int64_t)p.tiles, st)) return rc;
   Args a;
-  a.row_img = row_img; a.col_img = col_img; a.v_img = v_img; a.DK = p.DK;
+  a.row_img = w.row_img; a.col_img = w.col_img; a.v_img = w.v_img; a.DK = p.DK;
   a.n = n; a.tiles = p.tiles; a.nblocks = p.nblocks; a.n_items = p.n_items;
-  a.nsc = p.nsc; a.nsv = p.nsv; a.t = t;
-  a.expo = expo; a.acc = acc; a.acc_ld = p.acc_ld; a.bad = bad;
+  a.nsc = p.nsc; a.nsv = p.nsv; a.t = t; a.part = part; a.nparts = nparts;
+  a.expo = w.expo; a.acc = reinterpret_cast<unsigned long long*>(acc); a.acc_ld = p.acc_ld; a.bad = bad;
   a.prof = nullptr;
-  int grid = std::min(p.n_items, num_sms());
+  const int chunks = (p.n_items + ITEM_CHUNK - 1) / ITEM_CHUNK;
+  const int my_chunks = (chunks - part + nparts - 1) / nparts;
+  if (my_chunks < 1) return GP_OK;
+  int grid = std::min(my_chunks, num_sms());
   auto kern = desc->family == GP_FAMILY_RBF ? kv_sym_kernel<GP_FAMILY_RBF> : kv_sym_kernel<GP_FAMILY_MATERN32>;
   GP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   const char* pe = getenv("GP_SYM_PROF");
@@ -766,12 +818,42 @@ int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* ou
       fprintf(stderr, "\n");
     }
   }
-  int64_t tot = n * t;
-  sym_finalize_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(acc, p.acc_ld, bad, inv_scale, n, t, out, ldo,
-                                                                     desc->outputscale, desc->noise, V, ldv,
-                                                                     desc->diag_offset);
+  return GP_OK;
+}
+
+// rows [row0, row1) of s2 * K V (+ noise V) from the (summed) fixed-point
+// accumulator; the scales are recomputed from V (the same V as the partials)
+int kv_sym_finalize(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, const long long* acc,
+                    const int* bad, int64_t row0, int64_t row1, float* out, int64_t ldo, void* ws, size_t ws_bytes,
+                    cudaStream_t st) {
+  using namespace tcs;
+  GP_REQUIRE(kv_sym_supported(desc, t), "gp_kv_sym: shape unsupported by the symmetric kernel");
+  GP_REQUIRE(0 <= row0 && row0 <= row1 && row1 <= desc->n_rows, "gp_kv_sym_finalize: rows [%lld, %lld)",
+             (long long)row0, (long long)row1);
+  Plan p = make_plan(desc);
+  size_t need = kv_sym_workspace(desc, t);
+  GP_REQUIRE(ws != nullptr && ws_bytes >= need, "gp_kv(symmetric): workspace of %zu bytes required, %zu given",
+             need, ws_bytes);
+  WsView w = carve(p, ws);
+  sym_scale_kernel<<<TN, 256, 0, st>>>(V, ldv, desc->n_rows, t, w.expo, w.vscale, w.inv_scale);
+  GP_LAUNCH_CHECK();
+  const int64_t tot = (row1 - row0) * t;
+  if (tot == 0) return GP_OK;
+  sym_finalize_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(acc, p.acc_ld, bad, w.inv_scale, row0, row1, t,
+                                                                     out, ldo, desc->outputscale, desc->noise, V,
+                                                                     ldv, desc->diag_offset);
   GP_LAUNCH_CHECK();
   return GP_OK;
+}
+
+int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out, int64_t ldo, void* ws,
+           size_t ws_bytes, cudaStream_t st) {
+  using namespace tcs;
+  GP_REQUIRE(ws != nullptr && ws_bytes >= kv_sym_workspace(desc, t),
+             "gp_kv(symmetric): workspace of %zu bytes required, %zu given", kv_sym_workspace(desc, t), ws_bytes);
+  WsView w = carve(make_plan(desc), ws);
+  if (int rc = kv_sym_partial(desc, V, ldv, t, 0, 1, w.acc, w.bad, ws, ws_bytes, st)) return rc;
+  return kv_sym_finalize(desc, V, ldv, t, w.acc, w.bad, 0, desc->n_rows, out, ldo, ws, ws_bytes, st);
 }
 
 }  // namespace gp

@@ -1,12 +1,17 @@
 """Row-sharded MLL + gradients and predictive mean across GPUs (one process
 per GPU, torch.distributed) — SURVEY §8(e).
 
-Rank r owns rows [row0, row1) of K̂ and of every CG block; X, y, the probe
-block Z and the rank-k preconditioner are replicated (O(nd + nk) per GPU, as
-in the paper). Exchanges:
+Rank r owns rows [row0, row1) of every CG block; X, y, the probe block Z and
+the rank-k preconditioner are replicated (O(nd + nk) per GPU, as in the
+paper). K̂·P runs the symmetric kernel with its work items
+(unordered tile pairs) split across the ranks: each rank computes 64-bit
+fixed-point partial sums for all rows, the int64 sums are all-reduced and
+each rank finalises its rows (bitwise equal to the single-GPU product).
+Exchanges:
 
-* mBCG: all-gather of the fp32 search directions and all-reduce of the fp64
-  reduction payload each iteration (cg.MbcgRun with a TorchComm);
+* mBCG: all-gather of the fp32 search directions, all-reduce of the int64
+  K̂·P partial sums (8 n t bytes) and of the fp64 reduction payload each
+  iteration (cg.MbcgRun with a TorchComm);
 * MLL: all-reduce of the local y·a partial; the SLQ log-determinant comes
   from the all-reduced alpha/beta histories, identical on every rank;
 * gradients: all-gather of the representer weights a (8 n bytes), then each
@@ -70,8 +75,8 @@ def mll_value_and_grad_sharded(model: KernelModel, X, y, cg_config: CgConfig, pr
     cache = build_kernel_preconditioner(model, ps, cg_config.precond_rank)   # identical on every rank
     Z = draw_probes_device(n, t, probe_seed, cache)                          # identical on every rank
     Xs32, _ = ps.scaled(model.scale_for(ps.d))
-    kv = _ops.FusedKernelOperator(model.family_code, ps.d, Xs32[r0:r1], Xs32, model.outputscale, 0.0,
-                                  -1, self_offset=r0)
+    # symmetric schedule split across the ranks (row-tiled kernel for t > 16)
+    kv = _ops.training_operator(model.family_code, ps.d, Xs32, model.outputscale, 0.0, -1, comm)
     op = FusedOperator(kv, model.noise, n)
     B = T.cat([yc[:, None], Z], dim=1)[r0:r1].contiguous()
     sol = mbcg_device(op, B, cg_config.tolerance, cg_config.max_iters, cache, comm=comm, row_offset=r0)

@@ -46,16 +46,14 @@ def test_two_rank_sharded_mll_and_mean_match_single_process():
     X, y = g["X"], g["y"]
     model = gp.KernelModel("matern32", 1.0, np.linspace(0.75, 1.5, 8) * 0.5, 0.2)
     cfg = likelihood.CgConfig(tolerance=0.01, probes=10, precond_rank=50)
-    # the shards run the row-tiled kernel; compare against the same kernel on
-    # the whole operator (the single-GPU default is the symmetric kernel,
-    # equal to it only within fp32 round-off)
+    ref = gp.mll_value_and_grad(model, X, y, gp.plan_partitions(4096, 4096), gp.WorkerPool(), cfg, 3)
+    # the row-tiled kernel agrees with the symmetric one to fp32 round-off
     os.environ["GP_KV_NO_SYM"] = "1"
     try:
-        ref = gp.mll_value_and_grad(model, X, y, gp.plan_partitions(4096, 4096), gp.WorkerPool(), cfg, 3)
+        rowt = gp.mll_value_and_grad(model, X, y, gp.plan_partitions(4096, 4096), gp.WorkerPool(), cfg, 3)
     finally:
         del os.environ["GP_KV_NO_SYM"]
-    sym = gp.mll_value_and_grad(model, X, y, gp.plan_partitions(4096, 4096), gp.WorkerPool(), cfg, 3)
-    assert abs(sym.value - ref.value) <= 1e-5 * abs(ref.value)
+    assert abs(rowt.value - ref.value) <= 1e-5 * abs(ref.value)
     w = np.random.default_rng(1).standard_normal(X.shape[0])
     Xt = np.random.default_rng(2).uniform(size=(300, 8))
     cache = predictor.PredictionCache(model=model, X_train=X, weights=w, cache_tolerance=1e-3)
@@ -72,3 +70,52 @@ def test_two_rank_sharded_mll_and_mean_match_single_process():
         for k, v in ref.gradients.items():
             assert abs(got[k] - v) <= 1e-6 * scale, (k, got[k], v)
         assert np.linalg.norm(o["mean"] - ref_mean) <= 1e-5 * np.linalg.norm(ref_mean - model.mean)
+
+
+def _kv_rank_main(rank, world, port, outdir, n, d, t, fam):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_1903_08114_b200 import _device as D, _ops
+    from paper_1903_08114_b200.distributed import TorchComm
+    import paper_1903_08114_b200 as gp
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((n, d))
+    V = rng.standard_normal((n, t))
+    m = gp.KernelModel(fam, 1.3, np.linspace(0.8, 1.6, d) * np.sqrt(d), 0.2)
+    comm = TorchComm(n)
+    Xs32, _ = D.points(X).scaled(m.scale_for(d))
+    op = _ops.training_operator(m.family_code, d, Xs32, m.outputscale, m.noise, 0, comm)
+    assert isinstance(op, _ops.SymShardedKernelOperator)
+    V32 = torch.zeros((comm.rows_per_rank * world, t), dtype=torch.float32, device="cuda")
+    V32[:n] = torch.from_numpy(V).float().cuda()
+    out = op.apply32(V32, t).cpu().numpy()
+    np.save(os.path.join(outdir, f"kv{rank}.npy"), out)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_symmetric_items_split_across_ranks_bitwise_equal_single_device(world):
+    """The symmetric schedule split by work items over ranks (int64 partial
+    sums all-reduced) reproduces the single-device product bit for bit."""
+    import torch
+    import torch.multiprocessing as mp
+    import paper_1903_08114_b200 as gp
+    from paper_1903_08114_b200 import _device as D, _ops
+    n, d, t, fam = 3001, 8, 11, "matern32"
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((n, d))
+    V = rng.standard_normal((n, t))
+    m = gp.KernelModel(fam, 1.3, np.linspace(0.8, 1.6, d) * np.sqrt(d), 0.2)
+    Xs32, _ = D.points(X).scaled(m.scale_for(d))
+    single = _ops.training_operator(m.family_code, d, Xs32, m.outputscale, m.noise, 0)
+    ref = single.apply32(torch.from_numpy(V).float().cuda(), t).cpu().numpy()
+    with tempfile.TemporaryDirectory() as tmp:
+        port = 29700 + os.getpid() % 1000 + world
+        mp.spawn(_kv_rank_main, args=(world, port, tmp, n, d, t, fam), nprocs=world, join=True)
+        got = np.vstack([np.load(os.path.join(tmp, f"kv{r}.npy")) for r in range(world)])
+    assert got.shape == ref.shape
+    assert np.array_equal(got, ref)
