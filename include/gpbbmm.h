@@ -236,7 +236,9 @@ int gp_precond_factor(int64_t n, int k, const double* L, int64_t ldl, double noi
  * s2 and divides by l). fp64 output, deterministic fixed-order reduction. */
 size_t gp_grad_forms_workspace_bytes(int64_t n_rows, int64_t n_cols, int d, int ard, int w);
 /* self_offset: row i of Xr is column i + self_offset of Xc (-1 = unrelated);
- * algo: 0 = auto (tcgen05 when d + 2 <= 32 and w <= 128), 1 = SIMT, 2 = tcgen05 */
+ * algo: 0 = auto (ARD with d + 2 <= 32 and w <= 112: per-dimension sums on the tensor
+ *       core, grad_ard.cu; otherwise tcgen05 when d + 2 <= 32 and w <= 128, else SIMT),
+ *       1 = SIMT, 2 = tcgen05 per-entry epilogue, 3 = tcgen05 ARD (as auto) */
 int gp_grad_forms(int family, int d, int ard, const float* Xr, int64_t ldr, int64_t n_rows,
                   const float* Xc, int64_t ldc, int64_t n_cols, double outputscale,
                   const float* Y, int64_t ldy, const float* R, int64_t ldrr, int w,

@@ -183,6 +183,11 @@ __global__ void grad_finalize(const double* __restrict__ partials, int nblocks, 
 }
 
 bool grad_tc_supported(int64_t nr, int64_t nc, int d, int ard, int w);
+bool grad_ard_supported(int64_t nr, int64_t nc, int d, int w);
+size_t grad_ard_workspace(int64_t nr, int64_t nc, int d, int w);
+int grad_ard(int family, int d, const float* Xr, int64_t ldr, int64_t nr, const float* Xc, int64_t ldc, int64_t nc,
+             const float* Y, int64_t ldy, const float* R, int64_t ldrr, int w, int64_t self_offset, double* out,
+             void* ws, size_t ws_bytes, cudaStream_t st);
 size_t grad_tc_workspace(int64_t nr, int64_t nc, int d, int ard, int w);
 int grad_tc(int family, int d, int ard, const float* Xr, int64_t ldr, int64_t nr, const float* Xc,
             int64_t ldc, int64_t nc, const float* Y, int64_t ldy, const float* R, int64_t ldrr, int w,
@@ -209,7 +214,9 @@ size_t gp_grad_forms_workspace_bytes(int64_t n_rows, int64_t n_cols, int d, int 
   int64_t row_tiles = (n_rows + gBM - 1) / gBM;
   size_t simt = (size_t)((row_tiles + 2LL * num_sms() + 1) * 17) * sizeof(double);
   size_t tcw = grad_tc_supported(n_rows, n_cols, d, ard, w) ? grad_tc_workspace(n_rows, n_cols, d, ard, w) : 0;
-  return simt > tcw ? simt : tcw;
+  size_t gaw = ard && grad_ard_supported(n_rows, n_cols, d, w) ? grad_ard_workspace(n_rows, n_cols, d, w) : 0;
+  simt = simt > tcw ? simt : tcw;
+  return simt > gaw ? simt : gaw;
 }
 
 int gp_grad_forms(int family, int d, int ard, const float* Xr, int64_t ldr, int64_t n_rows,
@@ -226,6 +233,11 @@ int gp_grad_forms(int family, int d, int ard, const float* Xr, int64_t ldr, int6
     GP_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double) * nparams, st));
     return GP_OK;
   }
+  // ARD: per-dimension sums on the tensor core (grad_ard.cu); algo 2 forces
+  // the per-entry tcgen05 epilogue (grad_tc.cu), algo 1 the SIMT kernel
+  if (ard && (algo == 0 || algo == 3) && grad_ard_supported(n_rows, n_cols, d, w))
+    return grad_ard(family, d, Xr, ldr, n_rows, Xc, ldc, n_cols, Y, ldy, R, ldrr, w, self_offset, out, workspace,
+                    workspace_bytes, st);
   const bool tc_ok = grad_tc_supported(n_rows, n_cols, d, ard, w);
   if (algo == 2 || (algo == 0 && tc_ok)) {
     GP_REQUIRE(tc_ok, "gp_grad_forms: shape unsupported by the tcgen05 kernel (d=%d w=%d)", d, w);

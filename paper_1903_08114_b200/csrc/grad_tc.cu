@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(G_NTHREADS, 1) grad_tc_kernel(const GArgs a) {
         const float* xy = ARD ? reinterpret_cast<const float*>(stages + s * stage_bytes + col_bytes + r_bytes) +
                                     (half * 32) * DP
                               : nullptr;
-#pragma unroll 4
+#pragma unroll
         for (int e = 0; e < 32; ++e) {
           const float S = __uint_as_float(sv[e]);
           const float h = __uint_as_float(hv[e]);

@@ -218,3 +218,10 @@ def test_grad_forms_tcgen05_vs_simt(fam, ard, d, w):
     b0 = likelihood._grad_forms_raw(m, d, Xs32[:h], Xs32, Y[:h], R, 0, algo=2).cpu().numpy()
     b1 = likelihood._grad_forms_raw(m, d, Xs32[h:], Xs32, Y[h:], R, h, algo=2).cpu().numpy()
     np.testing.assert_allclose(b0 + b1, b, rtol=0, atol=2e-5 * scale + 1e-9)
+    if ard and d + 2 <= 32:
+        # per-dimension sums on the tensor core (bf16 two-term split, G = W [X | X^2])
+        c = likelihood._grad_forms_raw(m, d, Xs32, Xs32, Y, R, 0, algo=3).cpu().numpy()
+        np.testing.assert_allclose(c, a, rtol=0, atol=1e-4 * scale + 1e-9)
+        c0 = likelihood._grad_forms_raw(m, d, Xs32[:h], Xs32, Y[:h], R, 0, algo=3).cpu().numpy()
+        c1 = likelihood._grad_forms_raw(m, d, Xs32[h:], Xs32, Y[h:], R, h, algo=3).cpu().numpy()
+        np.testing.assert_allclose(c0 + c1, a, rtol=0, atol=1e-4 * scale + 1e-9)
