@@ -30,7 +30,7 @@ namespace ga {
 
 using namespace gp::tc;
 
-constexpr int BM = 128, BN = 64;
+constexpr int BM = 128;         // rows per tile; columns per tile BN = 64 (d + 2 <= 32) or 32 (larger d)
 constexpr int NTHREADS = 384;   // 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4-11 epilogue
 constexpr int EPI0 = 4, NEPI = 8;
 constexpr int MAXNL = 32;       // ARD dimensions per launch (G = 2 nl <= 64 TMEM columns)
@@ -51,10 +51,19 @@ struct Args {
   double* partials;       // [gridDim.x][1 + MAXNL]
 };
 
-// TMEM columns: S_b 64b | H_b 128 + 64b | Y1 256 | Y2 256 + WP | W1 368 | W2 400 | G 432
-__device__ __forceinline__ uint32_t TS_(uint32_t b) { return 64u * b; }
-__device__ __forceinline__ uint32_t TH_(uint32_t b) { return 128u + 64u * b; }
-constexpr uint32_t TY = 256, TW1 = 368, TW2 = 400, TG = 432;
+// TMEM columns (BN = 64: S_b 64b | H_b 128 + 64b | Y 256 | W1 368 | W2 400 | G 432;
+// BN = 32 halves the S, H and W blocks): S_b, H_b double buffered, Y1 | Y2
+// resident per row tile (<= 2 x 56 bf16-pair columns), W1 | W2 (the G
+// product's A operand), G = [W X | W X^2] (<= 64 columns)
+template <int BN> struct Tm {
+  __host__ __device__ static constexpr uint32_t S(uint32_t b) { return (uint32_t)BN * b; }
+  __host__ __device__ static constexpr uint32_t H(uint32_t b) { return 2u * BN + (uint32_t)BN * b; }
+  static constexpr uint32_t Y = 4u * BN;
+  static constexpr uint32_t W1 = Y + 2u * MAXWP;
+  static constexpr uint32_t W2 = W1 + BN / 2;
+  static constexpr uint32_t G = W2 + BN / 2;
+  static_assert(G + 64 <= 512, "TMEM plan");
+};
 
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -67,8 +76,10 @@ __device__ __forceinline__ void split_bf16(float a, float b, uint32_t& p1, uint3
   p2 = *reinterpret_cast<const uint32_t*>(&h2);
 }
 
-template <int FAM>
+template <int FAM, int BN>
 __global__ void __launch_bounds__(NTHREADS, 1) grad_ard_kernel(const Args a) {
+  using TM = Tm<BN>;
+  constexpr int CW = BN / 2;   // columns of a tile per epilogue warp
   extern __shared__ __align__(1024) uint8_t smem[];
   const int DK = a.DK, WK = a.WK, GN = a.GN;
   const uint32_t row_bytes = 2u * BM * DK * 4u;
@@ -168,7 +179,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_ard_kernel(const Args a) {
     const uint32_t ka16 = (2 * lbo_a) >> 4, kb16 = (2 * lbo_b) >> 4;
     const uint32_t kr16 = (2 * lbo_r) >> 4, kx16 = (2 * lbo_x) >> 4;
     const int dsteps = DK / 8, hsteps = WK / 16;
-    const uint32_t ty1 = tmem + TY, ty2 = tmem + TY + (uint32_t)a.WP;
+    const uint32_t ty1 = tmem + TM::Y, ty2 = tmem + TM::Y + (uint32_t)a.WP;
     const bool leader = elect_one();
     uint32_t s = 0, ph = 0, T = 0, itc = 0;
     auto issue_g = [&](uint32_t Tg, uint32_t sg, bool fresh, bool last) {
@@ -177,10 +188,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_ard_kernel(const Args a) {
       tc_fence_after();
       if (leader) {
         const uint64_t dx = dx0 + (uint64_t)(sg * stage16);
-        const uint32_t g = tmem + TG;
+        const uint32_t g = tmem + TM::G;
 #pragma unroll
         for (int pass = 0; pass < 3; ++pass) {   // W1.XX1 + W1.XX2 + W2.XX1
-          const uint32_t wa = tmem + (pass == 2 ? TW2 : TW1);
+          const uint32_t wa = tmem + (pass == 2 ? TM::W2 : TM::W1);
           const uint64_t xb = dx + (pass == 1 ? x_half16 : 0u);
 #pragma unroll
           for (int ks = 0; ks < BN / 16; ++ks)
@@ -206,7 +217,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_ard_kernel(const Args a) {
         mbar_wait(smem_u32(&full[s]), ph);
         tc_fence_after();
         if (leader) {
-          const uint32_t d_s = tmem + TS_(b), d_h = tmem + TH_(b);
+          const uint32_t d_s = tmem + TM::S(b), d_h = tmem + TM::H(b);
           const uint64_t db = db0 + (uint64_t)(s * stage16);
           const uint64_t dr = dr0 + (uint64_t)(s * stage16);
 #pragma unroll
@@ -256,7 +267,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_ard_kernel(const Args a) {
       tc_fence_after();
       {
         const uint32_t* src = a.y_rows + row * (2 * (int64_t)a.WP) + half * a.WP;
-        const uint32_t dst = tmem + lane_base + TY + (uint32_t)(half * a.WP);
+        const uint32_t dst = tmem + lane_base + TM::Y + (uint32_t)(half * a.WP);
         for (int c0 = 0; c0 < a.WP; c0 += 8) {
           uint32_t v[8];
 #pragma unroll
@@ -272,27 +283,32 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_ard_kernel(const Args a) {
         if (lane == 0) mbar_arrive(smem_u32(y_full));
       }
       const int64_t diag_col = (a.self_offset >= 0 && row < a.n_rows) ? row + a.self_offset : -1000;
-      int64_t e_diag = diag_col - ((int64_t)ct0 * BN + half * 32);
+      int64_t e_diag = diag_col - ((int64_t)ct0 * BN + half * CW);
       float rs = 0.f;   // sum_j W_ij over this warp's columns of the item
       for (int ct = ct0; ct < ct1; ++ct, e_diag -= BN, ++T) {
         const uint32_t b = T & 1;
         mbar_wait(smem_u32(&s_full[b]), (T >> 1) & 1);
         tc_fence_after();
-        uint32_t sv[32], hv[32];
-        tmem_ld32(tmem + lane_base + TS_(b) + half * 32, sv);
-        tmem_ld32(tmem + lane_base + TH_(b) + half * 32, hv);
+        uint32_t sv[CW], hv[CW];
+        if constexpr (CW == 32) {
+          tmem_ld32(tmem + lane_base + TM::S(b) + half * CW, reinterpret_cast<uint32_t (&)[32]>(sv));
+          tmem_ld32(tmem + lane_base + TM::H(b) + half * CW, reinterpret_cast<uint32_t (&)[32]>(hv));
+        } else {
+          tmem_ld16(tmem + lane_base + TM::S(b) + half * CW, reinterpret_cast<uint32_t (&)[16]>(sv));
+          tmem_ld16(tmem + lane_base + TM::H(b) + half * CW, reinterpret_cast<uint32_t (&)[16]>(hv));
+        }
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&s_empty[b]));
-        if (__any_sync(0xffffffffu, e_diag >= 0 && e_diag < 32)) {
+        if (__any_sync(0xffffffffu, e_diag >= 0 && e_diag < CW)) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
+          for (int e = 0; e < CW; ++e)
             if (e == e_diag) sv[e] = 0u;
         }
         float a0 = 0.f;
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
+        for (int e = 0; e < CW; ++e) {
           const float S = __uint_as_float(sv[e]);
           const float h = __uint_as_float(hv[e]);
           float kap, eps;
@@ -311,14 +327,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_ard_kernel(const Args a) {
           hv[e] = __float_as_uint(wv);
         }
         acc0 += (double)a0;
-        uint32_t p1[16], p2[16];
+        uint32_t p1[CW / 2], p2[CW / 2];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) split_bf16(__uint_as_float(hv[2 * k]), __uint_as_float(hv[2 * k + 1]), p1[k], p2[k]);
-        // W (this warp's 32 columns = 16 pair columns) once G of the previous tile is done with it
+        for (int k = 0; k < CW / 2; ++k)
+          split_bf16(__uint_as_float(hv[2 * k]), __uint_as_float(hv[2 * k + 1]), p1[k], p2[k]);
+        // W (this warp's CW columns = CW / 2 pair columns) once G of the previous tile is done with it
         if (T >= 1) mbar_wait(smem_u32(w_empty), (T - 1) & 1);
         tc_fence_after();
-        tmem_st16(tmem + lane_base + TW1 + half * 16, p1);
-        tmem_st16(tmem + lane_base + TW2 + half * 16, p2);
+        if constexpr (CW == 32) {
+          tmem_st16(tmem + lane_base + TM::W1 + half * 16, reinterpret_cast<const uint32_t (&)[16]>(p1));
+          tmem_st16(tmem + lane_base + TM::W2 + half * 16, reinterpret_cast<const uint32_t (&)[16]>(p2));
+        } else {
+          tmem_st8(tmem + lane_base + TM::W1 + half * 8, p1);
+          tmem_st8(tmem + lane_base + TM::W2 + half * 8, p2);
+        }
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -332,8 +354,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_ard_kernel(const Args a) {
       for (int k0 = 0; k0 < a.nl; k0 += 16) {
         uint32_t gx[16], gq[16];
         if (half == 0) {
-          tmem_ld16(tmem + lane_base + TG + k0, gx);
-          tmem_ld16(tmem + lane_base + TG + a.nl + k0, gq);
+          tmem_ld16(tmem + lane_base + TM::G + k0, gx);
+          tmem_ld16(tmem + lane_base + TM::G + a.nl + k0, gq);
           tmem_wait_ld();
         }
 #pragma unroll
@@ -388,8 +410,8 @@ __global__ void y_bf16_kernel(const float* __restrict__ Y, int64_t ldy, int64_t 
 }
 
 // R image per 64-column tile: bf16 K-major (rows = columns j, K = w), R1 then R2
-__global__ void r_bf16_kernel(const float* __restrict__ R, int64_t ldr, int64_t n, int w, int WK, int64_t ntiles,
-                              __nv_bfloat16* img) {
+__global__ void r_bf16_kernel(const float* __restrict__ R, int64_t ldr, int64_t n, int w, int WK, int BN,
+                              int64_t ntiles, __nv_bfloat16* img) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= ntiles * BN * WK) return;
   const int64_t tile = idx / (BN * WK);
@@ -407,7 +429,7 @@ __global__ void r_bf16_kernel(const float* __restrict__ R, int64_t ldr, int64_t 
 // [X | X^2] image per 64-column tile (centred coordinates of dims p0..p0+nl):
 // bf16 K-major with rows = the GN outputs (x_k, then x_k^2), K = the 64 columns
 __global__ void xx_bf16_kernel(const float* __restrict__ X, int64_t ldx, int64_t n, const double* __restrict__ mean,
-                               int p0, int nl, int GN, int64_t ntiles, __nv_bfloat16* img) {
+                               int p0, int nl, int GN, int BN, int64_t ntiles, __nv_bfloat16* img) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= ntiles * BN * GN) return;
   const int64_t tile = idx / (BN * GN);
@@ -437,7 +459,7 @@ __global__ void grad_ard_finalize(const double* __restrict__ partials, int nbloc
 }
 
 struct Plan {
-  int DK, WK, WP, row_tiles, col_tiles, splits, tiles_per_split, nstages, grid;
+  int BN, DK, WK, WP, row_tiles, col_tiles, splits, tiles_per_split, nstages, grid;
   size_t row_img, col_img, r_img, xx_img, y_rows, partials, smem;
 };
 
@@ -446,6 +468,8 @@ static int gn_for(int nl) { return std::max(16, (2 * nl + 15) / 16 * 16); }
 static Plan make_plan(int64_t nr, int64_t nc, int d, int w) {
   Plan p;
   p.DK = (d + 2 + 7) / 8 * 8;
+  const int BN = p.DK <= 32 ? 64 : 32;   // large d: narrower tiles keep two SMEM stages
+  p.BN = BN;
   p.WK = (w + 15) / 16 * 16;
   p.WP = p.WK / 2;
   p.row_tiles = (int)((nr + BM - 1) / BM);
@@ -475,10 +499,11 @@ static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace ga
 
-// ARD gradients on the tensor core: dims up to 30 (distance image in the
-// SMEM plan), w <= 112 (Y resident in TMEM as bf16 pairs)
+// ARD gradients on the tensor core: dims up to 94 (64-column tiles up to
+// d = 30, 32-column tiles beyond, for the SMEM plan), w <= 112 (Y resident in
+// TMEM as bf16 pairs)
 bool grad_ard_supported(int64_t nr, int64_t nc, int d, int w) {
-  if (d < 1 || d + 2 > 32 || w < 1 || w > 2 * ga::MAXWP || nr < 1 || nc < 1) return false;
+  if (d < 1 || d + 2 > 96 || w < 1 || w > 2 * ga::MAXWP || nr < 1 || nc < 1) return false;
   return ga::make_plan(nr, nc, d, w).nstages >= 2;
 }
 
@@ -504,6 +529,7 @@ int grad_ard(int family, int d, const float* Xr, int64_t ldr, int64_t nr, const 
   double* partials = reinterpret_cast<double*>(wp); wp += al256(p.partials);
   double* mean = reinterpret_cast<double*>(wp);
   const double c = family == GP_FAMILY_RBF ? 1.4426950408889634 : -6.0;
+  const int BN = p.BN;
   if (int rc = tc::distance_images(Xr, ldr, nr, Xc, ldc, nc, d, p.DK, BM, BN, c, mean, row_img, col_img, st))
     return rc;
   {
@@ -512,7 +538,7 @@ int grad_ard(int family, int d, const float* Xr, int64_t ldr, int64_t nr, const 
     y_bf16_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(Y, ldy, nr, w, p.WP, rows_pad, y_rows);
     GP_LAUNCH_CHECK();
     tot = (int64_t)p.col_tiles * BN * p.WK;
-    r_bf16_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(R, ldrr, nc, w, p.WK, p.col_tiles, r_img);
+    r_bf16_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(R, ldrr, nc, w, p.WK, BN, p.col_tiles, r_img);
     GP_LAUNCH_CHECK();
   }
   Args a;
@@ -521,7 +547,9 @@ int grad_ard(int family, int d, const float* Xr, int64_t ldr, int64_t nr, const 
   a.n_rows = nr; a.n_cols = nc; a.row_tiles = p.row_tiles; a.col_tiles = p.col_tiles;
   a.splits = p.splits; a.tiles_per_split = p.tiles_per_split; a.nstages = p.nstages;
   a.self_offset = self_offset; a.partials = partials;
-  auto kern = family == GP_FAMILY_RBF ? grad_ard_kernel<GP_FAMILY_RBF> : grad_ard_kernel<GP_FAMILY_MATERN32>;
+  auto kern = family == GP_FAMILY_RBF
+                  ? (BN == 64 ? grad_ard_kernel<GP_FAMILY_RBF, 64> : grad_ard_kernel<GP_FAMILY_RBF, 32>)
+                  : (BN == 64 ? grad_ard_kernel<GP_FAMILY_MATERN32, 64> : grad_ard_kernel<GP_FAMILY_MATERN32, 32>);
   GP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   const int nchunks = (d + MAXNL - 1) / MAXNL;
   for (int ch = 0; ch < nchunks; ++ch) {
@@ -529,8 +557,8 @@ int grad_ard(int family, int d, const float* Xr, int64_t ldr, int64_t nr, const 
     a.nl = std::min(MAXNL, d - a.p0);
     a.GN = gn_for(a.nl);
     const int64_t tot = (int64_t)p.col_tiles * BN * a.GN;
-    xx_bf16_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(Xc, ldc, nc, mean, a.p0, a.nl, a.GN, p.col_tiles,
-                                                                  xx_img);
+    xx_bf16_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(Xc, ldc, nc, mean, a.p0, a.nl, a.GN, BN,
+                                                                  p.col_tiles, xx_img);
     GP_LAUNCH_CHECK();
     kern<<<p.grid, NTHREADS, p.smem, st>>>(a);
     GP_LAUNCH_CHECK();
