@@ -132,6 +132,22 @@ def test_row_subsets_large_configs(key):
         assert colrel(got, exp) <= KV_RTOL, (key, s, colrel(got, exp))
 
 
+@pytest.mark.parametrize("key", ["C2", "C3", "C5", "M1e6"])
+def test_symmetric_full_operator_vs_reference_rows(key):
+    """The default training operator (symmetric kernel, whole square
+    operator in one launch) at full size, checked on the reference's golden
+    rows."""
+    g = load_golden("row_subsets")
+    w = syn.WORKLOADS[key]
+    X = syn.whitened_inputs(w.n, w.d, 0)
+    V = syn.rhs_block(w.n, 11, 2)
+    full = _kv_rows(w, X, V, 0, w.n, algo=3)
+    rows = int(g[f"{key}_rows"])
+    for s, exp in zip(g[f"{key}_starts"], g[f"{key}_KV"]):
+        s = int(s)
+        assert colrel(full[s:s + rows], exp) <= KV_RTOL, (key, s, colrel(full[s:s + rows], exp))
+
+
 def test_row_shards_bitwise_equal_full():
     """Row sharding (the multi-GPU decomposition) reproduces the full product
     bit-for-bit: per-row reduction order depends only on the column count."""
