@@ -293,3 +293,21 @@ def test_symmetric_kernel_edges_vs_oracle(fam):
         got = op.apply32(torch.from_numpy(V).float().cuda(), t).double().cpu().numpy()
         ref = O.kernel_mvm(O.make_hp(fam, 1.3, ls, 0.2), X, V)
         assert colrel(got, ref) <= KV_RTOL, (n, d, t, colrel(got, ref))
+
+
+def test_symmetric_kernel_propagates_nonfinite_inputs():
+    """A NaN coordinate poisons its row and column of K̂: the symmetric
+    kernel's fixed-point path flags the rows (NaN out), never a finite value."""
+    import torch
+    from paper_1903_08114_b200 import _device as D, _ops
+    rng = np.random.default_rng(3)
+    n, d, t = 1000, 6, 11
+    X = rng.standard_normal((n, d))
+    X[417, 2] = np.nan
+    V = rng.standard_normal((n, t))
+    m = gp.KernelModel("matern32", 1.0, np.ones(d), 0.1)
+    Xs32, _ = D.points(X).scaled(m.scale_for(d))
+    op = _ops.FusedKernelOperator(m.family_code, d, Xs32, Xs32, 1.0, 0.1, 0, algo=3)
+    out = op.apply32(torch.from_numpy(V).float().cuda(), t).cpu().numpy()
+    assert np.isnan(out[417]).all()
+    assert not np.isfinite(out).all(axis=1).any(), "a row touching the NaN column came out finite"
