@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
   uint64_t* s_full = vi_empty + 2;      // [2]   S in TMEM buffer b            MMA -> kappa
   uint64_t* k_full = s_full + 2;        // [2]   K written (TMEM + SMEM)       kappa -> MMA
   uint64_t* sk_empty = k_full + 2;      // [2]   products done with buffer b   MMA -> MMA
-  uint64_t* ks_empty = sk_empty + 2;    //       products done with the SMEM K MMA -> kappa
+  uint64_t* ks_empty = sk_empty + 2;    //       mirror products done with the SMEM K  MMA -> kappa
   uint64_t* xr_full = ks_empty + 1;     //       row image landed              TMA -> MMA
   uint64_t* xr_empty = xr_full + 1;     //       row image copied into TMEM    MMA -> TMA
   uint64_t* oi_full = xr_empty + 1;     // [2]   row's direct products done    MMA -> drain
@@ -417,8 +417,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
 #pragma unroll
           for (int k = 0; k < BT / 16; ++k)   // O_J[:, 0:16] += K2^T . V1
             mma16_ss(oj, dks + (uint64_t)(ks2_16 + 16 * k), vib + (uint64_t)(k * kstep_v16), idesc_m16, 1);
+          tc_commit(smem_u32(ks_empty));   // one phase per mirror tile: every phase has a waiter
         }
-        tc_commit(smem_u32(ks_empty));
         const uint32_t oi = tmem + TOI(rowc & 1), sk = tmem + TSK(b);
         const uint64_t vb = dv0 + (uint64_t)(vs * vt16);
         const uint32_t fresh = it.first_in_row() ? 1u : 0u;
@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
     const uint32_t ks_row = smem_u32(ks) + 16u * (uint32_t)i_loc + (uint32_t)(4 * ch) * 2048u;
     TileSeq it;
     it.begin(a);
-    uint32_t T = 0;
+    uint32_t T = 0, Mt = 0;   // tiles, mirror tiles
     while (it.ok) {
       const uint32_t b = T & 1;
       SYM_T(0, mbar_wait(smem_u32(&s_full[b]), (T >> 1) & 1));
@@ -495,7 +495,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       tmem_st8(sk + 24, p2 + 8);
       if (mir) {
         // K^T operand: 8 consecutive j of point i = one 16-byte core-matrix row
-        if (T >= 1) SYM_T(2, mbar_wait(smem_u32(ks_empty), (T - 1) & 1));
+        // the previous mirror tile's products have read the SMEM K
+        if (Mt >= 1) SYM_T(2, mbar_wait(smem_u32(ks_empty), (Mt - 1) & 1));
+        ++Mt;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
           sts128(ks_row + m * 2048u, p1[4 * m], p1[4 * m + 1], p1[4 * m + 2], p1[4 * m + 3]);

@@ -1,0 +1,71 @@
+"""Memory contract and sanitizer runs (the reference's
+`test_largest_transient_buffer_is_one_block` / `test_tracemalloc_agrees_at_small_scale`,
+test_partition.py:132-158, restated for the device: no n x n buffer ever
+exists, peak device memory grows linearly in n; and compute-sanitizer
+memcheck / synccheck over every kernel family at small shapes)."""
+
+import os
+import shutil
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import paper_1903_08114_b200 as gp
+from paper_1903_08114_b200 import kernels, likelihood
+
+pytestmark = pytest.mark.gpu
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _peak_bytes(fn):
+    import torch
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    base = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    fn()
+    torch.cuda.synchronize()
+    return torch.cuda.max_memory_allocated() - base
+
+
+def _mll_peak(n, d=6):
+    rng = np.random.default_rng(n)
+    X = rng.uniform(size=(n, d))
+    y = rng.standard_normal(n)
+    m = gp.KernelModel("matern32", 1.0, np.linspace(0.4, 0.8, d), 0.3)
+
+    def run():
+        gp.mll_value_and_grad(m, X, y, gp.plan_partitions(n, 1024), gp.WorkerPool(),
+                              likelihood.CgConfig(tolerance=1.0, probes=10, precond_rank=20), 0)
+        gp.partitioned_mvm(kernels.training_mvm_oracle(m), X, rng.standard_normal((n, 11)),
+                           gp.plan_partitions(n, 1024), gp.WorkerPool())
+    run()  # grow-only workspaces reach their size for this n
+    return _peak_bytes(run)
+
+
+def test_device_memory_is_linear_in_n():
+    n1, n2 = 8192, 32768
+    p1, p2 = _mll_peak(n1), _mll_peak(n2)
+    # O(n (d + t + k)) state; an n x n fp32 block at n2 alone would be 4.3 GB
+    assert p2 < n2 * n2 * 4 / 64, (p1, p2)
+    assert p2 < 6.0 * max(p1, 1), (p1, p2)   # 4x the points -> ~4x the memory, not 16x
+
+
+def _sanitizer():
+    for c in ("/usr/local/cuda/bin/compute-sanitizer", shutil.which("compute-sanitizer")):
+        if c and os.path.exists(c):
+            return c
+    pytest.skip("compute-sanitizer not found")
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "synccheck"])
+def test_compute_sanitizer_clean(tool):
+    cmd = [_sanitizer(), "--tool", tool, "--error-exitcode", "97", "--print-limit", "20",
+           sys.executable, os.path.join(REPO, "scripts", "sanitize_small.py")]
+    r = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=1500)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "sanitize workload ok" in out, out[-4000:]
+    assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
