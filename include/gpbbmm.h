@@ -112,6 +112,10 @@ int gp_kv(const gp_kv_desc* desc, const float* V, int64_t ldv, int t,
  * Workspace: gp_kv_workspace_bytes(desc, t). gp_kv_sym_supported tells
  * whether the descriptor qualifies (d <= 14, t <= 16, whole square operator). */
 int gp_kv_sym_supported(const gp_kv_desc* desc, int t);
+/* 1 when gp_kv with algo 0 picks the symmetric kernel for this descriptor
+ * (supported and at least ~12k points, where its work items fill the SMs);
+ * a multi-device caller uses it to make the same choice as one device. */
+int gp_kv_sym_auto(const gp_kv_desc* desc, int t);
 int64_t gp_kv_sym_acc_ld(const gp_kv_desc* desc);
 int gp_kv_sym_partial(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, int part, int nparts,
                       int64_t* acc, int32_t* bad, void* workspace, size_t workspace_bytes, void* stream);

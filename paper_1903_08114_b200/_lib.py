@@ -50,6 +50,7 @@ _SIGS = {
     "gp_kv_workspace_bytes": (c_sz, [C.POINTER(KvDesc), C.c_int]),
     "gp_kv": (C.c_int, [C.POINTER(KvDesc), c_p, c_i64, C.c_int, c_p, c_i64, c_p, c_sz, c_p]),
     "gp_kv_sym_supported": (C.c_int, [C.POINTER(KvDesc), C.c_int]),
+    "gp_kv_sym_auto": (C.c_int, [C.POINTER(KvDesc), C.c_int]),
     "gp_kv_sym_acc_ld": (c_i64, [C.POINTER(KvDesc)]),
     "gp_kv_sym_partial": (C.c_int, [C.POINTER(KvDesc), c_p, c_i64, C.c_int, C.c_int, C.c_int, c_p, c_p, c_p,
                                     c_sz, c_p]),

@@ -82,11 +82,12 @@ class SymShardedKernelOperator:
     integer sums are all-reduced (deterministic), and each rank finalises its
     own rows — bitwise equal to the single-device gp_kv result. Every rank
     then evaluates ~n^2/(2 world) kernel entries instead of n^2/world. Falls
-    back to the row-tiled kernel (`fallback`) for shapes the symmetric kernel
-    does not take (t > 16)."""
+    back to the row-tiled kernel (`fallback`) where one device would not use
+    the symmetric kernel either (t > 16, or too few points to fill the SMs,
+    gp_kv_sym_auto), unless `force` (algo 3) asks for it whenever supported."""
 
     def __init__(self, family_code: int, d: int, X32_full, outputscale: float, noise: float,
-                 diag_offset: int, comm, fallback=None):
+                 diag_offset: int, comm, fallback=None, force: bool = False):
         self.desc = _lib.KvDesc(family=family_code, d=d, Xr=_lib.ptr(X32_full), ldr=X32_full.stride(0),
                                 n_rows=X32_full.shape[0], Xc=_lib.ptr(X32_full), ldc=X32_full.stride(0),
                                 n_cols=X32_full.shape[0], outputscale=float(outputscale),
@@ -97,10 +98,12 @@ class SymShardedKernelOperator:
         self.n_rows = self.row1 - self.row0
         self.n_cols = X32_full.shape[0]
         self.fallback = fallback
+        self.force = bool(force)
         self._acc = None
 
     def supported(self, t: int) -> bool:
-        return bool(_lib.lib().gp_kv_sym_supported(self.desc, t))
+        L = _lib.lib()
+        return bool(L.gp_kv_sym_supported(self.desc, t) if self.force else L.gp_kv_sym_auto(self.desc, t))
 
     def apply32(self, V32_full, t: int, out32=None):
         """out32[:, :t] = rows [row0, row1) of K V32_full[:n, :t]."""
@@ -145,7 +148,7 @@ def training_operator(family_code: int, d: int, X32_full, outputscale: float, no
     if algo not in (0, 3):
         return rows
     return SymShardedKernelOperator(family_code, d, X32_full, outputscale, noise, diag_offset, comm,
-                                    fallback=rows)
+                                    fallback=rows, force=algo == 3)
 
 
 def coldot(A, B):

@@ -465,10 +465,15 @@ static bool use_tc(const gp_kv_desc* d, int t) {
   return gp_has_tcgen05() && gp::kv_tc_supported(d, t);
 }
 // auto: the symmetric kernel whenever the call is the whole square training
-// operator (each unordered pair evaluated once); GP_KV_NO_SYM=1 opts out
+// operator (each unordered pair evaluated once) with enough work items to
+// fill the SMs: below ~12k points its 4 x 4-tile items leave most SMs idle and
+// the row-tiled kernel is faster (n = 8192: 0.11 vs 0.18 ms; n = 16384: 0.24
+// vs 0.19 ms, profiles/r01d_small_n.md). GP_KV_NO_SYM=1 opts out.
+constexpr int64_t kSymAutoMinPoints = 12288;
 static bool use_sym(const gp_kv_desc* d, int t) {
   if (d->algo == 3) return true;
   if (d->algo != 0 || !gp_has_tcgen05() || !gp::kv_sym_supported(d, t)) return false;
+  if (d->n_rows < kSymAutoMinPoints) return false;
   const char* e = getenv("GP_KV_NO_SYM");
   return !(e && *e == '1');
 }
@@ -518,6 +523,13 @@ int gp_kv(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out
 
 int gp_kv_sym_supported(const gp_kv_desc* desc, int t) {
   return desc != nullptr && gp_has_tcgen05() && gp::kv_sym_supported(desc, t) ? 1 : 0;
+}
+
+int gp_kv_sym_auto(const gp_kv_desc* desc, int t) {
+  if (desc == nullptr || t < 1) return 0;
+  gp_kv_desc d = *desc;
+  d.algo = 0;
+  return use_sym(&d, t) ? 1 : 0;
 }
 
 int64_t gp_kv_sym_acc_ld(const gp_kv_desc* desc) {

@@ -89,7 +89,7 @@ def _kv_rank_main(rank, world, port, outdir, n, d, t, fam):
     m = gp.KernelModel(fam, 1.3, np.linspace(0.8, 1.6, d) * np.sqrt(d), 0.2)
     comm = TorchComm(n)
     Xs32, _ = D.points(X).scaled(m.scale_for(d))
-    op = _ops.training_operator(m.family_code, d, Xs32, m.outputscale, m.noise, 0, comm)
+    op = _ops.training_operator(m.family_code, d, Xs32, m.outputscale, m.noise, 0, comm, algo=3)
     assert isinstance(op, _ops.SymShardedKernelOperator)
     V32 = torch.zeros((comm.rows_per_rank * world, t), dtype=torch.float32, device="cuda")
     V32[:n] = torch.from_numpy(V).float().cuda()
@@ -113,7 +113,7 @@ def test_symmetric_items_split_across_ranks_bitwise_equal_single_device(world):
     V = rng.standard_normal((n, t))
     m = gp.KernelModel(fam, 1.3, np.linspace(0.8, 1.6, d) * np.sqrt(d), 0.2)
     Xs32, _ = D.points(X).scaled(m.scale_for(d))
-    single = _ops.training_operator(m.family_code, d, Xs32, m.outputscale, m.noise, 0)
+    single = _ops.training_operator(m.family_code, d, Xs32, m.outputscale, m.noise, 0, algo=3)
     ref = single.apply32(torch.from_numpy(V).float().cuda(), t).cpu().numpy()
     with tempfile.TemporaryDirectory() as tmp:
         port = 29700 + os.getpid() % 1000 + world
