@@ -318,9 +318,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    // per tile T: dist(T+1) (into the other S/K buffer, once the products of
-    // T-1 are done with it), then direct(T) and mirror(T) once the kappa warps
-    // have written K(T)
+    // per tile T: dist(T+1) (into the other S/K buffer, once the direct
+    // product of T-1 is done with it), then direct(T) and mirror(T) once the
+    // kappa warps have written K(T)
     const uint32_t idesc_d = make_idesc(BT, BT);
     const uint32_t idesc_n16 = idesc_f16(BT, TN), idesc_n32 = idesc_f16(BT, 2 * TN);
     const uint32_t idesc_m32 = idesc_f16(BT, 2 * TN) | IDESC_A_MN_MAJOR;
@@ -406,7 +406,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       if (mir) SYM_T(5, mbar_wait(smem_u32(&vi_full[rowc & 1]), (rowc >> 1) & 1));
       tc_fence_after();
       if (leader) {
-        // mirror first: its completion releases the SMEM K for the next tile
+        // direct first, then release the S/K buffer: the mirror reads only
+        // SMEM, so it keeps the tensor pipe busy while this thread wakes up on
+        // sk_empty and issues the distance product of tile T + 2 into it (with
+        // the release after both products the pipe drained every tile)
+        const uint32_t oi = tmem + TOI(rowc & 1), sk = tmem + TSK(b);
+        const uint64_t vb = dv0 + (uint64_t)(vs * vt16);
+        const uint32_t fresh = it.first_in_row() ? 1u : 0u;
+#pragma unroll
+        for (int k = 0; k < BT / 16; ++k)   // O_I (+)= K1 . [V1 | V2]
+          mma16_ts(oi, sk + 16 * k, vb + (uint64_t)(k * kstep_v16), idesc_n32, !(fresh && k == 0));
+#pragma unroll
+        for (int k = 0; k < BT / 16; ++k)   // O_I[:, 0:16] += K2 . V1
+          mma16_ts(oi, sk + 16 * k + 8, vb + (uint64_t)(k * kstep_v16), idesc_n16, 1);
+        tc_commit(smem_u32(&vempty[vs]));
+        tc_commit(smem_u32(&sk_empty[b]));
+        if (it.last_in_row()) tc_commit(smem_u32(&oi_full[rowc & 1]));
         if (mir) {
           const uint32_t oj = tmem + TOJ(it.c);
           const uint64_t vib = dvi0 + (uint64_t)((rowc & 1) * vt16);
@@ -419,21 +434,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
             mma16_ss(oj, dks + (uint64_t)(ks2_16 + 16 * k), vib + (uint64_t)(k * kstep_v16), idesc_m16, 1);
           tc_commit(smem_u32(ks_empty));   // one phase per mirror tile: every phase has a waiter
         }
-        const uint32_t oi = tmem + TOI(rowc & 1), sk = tmem + TSK(b);
-        const uint64_t vb = dv0 + (uint64_t)(vs * vt16);
-        const uint32_t fresh = it.first_in_row() ? 1u : 0u;
-#pragma unroll
-        for (int k = 0; k < BT / 16; ++k)   // O_I (+)= K1 . [V1 | V2]
-          mma16_ts(oi, sk + 16 * k, vb + (uint64_t)(k * kstep_v16), idesc_n32, !(fresh && k == 0));
-#pragma unroll
-        for (int k = 0; k < BT / 16; ++k)   // O_I[:, 0:16] += K2 . V1
-          mma16_ts(oi, sk + 16 * k + 8, vb + (uint64_t)(k * kstep_v16), idesc_n16, 1);
-        tc_commit(smem_u32(&vempty[vs]));
-        tc_commit(smem_u32(&sk_empty[b]));
-        if (it.last_in_row()) {
-          tc_commit(smem_u32(&vi_empty[rowc & 1]));
-          tc_commit(smem_u32(&oi_full[rowc & 1]));
-        }
+        if (it.last_in_row()) tc_commit(smem_u32(&vi_empty[rowc & 1]));
         if (it.last_in_item()) tc_commit(smem_u32(oj_full));
       }
       __syncwarp();
