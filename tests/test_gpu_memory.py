@@ -2,7 +2,7 @@
 `test_largest_transient_buffer_is_one_block` / `test_tracemalloc_agrees_at_small_scale`,
 test_partition.py:132-158, restated for the device: no n x n buffer ever
 exists, peak device memory grows linearly in n; and compute-sanitizer
-memcheck / synccheck over every kernel family at small shapes)."""
+memcheck / synccheck / racecheck over every kernel family at small shapes)."""
 
 import os
 import shutil
@@ -60,7 +60,7 @@ def _sanitizer():
     pytest.skip("compute-sanitizer not found")
 
 
-@pytest.mark.parametrize("tool", ["memcheck", "synccheck"])
+@pytest.mark.parametrize("tool", ["memcheck", "synccheck", "racecheck"])
 def test_compute_sanitizer_clean(tool):
     cmd = [_sanitizer(), "--tool", tool, "--error-exitcode", "97", "--print-limit", "20",
            sys.executable, os.path.join(REPO, "scripts", "sanitize_small.py")]
@@ -68,4 +68,6 @@ def test_compute_sanitizer_clean(tool):
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert "sanitize workload ok" in out, out[-4000:]
-    assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
+    clean = "RACECHECK SUMMARY: 0 hazards displayed (0 errors, 0 warnings)" if tool == "racecheck" \
+        else "ERROR SUMMARY: 0 errors"
+    assert clean in out, out[-4000:]
