@@ -208,6 +208,152 @@ __global__ void __launch_bounds__(kRT) cg_precond_z(CgK s) {
   }, part + off_gam(t, k), sred);
 }
 
+// ---------------------------------------------------------------------------
+// Wide right-hand-side blocks (t >= kWideT: the 256-column variance solves).
+// The Woodbury terms are GEMM-shaped there (n x k by k x t, k x n by n x t)
+// and the one-output-per-thread forms above re-read L and C k times per
+// element; these register-tiled forms (64 x 64 output tile per block, 4 x 4
+// per thread, operands staged in SMEM, 16 DFMA per 4 LDS.128) keep the fp64
+// pipe busy instead. Grid (nb, ceil(t / 64)): blockIdx.x owns the same row
+// range as the narrow kernels (row_range), so partials stay per row block.
+// ---------------------------------------------------------------------------
+constexpr int kWideT = 32;
+constexpr int kWT = 64;        // output tile edge
+constexpr int kWLS = kWT + 4;  // padded SMEM row (keeps 16-byte alignment)
+
+// Z = (R - L C) / pc_noise on (active) columns, C = s.cbuf (k x t);
+// partial gam = sum R o Z (cg_precond_z semantics, k > 0 and pc_noise > 0)
+template <bool INIT>
+__global__ void __launch_bounds__(256) cg_precond_z_wide(CgK s) {
+  extern __shared__ __align__(16) double dsm[];
+  const int t = s.t, k = s.k;
+  const int c0 = blockIdx.y * kWT;
+  double* sC = dsm;                    // [k][kWT]
+  double* sL = sC + (size_t)k * kWT;   // [k][kWLS]: L^T of the current 64-row tile
+  double* sred = sL + (size_t)k * kWLS;  // [16][kWT]
+  for (int p = threadIdx.x; p < k * kWT; p += 256) {
+    const int kk = p / kWT, c = p - kk * kWT;
+    sC[p] = c0 + c < t ? s.cbuf[kk * t + c0 + c] : 0.0;
+  }
+  int64_t r0, r1;
+  row_range(s.n, r0, r1);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  bool live[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = c0 + 4 * tx + j;
+    live[j] = c < t && (INIT || s.active[c]);
+  }
+  double colacc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t rb = r0; rb < r1; rb += kWT) {
+    const int nr = (int)min((int64_t)kWT, r1 - rb);
+    __syncthreads();
+    for (int p = threadIdx.x; p < kWT * k; p += 256) {
+      const int r = p / k, kk = p - r * k;
+      sL[kk * kWLS + r] = r < nr ? s.L[(rb + r) * s.ldl + kk] : 0.0;
+    }
+    __syncthreads();
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int kk = 0; kk < k; ++kk) {
+      const double2 la = *reinterpret_cast<const double2*>(sL + kk * kWLS + 4 * ty);
+      const double2 lb = *reinterpret_cast<const double2*>(sL + kk * kWLS + 4 * ty + 2);
+      const double2 ca = *reinterpret_cast<const double2*>(sC + kk * kWT + 4 * tx);
+      const double2 cb = *reinterpret_cast<const double2*>(sC + kk * kWT + 4 * tx + 2);
+      const double l[4] = {la.x, la.y, lb.x, lb.y}, c[4] = {ca.x, ca.y, cb.x, cb.y};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(l[i], c[j], acc[i][j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int rl = 4 * ty + i;
+      if (rl >= nr) continue;
+      const int64_t r = rb + rl;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!live[j]) continue;
+        const int c = c0 + 4 * tx + j;
+        const double rv = s.R[r * s.ld + c];
+        const double z = (rv - acc[i][j]) / s.pc_noise;   // same kk order as cg_precond_z: same z
+        s.Z[r * s.ld + c] = z;
+        if (INIT) {
+          s.P[r * s.ld + c] = z;
+          s.P32[r * s.ld32 + c] = (float)z;
+        }
+        colacc[j] += rv * z;
+      }
+    }
+  }
+  // per-column partials: threads of equal tx summed in ty order (deterministic)
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) sred[ty * kWT + 4 * tx + j] = colacc[j];
+  __syncthreads();
+  if (threadIdx.x < kWT && c0 + (int)threadIdx.x < t) {
+    double v = 0.0;
+    for (int q = 0; q < 16; ++q) v += sred[q * kWT + threadIdx.x];
+    s.partials[(int64_t)blockIdx.x * (3 * t + k * t) + off_gam(t, k) + c0 + threadIdx.x] = v;
+  }
+}
+
+// partial L^T A over this block's rows into part[kk * t + c] (columns with
+// colmask[c] == 0 get 0): the block_ltmul product for wide t
+__global__ void __launch_bounds__(256) ltr_wide(int64_t n, int k, int t, const double* __restrict__ L,
+                                                int64_t ldl, const double* __restrict__ A, int64_t lda,
+                                                double* partials, int W, int slot, const int* colmask) {
+  __shared__ __align__(16) double sL[32 * kWLS];
+  __shared__ __align__(16) double sA[32 * kWLS];
+  int64_t r0, r1;
+  row_range(n, r0, r1);
+  const int c0 = blockIdx.y * kWT;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double* part = partials + (int64_t)blockIdx.x * W + slot;
+  for (int k0 = 0; k0 < k; k0 += kWT) {
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int64_t rb = r0; rb < r1; rb += 32) {
+      const int nr = (int)min((int64_t)32, r1 - rb);
+      __syncthreads();
+      for (int p = threadIdx.x; p < 32 * kWT; p += 256) {
+        const int r = p / kWT, q = p - r * kWT;
+        const bool in = r < nr;
+        sL[r * kWLS + q] = in && k0 + q < k ? L[(rb + r) * ldl + k0 + q] : 0.0;
+        sA[r * kWLS + q] = in && c0 + q < t ? A[(rb + r) * lda + c0 + q] : 0.0;
+      }
+      __syncthreads();
+      for (int r = 0; r < nr; ++r) {
+        const double2 la = *reinterpret_cast<const double2*>(sL + r * kWLS + 4 * ty);
+        const double2 lb = *reinterpret_cast<const double2*>(sL + r * kWLS + 4 * ty + 2);
+        const double2 aa = *reinterpret_cast<const double2*>(sA + r * kWLS + 4 * tx);
+        const double2 ab = *reinterpret_cast<const double2*>(sA + r * kWLS + 4 * tx + 2);
+        const double l[4] = {la.x, la.y, lb.x, lb.y}, a[4] = {aa.x, aa.y, ab.x, ab.y};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fma(l[i], a[j], acc[i][j]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int kk = k0 + 4 * ty + i;
+      if (kk >= k) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = c0 + 4 * tx + j;
+        if (c < t) part[kk * t + c] = (colmask && !colmask[c]) ? 0.0 : acc[i][j];
+      }
+    }
+  }
+}
+
 __global__ void cg_init_c(CgK s) {
   for (int c = threadIdx.x; c < s.t; c += blockDim.x) {
     s.gamma[c] = s.red[off_gam(s.t, s.k) + c];
@@ -260,7 +406,8 @@ __global__ void cg_alpha(CgK s, int it) {
 
 // U += alpha P; R -= alpha (Q + noise P); partial rn2; partial L^T R
 template <typename QT>
-__global__ void __launch_bounds__(kRT) cg_update(CgK s, const QT* __restrict__ Q, int64_t ldq, int it) {
+__global__ void __launch_bounds__(kRT) cg_update(CgK s, const QT* __restrict__ Q, int64_t ldq, int it,
+                                                 int with_ltr) {
   extern __shared__ double dsm[];
   double* sred = dsm;
   double* sal = sred + kRT;               // t
@@ -286,7 +433,7 @@ __global__ void __launch_bounds__(kRT) cg_update(CgK s, const QT* __restrict__ Q
     }
     return rv * rv;
   }, part + t, sred);
-  if (k > 0 && s.pc_noise > 0.0) {
+  if (with_ltr && k > 0 && s.pc_noise > 0.0) {
     __syncthreads();
     block_ltmul(r0, r1, k, t, s.L, s.ldl, s.R, s.ld, part + 2 * t, sL, sA, s.active);
   }
@@ -490,6 +637,13 @@ static int check_state(const gp_mbcg* s) {
 
 static size_t ltmul_smem(int k, int t) { return (size_t)(16 * std::max(k, 1) + 16 * t) * sizeof(double); }
 
+static size_t pz_wide_smem(int k) { return ((size_t)k * (kWT + kWLS) + 16 * kWT) * sizeof(double); }
+// the register-tiled Woodbury forms apply to wide blocks with a preconditioner
+// whose C tile and L^T tile fit in SMEM (k <= ~200)
+static bool use_wide(const gp_mbcg* s) {
+  return s->t >= kWideT && s->k > 0 && s->pc_noise > 0.0 && pz_wide_smem(s->k) <= 227 * 1024;
+}
+
 template <class K>
 static int set_smem(K kern, size_t bytes) {
   if (bytes > 48 * 1024)
@@ -534,6 +688,13 @@ int gp_mbcg_init_b(gp_mbcg* s, void* stream) {
   if (k > 0 && s->pc_noise > 0.0) {
     cg_cvec<<<1, 1024, 0, st>>>(v, 0);
     GP_LAUNCH_CHECK();
+  }
+  if (s->n > 0 && use_wide(s)) {
+    const size_t smem = pz_wide_smem(k);
+    if (int rc = set_smem(cg_precond_z_wide<true>, smem)) return rc;
+    cg_precond_z_wide<true><<<dim3(nb, (t + kWT - 1) / kWT), 256, smem, st>>>(v);
+    GP_LAUNCH_CHECK();
+    return finalize(s->partials, nb, W, off_gam(t, k), off_gam(t, k) + t, s->red, st);
   }
   if (s->n > 0) {
     size_t smem = (kRT + (size_t)k * t) * sizeof(double);
@@ -580,14 +741,20 @@ int gp_mbcg_update(gp_mbcg* s, const void* Q, int64_t ldq, int q_is_f64, int ite
   GP_LAUNCH_CHECK();
   if (s->n > 0) {
     size_t smem = (kRT + t) * sizeof(double) + ltmul_smem(k, t);
+    const int in_kernel_ltr = use_wide(s) ? 0 : 1;
     if (q_is_f64) {
       if (int rc = set_smem(cg_update<double>, smem)) return rc;
-      cg_update<double><<<nb, kRT, smem, st>>>(v, static_cast<const double*>(Q), ldq, iteration);
+      cg_update<double><<<nb, kRT, smem, st>>>(v, static_cast<const double*>(Q), ldq, iteration, in_kernel_ltr);
     } else {
       if (int rc = set_smem(cg_update<float>, smem)) return rc;
-      cg_update<float><<<nb, kRT, smem, st>>>(v, static_cast<const float*>(Q), ldq, iteration);
+      cg_update<float><<<nb, kRT, smem, st>>>(v, static_cast<const float*>(Q), ldq, iteration, in_kernel_ltr);
     }
     GP_LAUNCH_CHECK();
+    if (!in_kernel_ltr) {
+      ltr_wide<<<dim3(nb, (t + kWT - 1) / kWT), 256, 0, st>>>(s->n, k, t, s->L, s->ldl, s->R, s->ld, s->partials, W,
+                                                             off_ltr(t), s->active);
+      GP_LAUNCH_CHECK();
+    }
     int s1 = (k > 0 && s->pc_noise > 0.0) ? off_ltr(t) + k * t : off_ltr(t);
     return finalize(s->partials, nb, W, off_rn2(t), s1, s->red, st);
   }
@@ -605,6 +772,13 @@ int gp_mbcg_precond(gp_mbcg* s, int iteration, double tolerance, void* stream) {
   if (k > 0 && s->pc_noise > 0.0) {
     cg_cvec<<<1, 1024, 0, st>>>(v, 1);
     GP_LAUNCH_CHECK();
+  }
+  if (s->n > 0 && use_wide(s)) {
+    const size_t smem = pz_wide_smem(k);
+    if (int rc = set_smem(cg_precond_z_wide<false>, smem)) return rc;
+    cg_precond_z_wide<false><<<dim3(nb, (t + kWT - 1) / kWT), 256, smem, st>>>(v);
+    GP_LAUNCH_CHECK();
+    return finalize(s->partials, nb, W, off_gam(t, k), off_gam(t, k) + t, s->red, st);
   }
   if (s->n > 0) {
     size_t smem = (kRT + (size_t)k * t) * sizeof(double);
