@@ -159,11 +159,11 @@ __global__ void __launch_bounds__(kRT) cg_init_a(CgK s, const double* __restrict
   }
 }
 
-// c = B^{-1} (L^T R) for the given columns; single block
+// c = B^{-1} (L^T R) for the given columns (one output per thread, k-long dots)
 __global__ void cg_cvec(CgK s, int use_active) {
   const int t = s.t, k = s.k;
   const double* ltr = s.red + off_ltr(t);
-  for (int p = threadIdx.x; p < k * t; p += blockDim.x) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < k * t; p += gridDim.x * blockDim.x) {
     int kk = p / t, c = p - kk * t;
     double acc = 0.0;
     if (!use_active || s.active[c])
@@ -686,7 +686,7 @@ int gp_mbcg_init_b(gp_mbcg* s, void* stream) {
   cg_bnorm<<<1, 256, 0, st>>>(v);
   GP_LAUNCH_CHECK();
   if (k > 0 && s->pc_noise > 0.0) {
-    cg_cvec<<<1, 1024, 0, st>>>(v, 0);
+    cg_cvec<<<(k * t + 255) / 256, 256, 0, st>>>(v, 0);
     GP_LAUNCH_CHECK();
   }
   if (s->n > 0 && use_wide(s)) {
@@ -770,7 +770,7 @@ int gp_mbcg_precond(gp_mbcg* s, int iteration, double tolerance, void* stream) {
   cg_freeze<<<1, 256, 0, st>>>(v, iteration, tolerance);
   GP_LAUNCH_CHECK();
   if (k > 0 && s->pc_noise > 0.0) {
-    cg_cvec<<<1, 1024, 0, st>>>(v, 1);
+    cg_cvec<<<(k * t + 255) / 256, 256, 0, st>>>(v, 1);
     GP_LAUNCH_CHECK();
   }
   if (s->n > 0 && use_wide(s)) {

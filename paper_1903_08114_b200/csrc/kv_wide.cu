@@ -40,7 +40,7 @@ struct Args {
   int DK, NW;             // NW = t rounded up to 16
   int64_t n_rows, n_cols;
   int row_tiles, col_tiles, splits, tiles_per_split;
-  int nstages;
+  int nsc, nsv;           // column-image ring and V ring depths
   int t;
   float s2, noise;
   int64_t diag_offset, self_offset;
@@ -79,14 +79,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
   const uint32_t row_bytes = 2u * BM * DK * 4u;
   const uint32_t col_bytes = 2u * BN * DK * 4u;
   const uint32_t v_bytes = 2u * NW * BN * 2u;
-  const uint32_t stage_bytes = col_bytes + v_bytes;
-  const int NS = a.nstages;
+  const int NSC = a.nsc, NSV = a.nsv;
   uint8_t* xr_s = smem;
-  uint8_t* stages = smem + row_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + NS * stage_bytes);
-  uint64_t* full = bars;             // [NS]
-  uint64_t* empty = bars + NS;       // [NS]
-  uint64_t* s_full = bars + 2 * NS;  // [2]
+  uint8_t* cring = smem + row_bytes;           // [NSC] column images (distance B operand)
+  uint8_t* vring = cring + NSC * col_bytes;    // [NSV] V images (contraction B operand)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(vring + NSV * v_bytes);
+  // separate rings: the small column images run far ahead of the 64 KB V
+  // tiles, so the distance product of the next tile never waits on a V load
+  uint64_t* cfull = bars;                 // [NSC]
+  uint64_t* cempty = cfull + NSC;         // [NSC]
+  uint64_t* vfull = cempty + NSC;         // [NSV]
+  uint64_t* vempty = vfull + NSV;         // [NSV]
+  uint64_t* s_full = vempty + NSV;        // [2]
   uint64_t* k_full = s_full + 2;     // [2]
   uint64_t* k_empty = k_full + 2;    // [2]
   uint64_t* o_full = k_empty + 2;    // chunk accumulated
@@ -94,13 +98,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
   uint64_t* xr_full = o_empty + 1;
   uint64_t* xr_empty = xr_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xr_empty + 1);
-  float* fold_s = reinterpret_cast<float*>(smem + row_bytes + NS * stage_bytes + 256);   // [8 warps][2][32 x 16]
+  float* fold_s = reinterpret_cast<float*>(vring + NSV * v_bytes + 512);   // [8 warps][2][32 x 16]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), 1);
+    for (int s = 0; s < NSC; ++s) {
+      mbar_init(smem_u32(&cfull[s]), 1);
+      mbar_init(smem_u32(&cempty[s]), 1);
+    }
+    for (int s = 0; s < NSV; ++s) {
+      mbar_init(smem_u32(&vfull[s]), 1);
+      mbar_init(smem_u32(&vempty[s]), 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&s_full[b]), 1);
@@ -124,7 +132,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
   const int n_items = a.row_tiles * a.splits;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer: row and column images =====================
     if (lane == 0) {
       uint32_t s = 0, ph = 0, itc = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++itc) {
@@ -135,16 +143,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
         mbar_expect_tx(smem_u32(xr_full), row_bytes);
         bulk_g2s(smem_u32(xr_s), a.row_img + (int64_t)rt * (row_bytes / 4), row_bytes, smem_u32(xr_full));
         const float* cimg = a.col_img + (int64_t)ct0 * (col_bytes / 4);
+        for (int ct = ct0; ct < ct1; ++ct) {
+          mbar_wait(smem_u32(&cempty[s]), ph ^ 1);
+          mbar_expect_tx(smem_u32(&cfull[s]), col_bytes);
+          bulk_g2s(smem_u32(cring + s * col_bytes), cimg, col_bytes, smem_u32(&cfull[s]));
+          cimg += col_bytes / 4;
+          if (++s == (uint32_t)NSC) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 3) {
+    // ===================== TMA producer: V tiles =====================
+    if (lane == 0) {
+      uint32_t s = 0, ph = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int sp = it % a.splits;
+        const int ct0 = sp * a.tiles_per_split;
+        const int ct1 = min(a.col_tiles, ct0 + a.tiles_per_split);
         const uint8_t* vimg = reinterpret_cast<const uint8_t*>(a.v_img) + (int64_t)ct0 * v_bytes;
         for (int ct = ct0; ct < ct1; ++ct) {
-          mbar_wait(smem_u32(&empty[s]), ph ^ 1);
-          uint8_t* st = stages + s * stage_bytes;
-          mbar_expect_tx(smem_u32(&full[s]), stage_bytes);
-          bulk_g2s(smem_u32(st), cimg, col_bytes, smem_u32(&full[s]));
-          bulk_g2s(smem_u32(st + col_bytes), vimg, v_bytes, smem_u32(&full[s]));
-          cimg += col_bytes / 4;
+          mbar_wait(smem_u32(&vempty[s]), ph ^ 1);
+          mbar_expect_tx(smem_u32(&vfull[s]), v_bytes);
+          bulk_g2s(smem_u32(vring + s * v_bytes), vimg, v_bytes, smem_u32(&vfull[s]));
           vimg += v_bytes;
-          if (++s == (uint32_t)NS) { s = 0; ph ^= 1; }
+          if (++s == (uint32_t)NSV) { s = 0; ph ^= 1; }
         }
       }
     }
@@ -157,12 +179,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
     const uint32_t v2_16 = ((NW / 8) * 128) >> 4;   // V2 rows start NW/8 core rows down
     const int ksteps = DK / 8;
     const uint64_t da0 = make_desc(smem_u32(xr_s), lbo_a, 128);
-    const uint64_t db0 = make_desc(smem_u32(stages), lbo_b, 128);
-    const uint64_t dv0 = make_desc(smem_u32(stages + col_bytes), lbo_v, 128);
-    const uint32_t stage16 = stage_bytes >> 4;
+    const uint64_t db0 = make_desc(smem_u32(cring), lbo_b, 128);
+    const uint64_t dv0 = make_desc(smem_u32(vring), lbo_v, 128);
+    const uint32_t col16 = col_bytes >> 4, v16 = v_bytes >> 4;
     const uint32_t kstep_a16 = (2 * lbo_a) >> 4, kstep_b16 = (2 * lbo_b) >> 4, kstep_v16 = (2 * lbo_v) >> 4;
     const bool leader = elect_one();
-    uint32_t ds = 0, dph = 0, cs = 0, sbn = 0, kb = 0, kph = 0, oph = 0;
+    uint32_t ds = 0, dph = 0, vs = 0, vph = 0, sbn = 0, kb = 0, kph = 0, oph = 0;
     uint32_t itc = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++itc) {
       const int sp = it % a.splits;
@@ -172,10 +194,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
       mbar_wait(smem_u32(xr_full), itc & 1);
       tc_fence_after();
       auto dist = [&]() {
-        mbar_wait(smem_u32(&full[ds]), dph);
+        mbar_wait(smem_u32(&cfull[ds]), dph);
         tc_fence_after();
         const uint32_t d_tm = tmem + TMS(sbn);
-        const uint64_t db = db0 + (uint64_t)(ds * stage16);
+        const uint64_t db = db0 + (uint64_t)(ds * col16);
         if (leader) {
 #pragma unroll
           for (int pass = 0; pass < 3; ++pass) {
@@ -186,9 +208,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
                      (pass | ks) != 0);
           }
           tc_commit(smem_u32(&s_full[sbn]));
+          tc_commit(smem_u32(&cempty[ds]));
         }
         __syncwarp();
-        if (++ds == (uint32_t)NS) { ds = 0; dph ^= 1; }
+        if (++ds == (uint32_t)NSC) { ds = 0; dph ^= 1; }
         sbn ^= 1;
       };
       dist();
@@ -201,7 +224,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
           mbar_wait(smem_u32(o_empty), oph ^ 1);
           tc_fence_after();
         }
-        const uint64_t vb = dv0 + (uint64_t)(cs * stage16);
+        mbar_wait(smem_u32(&vfull[vs]), vph);
+        tc_fence_after();
+        const uint64_t vb = dv0 + (uint64_t)(vs * v16);
         const uint32_t k1 = tmem + TMK1(kb), k2 = tmem + TMK2(kb);
         if (leader) {
           // O += K1.V1 + K1.V2 + K2.V1  (K = 64 = 4 x 16, N = NW)
@@ -214,13 +239,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
 #pragma unroll
           for (int ks = 0; ks < BN / 16; ++ks)
             mma16_ts(tmem + TMO, k2 + ks * 8, vb + (uint64_t)(ks * kstep_v16), idesc_c, 1);
-          tc_commit(smem_u32(&empty[cs]));
+          tc_commit(smem_u32(&vempty[vs]));
           tc_commit(smem_u32(&k_empty[kb]));
           if ((jj % CH) == CH - 1 || jj == J - 1) tc_commit(smem_u32(o_full));
         }
         __syncwarp();
         if ((jj % CH) == CH - 1 || jj == J - 1) oph ^= 1;
-        if (++cs == (uint32_t)NS) cs = 0;
+        if (++vs == (uint32_t)NSV) { vs = 0; vph ^= 1; }
         if (++kb == 2) { kb = 0; kph ^= 1; }
       }
       if (leader) tc_commit(smem_u32(xr_empty));
@@ -345,7 +370,7 @@ __global__ void kv_wide_finalize(const float* __restrict__ accw, int splits, int
 }
 
 struct Plan {
-  int DK, NW, row_tiles, col_tiles, splits, tiles_per_split, nstages;
+  int DK, NW, row_tiles, col_tiles, splits, tiles_per_split, nsc, nsv;
   int64_t rows_pad;
   size_t row_img_bytes, col_img_bytes, v_img_bytes, split_bytes, smem;
 };
@@ -370,11 +395,14 @@ static Plan make_plan(const gp_kv_desc* d, int t) {
   p.v_img_bytes = (size_t)p.col_tiles * 2 * p.NW * BN * 2;
   p.rows_pad = (int64_t)p.row_tiles * BM;
   p.split_bytes = (size_t)p.splits * p.NW * p.rows_pad * 4 + 256 * sizeof(double) + 2 * TMAX * sizeof(float);
-  const size_t row_b = 2u * BM * p.DK * 4, stage_b = 2u * BN * p.DK * 4 + 2u * p.NW * BN * 2;
+  const size_t row_b = 2u * BM * p.DK * 4, col_b = 2u * BN * p.DK * 4, v_b = 2u * p.NW * BN * 2;
   const size_t fold_b = NUM_EPI_WARPS * 2 * STAGE_FOLD_BYTES;
-  const size_t budget = 224 * 1024 - row_b - 256 - fold_b;
-  p.nstages = (int)std::min<size_t>(4, budget / stage_b);
-  p.smem = row_b + p.nstages * stage_b + 256 + fold_b;
+  const size_t budget = 224 * 1024 - row_b - 512 - fold_b;
+  // V ring as deep as fits next to a 2-deep column ring (at most 4), then the
+  // column ring takes the rest (at most 8)
+  p.nsv = (int)std::min<size_t>(4, budget >= 2 * col_b ? (budget - 2 * col_b) / v_b : 0);
+  p.nsc = p.nsv >= 2 ? (int)std::min<size_t>(8, (budget - p.nsv * v_b) / col_b) : 0;
+  p.smem = row_b + p.nsc * col_b + p.nsv * v_b + 512 + fold_b;
   return p;
 }
 
@@ -385,7 +413,8 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 bool kv_wide_supported(const gp_kv_desc* d, int t) {
   if (t <= 16 || t > tw::TMAX) return false;
   if (d->d < 1 || d->d + 2 > 32) return false;
-  return tw::make_plan(d, t).nstages >= 2;
+  const tw::Plan p = tw::make_plan(d, t);
+  return p.nsv >= 2 && p.nsc >= 2;
 }
 
 size_t kv_wide_workspace(const gp_kv_desc* d, int t) {
@@ -421,7 +450,7 @@ int kv_wide(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* o
   a.DK = p.DK; a.NW = p.NW;
   a.n_rows = desc->n_rows; a.n_cols = desc->n_cols;
   a.row_tiles = p.row_tiles; a.col_tiles = p.col_tiles; a.splits = p.splits;
-  a.tiles_per_split = p.tiles_per_split; a.nstages = p.nstages; a.t = t;
+  a.tiles_per_split = p.tiles_per_split; a.nsc = p.nsc; a.nsv = p.nsv; a.t = t;
   a.s2 = (float)desc->outputscale; a.noise = (float)desc->noise; a.diag_offset = desc->diag_offset;
   a.self_offset = desc->self_offset;
   a.accw = accw; a.rows_pad = p.rows_pad;
