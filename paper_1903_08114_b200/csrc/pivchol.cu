@@ -59,32 +59,60 @@ __global__ void pivchol_init(PivArgs a) {
 }
 
 // choose pivot j from the block partials and stage its data
+// argmax of the per-block partials (largest residual, lowest index on ties:
+// an associative choice, so the tree order cannot change the pivot), then the
+// pivot's point and L row into pinfo for the step kernel
 __global__ void pivchol_select(PivArgs a, int j) {
   if (*a.stop) return;
-  __shared__ double sv[1024];
-  __shared__ int64_t si[1024];
+  __shared__ double sv[32];
+  __shared__ int64_t si[32];
+  __shared__ int64_t s_piv;
+  __shared__ int s_stop;
   double bv = -INFINITY; int64_t bi = INT64_MAX;
   for (int b = threadIdx.x; b < a.nb; b += blockDim.x) better(bv, bi, a.pval[b], a.pidx[b]);
-  sv[threadIdx.x] = bv; si[threadIdx.x] = bi;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    better(bv, bi, ov, oi);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) { sv[w] = bv; si[w] = bi; }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int q = 1; q < (int)blockDim.x; ++q) better(bv, bi, sv[q], si[q]);
-    sv[0] = bv; si[0] = bi;
-    if (!(bv > 0.0)) {  // residual mass exhausted: stop at rank j
-      *a.stop = 1;
-      a.info[0] = j;
-    } else {
-      a.piv[j] = bi;
-      a.pinfo[0] = bv;
+  if (w == 0) {
+    const int nw = (int)(blockDim.x >> 5);
+    bv = lane < nw ? sv[lane] : -INFINITY;
+    bi = lane < nw ? si[lane] : INT64_MAX;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      better(bv, bi, ov, oi);
+    }
+    if (lane == 0) {
+      if (!(bv > 0.0)) {  // residual mass exhausted: stop at rank j
+        *a.stop = 1;
+        a.info[0] = j;
+        s_stop = 1;
+      } else {
+        a.piv[j] = bi;
+        a.pinfo[0] = bv;
+        s_stop = 0;
+      }
+      s_piv = bi;
     }
   }
   __syncthreads();
-  if (*a.stop) return;
-  int64_t p = si[0];
+  if (s_stop) return;
+  const int64_t p = s_piv;
   for (int q = threadIdx.x; q < a.d; q += blockDim.x) a.pinfo[1 + q] = a.X[p * a.ldx + q];
   for (int m = threadIdx.x; m < j; m += blockDim.x) a.pinfo[1 + a.d + m] = a.L[p * a.ldl + m];
 }
 
+// one step of the greedy factorisation over this block's rows. L is n x k
+// row-major, so a thread per row would read its row with a 8*ldl-byte stride
+// across the warp; instead 8 lanes share a row (coalesced 64-byte reads of
+// L[i, :j] and X[i, :]) and combine their partial sums with shuffles.
 __global__ void pivchol_step(PivArgs a, int j) {
   if (*a.stop) return;
   extern __shared__ double sp[];  // pinfo copy: 1 + d + j
@@ -96,25 +124,36 @@ __global__ void pivchol_step(PivArgs a, int j) {
   const int64_t pj = a.piv[j];
   int64_t per = (a.n + gridDim.x - 1) / gridDim.x;
   int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(a.n, r0 + per);
+  const int g = threadIdx.x & 7, grp = threadIdx.x >> 3, ngrp = blockDim.x >> 3;
   double bv = -INFINITY; int64_t bi = INT64_MAX;
-  for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-    const double* xi = a.X + i * a.ldx;
-    double r2 = 0.0;
-    for (int q = 0; q < a.d; ++q) {
-      double df = xi[q] - xp[q];
-      r2 = fma(df, df, r2);
+  for (int64_t i0 = r0; i0 < r1; i0 += ngrp) {   // warp-uniform trip count (shuffles below)
+    const int64_t i = i0 + grp;
+    const bool in = i < r1;
+    double r2 = 0.0, dot = 0.0;
+    if (in) {
+      const double* xi = a.X + i * a.ldx;
+      for (int q = g; q < a.d; q += 8) {
+        double df = xi[q] - xp[q];
+        r2 = fma(df, df, r2);
+      }
+      const double* li = a.L + i * a.ldl;
+      for (int m = g; m < j; m += 8) dot = fma(li[m], lp[m], dot);
     }
-    double row = a.s2 * kappa_f64(a.fam, r2);
-    double* li = a.L + i * a.ldl;
-    double dot = 0.0;
-    for (int m = 0; m < j; ++m) dot = fma(li[m], lp[m], dot);
-    double col = (row - dot) * inv_sq;
-    li[j] = col;
-    double di = a.dres[i] - col * col;
-    di = di > 0.0 ? di : 0.0;
-    if (i == pj) di = 0.0;
-    a.dres[i] = di;
-    better(bv, bi, di, i);
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+      dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    }
+    if (in && g == 0) {
+      double row = a.s2 * kappa_f64(a.fam, r2);
+      double col = (row - dot) * inv_sq;
+      a.L[i * a.ldl + j] = col;
+      double di = a.dres[i] - col * col;
+      di = di > 0.0 ? di : 0.0;
+      if (i == pj) di = 0.0;
+      a.dres[i] = di;
+      better(bv, bi, di, i);
+    }
   }
   block_argmax_store(bv, bi, a.pval, a.pidx);
 }
@@ -123,8 +162,11 @@ __global__ void pivchol_finish(PivArgs a) {
   if (!*a.stop) a.info[0] = a.k;
 }
 
+// row blocks of >= 64 rows (two passes of the 32 row groups of a block), at
+// most 1024 of them (the select kernel's single block reduces their partials):
+// small n spreads over many SMs instead of a few long blocks
 static int piv_nb(int64_t n) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>(2 * num_sms(), (n + 255) / 256));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(1024, (n + 63) / 64));
 }
 
 }  // namespace gp
