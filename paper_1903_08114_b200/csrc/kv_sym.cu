@@ -195,10 +195,12 @@ struct TileSeq {
   __device__ int J() const { return RB * Q + c; }
 };
 
-template <int FAM>
+// DKT: the augmented-point width (8 or 16) as a compile-time constant, so the
+// MMA thread's distance products and row-image copies unroll fully
+template <int FAM, int DKT>
 __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int DK = a.DK;
+  constexpr int DK = DKT;
   const uint32_t img_bytes = 2u * BT * DK * 4u;       // row or column image of one tile (hi | lo)
   const int NSC = a.nsc, NSV = a.nsv;
   uint8_t* ks = smem;                                  // K1 | K2 of the current tile (mirror A operand)
@@ -327,7 +329,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
     const uint32_t idesc_m16 = idesc_f16(BT, TN) | IDESC_A_MN_MAJOR;
     const uint32_t lbo_b = (BT / 8) * 128, lbo_v = (2 * TN / 8) * 128;
     const uint32_t half16 = (BT * DK * 4) >> 4;
-    const int ksteps = DK / 8;
+    constexpr int ksteps = DK / 8;
     const uint64_t dc0 = make_desc(smem_u32(cring), lbo_b, 128);
     const uint64_t dv0 = make_desc(smem_u32(vring), lbo_v, 128);
     const uint64_t dvi0 = make_desc(smem_u32(vi_s), lbo_v, 128);
@@ -353,6 +355,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
         tc_fence_after();
         if (leader) {
           for (int part = 0; part < 2; ++part)
+#pragma unroll
             for (int kb = 0; kb < ksteps; ++kb)
               tmem_cp_128x256b(tmem + TXA(R & 1) + part * DK + 8 * kb,
                                dxr0 + (uint64_t)((part * BT * DK * 4 + kb * 2 * lbo_b) >> 4));
@@ -371,6 +374,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
         for (int pass = 0; pass < 3; ++pass) {
           const uint32_t a_t = tmem + TXA(xb) + (pass == 0 ? (uint32_t)DK : 0u);
           const uint64_t b_p = db + (pass == 1 ? half16 : 0u);
+#pragma unroll
           for (int k = 0; k < ksteps; ++k)
             mma_ts(d_tm, a_t + k * 8, b_p + (uint64_t)(k * kstep_b16), idesc_d, (pass | k) != 0);
         }
@@ -801,7 +805,9 @@ int kv_sym_partial(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, i
   const int my_chunks = (chunks - part + nparts - 1) / nparts;
   if (my_chunks < 1) return GP_OK;
   int grid = std::min(my_chunks, num_sms());
-  auto kern = desc->family == GP_FAMILY_RBF ? kv_sym_kernel<GP_FAMILY_RBF> : kv_sym_kernel<GP_FAMILY_MATERN32>;
+  auto kern = desc->family == GP_FAMILY_RBF
+                  ? (p.DK == 8 ? kv_sym_kernel<GP_FAMILY_RBF, 8> : kv_sym_kernel<GP_FAMILY_RBF, 16>)
+                  : (p.DK == 8 ? kv_sym_kernel<GP_FAMILY_MATERN32, 8> : kv_sym_kernel<GP_FAMILY_MATERN32, 16>);
   GP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   const char* pe = getenv("GP_SYM_PROF");
   if (GP_SYM_PROF_BUILD && pe && *pe == '1') GP_CUDA_TRY(cudaMalloc(&a.prof, (size_t)grid * (NTHREADS / 32) * 8 * sizeof(long long)));
