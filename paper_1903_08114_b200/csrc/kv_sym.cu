@@ -42,6 +42,7 @@
 // the sigma^2 diagonal), partition.py:224-241 (row-block products).
 #include "tc_common.cuh"
 
+#include <cooperative_groups.h>
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -641,37 +642,62 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
 // per column: E_c with 2^E_c ||V_c||_1 <= 2^61 (no fixed-point overflow: kappa
 // <= 1), s_c with 2^s_c max|V_c| <= 2^14 (fp16 range); partial sums arrive in
 // units of 2^s_c, so they are converted with exponent E_c - s_c
-__global__ void sym_scale_kernel(const float* __restrict__ V, int64_t ldv, int64_t n, int t, int* expo,
-                                 float* vscale, double* inv_scale) {
-  __shared__ double red[256];
-  __shared__ float mx[256];
-  const int c = blockIdx.x;
+// the per-column sums run on an 8-CTA cluster (rows split across the CTAs,
+// partials combined by CTA 0 over distributed shared memory in rank order:
+// deterministic, no workspace; one CTA per column took ~0.5 ms at n = 10^6)
+constexpr int kScaleCtas = 8;
+__global__ void __cluster_dims__(kScaleCtas, 1, 1) __launch_bounds__(1024)
+    sym_scale_kernel(const float* __restrict__ V, int64_t ldv, int64_t n, int t, int* expo, float* vscale,
+                     double* inv_scale) {
+  namespace cgr = cooperative_groups;
+  cgr::cluster_group cl = cgr::this_cluster();
+  __shared__ double red[1024];
+  __shared__ float mxr[1024];
+  __shared__ double psum[TN];
+  __shared__ float pmax[TN];
+  const int rank = (int)cl.block_rank(), nb = (int)cl.num_blocks();
+  const int64_t per = (n + nb - 1) / nb;
+  const int64_t r0 = min(n, (int64_t)rank * per), r1 = min(n, r0 + per);
+  const int tw = max(t, 1), rpp = (int)blockDim.x / tw;
+  const int tr = (int)threadIdx.x / tw, tc = (int)threadIdx.x - tr * tw;
   double s = 0.0;
   float m = 0.f;
-  if (c < t)
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-      const float x = fabsf(V[i * ldv + c]);
+  if (tr < rpp && tc < t)
+#pragma unroll 8  // loads of later rows issue ahead of the dependent adds
+    for (int64_t i = r0 + tr; i < r1; i += rpp) {
+      const float x = fabsf(V[i * ldv + tc]);
       s += (double)x;
       m = fmaxf(m, x);
     }
   red[threadIdx.x] = s;
-  mx[threadIdx.x] = m;
+  mxr[threadIdx.x] = m;
   __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) {
-      red[threadIdx.x] += red[threadIdx.x + o];
-      mx[threadIdx.x] = fmaxf(mx[threadIdx.x], mx[threadIdx.x + o]);
+  if ((int)threadIdx.x < t) {
+    double ss = 0.0;
+    float mm = 0.f;
+    for (int q = 0; q < rpp; ++q) {
+      ss += red[q * tw + threadIdx.x];
+      mm = fmaxf(mm, mxr[q * tw + threadIdx.x]);
     }
-    __syncthreads();
+    psum[threadIdx.x] = ss;
+    pmax[threadIdx.x] = mm;
   }
-  if (threadIdx.x == 0) {
+  cl.sync();
+  if (rank == 0 && (int)threadIdx.x < TN) {
+    const int c = threadIdx.x;
+    double l1 = 0.0;
+    float mx = 0.f;
+    if (c < t)
+      for (int b = 0; b < nb; ++b) {
+        l1 += *cl.map_shared_rank(&psum[c], b);
+        mx = fmaxf(mx, *cl.map_shared_rank(&pmax[c], b));
+      }
     int E = 61, S = 0;
-    const double l1 = red[0];
     if (l1 > 0.0 && l1 < INFINITY) {
       int ex;
       frexp(l1, &ex);  // l1 < 2^ex
       E = 61 - ex;
-      frexp((double)mx[0], &ex);
+      frexp((double)mx, &ex);
       S = 14 - ex;
     }
     E = max(-100, min(100, E));
@@ -680,6 +706,7 @@ __global__ void sym_scale_kernel(const float* __restrict__ V, int64_t ldv, int64
     vscale[c] = ldexpf(1.0f, S);
     inv_scale[c] = ldexp(1.0, -E);
   }
+  cl.sync();
 }
 
 // out[i, c] = s2 * acc[c][i] 2^-E_c (+ noise V[i + diag_offset, c]); NaN where a
@@ -788,7 +815,7 @@ int kv_sym_partial(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, i
   const double c = desc->family == GP_FAMILY_RBF ? 1.4426950408889634 : -6.0;
   GP_CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)t * p.acc_ld * 8, st));
   GP_CUDA_TRY(cudaMemsetAsync(bad, 0, p.bad_bytes, st));
-  sym_scale_kernel<<<TN, 256, 0, st>>>(V, ldv, n, t, w.expo, w.vscale, w.inv_scale);
+  sym_scale_kernel<<<kScaleCtas, 1024, 0, st>>>(V, ldv, n, t, w.expo, w.vscale, w.inv_scale);
   GP_LAUNCH_CHECK();
   if (int rc = tc::distance_images(desc->Xr, desc->ldr, n, desc->Xc, desc->ldc, n, desc->d, p.DK, BT, BT, c,
                                    w.mean, w.row_img, w.col_img, st))
@@ -844,7 +871,7 @@ int kv_sym_finalize(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, 
   GP_REQUIRE(ws != nullptr && ws_bytes >= need, "gp_kv(symmetric): workspace of %zu bytes required, %zu given",
              need, ws_bytes);
   WsView w = carve(p, ws);
-  sym_scale_kernel<<<TN, 256, 0, st>>>(V, ldv, desc->n_rows, t, w.expo, w.vscale, w.inv_scale);
+  sym_scale_kernel<<<kScaleCtas, 1024, 0, st>>>(V, ldv, desc->n_rows, t, w.expo, w.vscale, w.inv_scale);
   GP_LAUNCH_CHECK();
   const int64_t tot = (row1 - row0) * t;
   if (tot == 0) return GP_OK;
