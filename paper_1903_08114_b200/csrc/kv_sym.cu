@@ -857,11 +857,13 @@ int kv_sym_partial(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, i
   return GP_OK;
 }
 
+namespace tcs {
 // rows [row0, row1) of s2 * K V (+ noise V) from the (summed) fixed-point
 // accumulator; the scales are recomputed from V (the same V as the partials)
-int kv_sym_finalize(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, const long long* acc,
-                    const int* bad, int64_t row0, int64_t row1, float* out, int64_t ldo, void* ws, size_t ws_bytes,
-                    cudaStream_t st) {
+// unless this workspace already holds them (the single-device product)
+static int finalize_rows(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, const long long* acc,
+                         const int* bad, int64_t row0, int64_t row1, float* out, int64_t ldo, void* ws,
+                         size_t ws_bytes, cudaStream_t st, bool scales_ready) {
   using namespace tcs;
   GP_REQUIRE(kv_sym_supported(desc, t), "gp_kv_sym: shape unsupported by the symmetric kernel");
   GP_REQUIRE(0 <= row0 && row0 <= row1 && row1 <= desc->n_rows, "gp_kv_sym_finalize: rows [%lld, %lld)",
@@ -871,8 +873,10 @@ int kv_sym_finalize(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, 
   GP_REQUIRE(ws != nullptr && ws_bytes >= need, "gp_kv(symmetric): workspace of %zu bytes required, %zu given",
              need, ws_bytes);
   WsView w = carve(p, ws);
-  sym_scale_kernel<<<kScaleCtas, 1024, 0, st>>>(V, ldv, desc->n_rows, t, w.expo, w.vscale, w.inv_scale);
-  GP_LAUNCH_CHECK();
+  if (!scales_ready) {
+    sym_scale_kernel<<<kScaleCtas, 1024, 0, st>>>(V, ldv, desc->n_rows, t, w.expo, w.vscale, w.inv_scale);
+    GP_LAUNCH_CHECK();
+  }
   const int64_t tot = (row1 - row0) * t;
   if (tot == 0) return GP_OK;
   sym_finalize_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(acc, p.acc_ld, bad, w.inv_scale, row0, row1, t,
@@ -880,6 +884,13 @@ int kv_sym_finalize(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, 
                                                                      ldv, desc->diag_offset);
   GP_LAUNCH_CHECK();
   return GP_OK;
+}
+}  // namespace tcs
+
+int kv_sym_finalize(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, const long long* acc,
+                    const int* bad, int64_t row0, int64_t row1, float* out, int64_t ldo, void* ws, size_t ws_bytes,
+                    cudaStream_t st) {
+  return tcs::finalize_rows(desc, V, ldv, t, acc, bad, row0, row1, out, ldo, ws, ws_bytes, st, false);
 }
 
 int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out, int64_t ldo, void* ws,
@@ -889,7 +900,8 @@ int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* ou
              "gp_kv(symmetric): workspace of %zu bytes required, %zu given", kv_sym_workspace(desc, t), ws_bytes);
   WsView w = carve(make_plan(desc), ws);
   if (int rc = kv_sym_partial(desc, V, ldv, t, 0, 1, w.acc, w.bad, ws, ws_bytes, st)) return rc;
-  return kv_sym_finalize(desc, V, ldv, t, w.acc, w.bad, 0, desc->n_rows, out, ldo, ws, ws_bytes, st);
+  // kv_sym_partial left this V's scales in the workspace
+  return finalize_rows(desc, V, ldv, t, w.acc, w.bad, 0, desc->n_rows, out, ldo, ws, ws_bytes, st, true);
 }
 
 }  // namespace gp
