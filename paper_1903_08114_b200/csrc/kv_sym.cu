@@ -65,12 +65,19 @@ constexpr uint32_t KS_HALF = BT * BT * 2;            // K1 (or K2) of one tile, 
 constexpr uint32_t KS_BYTES = 2 * KS_HALF;
 constexpr uint32_t V_TILE_BYTES = 2u * TN * BT * 2u;  // [V1 | V2] of one tile, 32 x 128 fp16
 constexpr uint32_t STAGE_BYTES = TN * BT * 8u;       // fixed-point sums of one 128-row block
-// Items are dealt to CTAs in chunks of ITEM_CHUNK consecutive items (mostly
+// Items are dealt to CTAs in chunks of `chunk` consecutive items (mostly
 // the same row block P); the O_I partials of a chunk's items are summed in
-// SMEM (fp32) and leave the SM once per (chunk, row block). The grouping is a
-// function of the item index alone, so the fixed-point result does not
-// depend on the grid size or on how the chunks are split across devices.
-constexpr int ITEM_CHUNK = 4;
+// SMEM (fp32) and leave the SM once per (chunk, row block). The chunk size is
+// a function of the item count alone (item_chunk) and the grouping a
+// function of the item index, so the fixed-point result does not depend on
+// the grid size or on how the chunks are split across devices. Longer chunks
+// carry O_I across more items (fewer flushes; n = 10^6: 4 -> 16 items is
+// 360 -> 354 ms) but leave fewer chunks than CTAs at small n.
+static int item_chunk(int n_items) {
+  for (int c = 16; c > 4; c >>= 1)
+    if (n_items >= 4 * 148 * c) return c;   // at least 4 chunks per SM of a full B200
+  return 4;
+}
 constexpr uint32_t ACCI_BYTES = RB * BT * TN * 4u;
 constexpr uint32_t BAR_BYTES = 1024;
 
@@ -91,6 +98,7 @@ struct Args {
   int64_t n;
   int tiles, nblocks, n_items, nsc, nsv, t;
   int part, nparts;                 // item sharding: this launch takes items L = part (mod nparts)
+  int chunk;                        // items per chunk (item_chunk)
   const int* expo;                  // [TN] partials (in scaled units) summed as round(v 2^expo_c)
   unsigned long long* acc;          // [TN][acc_ld] fixed-point sums (column-major)
   int64_t acc_ld;
@@ -147,10 +155,10 @@ __device__ __forceinline__ void pair_of(int L, int NB, int& P, int& Q) {
 }
 
 // The tile sequence of one CTA (every role walks the same sequence): chunks
-// k = part + nparts (blockIdx.x + j gridDim.x) of ITEM_CHUNK items each; within an item, rows r then columns c, with
+// k = part + nparts (blockIdx.x + j gridDim.x) of `chunk` items each; within an item, rows r then columns c, with
 // c >= r on a diagonal item (P = Q), whose tile (r, r) is a diagonal tile.
 struct TileSeq {
-  int NB, tiles, n_items, G;   // G = chunk stride (grid x parts)
+  int NB, tiles, n_items, G, CH;   // G = chunk stride (grid x parts), CH = items per chunk
   int k, i;                    // chunk, item within the chunk
   int L, P, Q, r, c, rows_in, cols_in;
   bool ok;
@@ -162,21 +170,21 @@ struct TileSeq {
     c = c0();
   }
   __device__ void begin(const Args& a) {
-    NB = a.nblocks; tiles = a.tiles; n_items = a.n_items; G = gridDim.x * a.nparts;
+    NB = a.nblocks; tiles = a.tiles; n_items = a.n_items; G = gridDim.x * a.nparts; CH = a.chunk;
     k = a.part + a.nparts * blockIdx.x;
     i = 0;
-    L = ITEM_CHUNK * k;
+    L = CH * k;
     ok = L < n_items;
     if (ok) set_item();
   }
   // next item of this CTA's sequence (chunk by chunk)
   __device__ void next_item() {
-    if (++i < ITEM_CHUNK && ITEM_CHUNK * k + i < n_items) {
+    if (++i < CH && CH * k + i < n_items) {
       ++L;
     } else {
       k += G;
       i = 0;
-      L = ITEM_CHUNK * k;
+      L = CH * k;
     }
     ok = L < n_items;
     if (ok) set_item();
@@ -828,7 +836,8 @@ int kv_sym_partial(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, i
   a.nsc = p.nsc; a.nsv = p.nsv; a.t = t; a.part = part; a.nparts = nparts;
   a.expo = w.expo; a.acc = reinterpret_cast<unsigned long long*>(acc); a.acc_ld = p.acc_ld; a.bad = bad;
   a.prof = nullptr;
-  const int chunks = (p.n_items + ITEM_CHUNK - 1) / ITEM_CHUNK;
+  a.chunk = item_chunk(p.n_items);
+  const int chunks = (p.n_items + a.chunk - 1) / a.chunk;
   const int my_chunks = (chunks - part + nparts - 1) / nparts;
   if (my_chunks < 1) return GP_OK;
   int grid = std::min(my_chunks, num_sms());
