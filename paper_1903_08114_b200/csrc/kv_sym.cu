@@ -289,7 +289,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       const uint32_t img_f = img_bytes / 4, vt_h = V_TILE_BYTES / 2;
       while (it.ok) {
         const int J = it.J();
-        mbar_wait(smem_u32(&cempty[cs]), cph ^ 1);
+        // column slot cs holds tile Tn with Tn & 1 == cs (two slots), and the
+        // distance product that reads it commits s_full[cs]: wait on that
+        mbar_wait(smem_u32(NSC == 2 ? &s_full[cs] : &cempty[cs]), cph ^ 1);
         mbar_expect_tx(smem_u32(&cfull[cs]), img_bytes);
         bulk_g2s(smem_u32(cring + cs * img_bytes), a.col_img + (int64_t)J * img_f, img_bytes, smem_u32(&cfull[cs]));
         if (++cs == (uint32_t)NSC) { cs = 0; cph ^= 1; }
@@ -390,7 +392,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
             mma_ts(d_tm, a_t + k * 8, b_p + (uint64_t)(k * kstep_b16), idesc_d, (pass | k) != 0);
         }
         tc_commit(smem_u32(&s_full[b]));
-        tc_commit(smem_u32(&cempty[cs]));
+        if (NSC != 2) tc_commit(smem_u32(&cempty[cs]));   // NSC = 2: s_full[b] above releases the slot
       }
       __syncwarp();
       if (++cs == (uint32_t)NSC) { cs = 0; cph ^= 1; }
