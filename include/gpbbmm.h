@@ -139,6 +139,22 @@ int gp_block_mvm(const double* block, int64_t n_rows, int64_t n_cols, int64_t ld
                  const double* V, int64_t ldv, int t, double* out, int64_t ldo,
                  int32_t* first_bad_row_dev, void* stream);
 
+/* fp64 fused K̂·V without materialising the block: the precision of the
+ * reference's partitioned_mvm(training_mvm_oracle / cross_mvm_oracle),
+ * predict_mean and verify_cache (partition.py:186-241, kernels.py:293-325,
+ * predictor.py:100-132; all float64). Xr / Xc are prescaled fp64 points
+ * (x / lengthscale); out = s2 kappa(Xr, Xc) V (+ noise V[row + diag_offset]
+ * when diag_offset >= 0). *first_bad_row_dev (if non-NULL, initialised by
+ * the caller to n_rows) receives the first row with a non-finite value.
+ * Deterministic (fixed-order column-split reduction). Workspace:
+ * gp_kv_f64_workspace_bytes(n_rows, n_cols, t). */
+size_t gp_kv_f64_workspace_bytes(int64_t n_rows, int64_t n_cols, int t);
+int gp_kv_f64(int family, int d, const double* Xr, int64_t ldr, int64_t n_rows,
+              const double* Xc, int64_t ldc, int64_t n_cols, double outputscale,
+              double noise, int64_t diag_offset, const double* V, int64_t ldv, int t,
+              double* out, int64_t ldo, int32_t* first_bad_row_dev, void* workspace,
+              size_t workspace_bytes, void* stream);
+
 /* ---- mBCG (cg.py:84-164) ------------------------------------------------
  * Device-resident batched PCG. The host drives iterations phase by phase so
  * a sharded (multi-GPU) caller can all-reduce the `red` payload between

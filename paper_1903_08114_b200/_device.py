@@ -4,6 +4,7 @@ and prescaled point sets (X / lengthscale) in the layouts the kernels read."""
 from __future__ import annotations
 
 import weakref
+import zlib
 from collections import OrderedDict
 
 import numpy as np
@@ -48,7 +49,10 @@ def to_host(t) -> np.ndarray:
 class _UploadCache:
     """Keeps recently uploaded read-only host arrays (training inputs) in HBM
     so repeated MLL evaluations over the same X do not re-copy it. Keyed by
-    the array object (weakref), its data pointer, shape and a content probe."""
+    the array object (weakref), its data pointer, shape and a CRC-32 of its
+    full contents, so an in-place edit anywhere in the array invalidates the
+    cached copy (≈4 GB/s on the host: 23 ms for a 10^6 x 11 array, less than
+    the pinned staging copy of the upload it avoids)."""
 
     def __init__(self, capacity=4):
         self.capacity = capacity
@@ -56,16 +60,16 @@ class _UploadCache:
 
     @staticmethod
     def _probe(a: np.ndarray):
-        flat = a.reshape(-1)
-        idx = np.linspace(0, flat.size - 1, num=min(flat.size, 64)).astype(np.int64)
-        return hash(flat[idx].tobytes())
+        c = np.ascontiguousarray(a)
+        return (c.shape, zlib.crc32(memoryview(c.reshape(-1)).cast("B")))
 
-    def get(self, a):
+    def get(self, a, probe=None):
         if is_tensor(a):
             return to_device(a)
         a = np.asarray(a, dtype=np.float64)
         key = (id(a), a.__array_interface__["data"][0], a.shape, a.strides)
-        probe = self._probe(a) if a.size else 0
+        if probe is None:
+            probe = self._probe(a) if a.size else 0
         hit = self.entries.get(key)
         if hit is not None:
             ref, pr, t = hit
@@ -95,8 +99,8 @@ class PointSet:
     Xs32 (n x ld32, fp32, zero padded) for the fused kernels and
     Xs64 (n x d, fp64) for the fp64 paths (pivoted Cholesky, dense blocks)."""
 
-    def __init__(self, X):
-        X = upload_cache.get(X)
+    def __init__(self, X, probe=None):
+        X = upload_cache.get(X, probe)
         if X.dim() != 2:
             X = X.reshape(X.shape[0], -1)
         self.X = X
@@ -143,7 +147,7 @@ def points(X) -> PointSet:
     if ps is not None and ps._src() is X and ps._probe == probe:
         _points.move_to_end(key)
         return ps
-    ps = PointSet(X)
+    ps = PointSet(X, probe if a is X else None)
     try:
         ps._src = weakref.ref(X)
     except TypeError:

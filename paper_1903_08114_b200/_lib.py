@@ -58,6 +58,9 @@ _SIGS = {
                                      c_i64, c_p, c_sz, c_p]),
     "gp_kernel_block": (C.c_int, [C.c_int, C.c_int, c_p, c_i64, c_i64, c_p, c_i64, c_i64, c_f64,
                                   c_f64, c_i64, c_p, c_i64, c_p]),
+    "gp_kv_f64_workspace_bytes": (c_sz, [c_i64, c_i64, C.c_int]),
+    "gp_kv_f64": (C.c_int, [C.c_int, C.c_int, c_p, c_i64, c_i64, c_p, c_i64, c_i64, c_f64, c_f64, c_i64,
+                            c_p, c_i64, C.c_int, c_p, c_i64, c_p, c_p, c_sz, c_p]),
     "gp_block_mvm": (C.c_int, [c_p, c_i64, c_i64, c_i64, c_p, c_i64, C.c_int, c_p, c_i64, c_p, c_p]),
     "gp_mbcg_partials_len": (c_i64, [c_i64, C.c_int, C.c_int]),
     "gp_mbcg_init_a": (C.c_int, [C.POINTER(MbcgState), c_p, c_i64, c_p]),

@@ -151,6 +151,32 @@ def training_operator(family_code: int, d: int, X32_full, outputscale: float, no
                                     fallback=rows, force=algo == 3)
 
 
+def kv_f64(family_code: int, d: int, Xr64, Xc64, outputscale: float, noise: float, diag_offset: int, V,
+           out=None):
+    """fp64 fused K(Xr, Xc)·V (+ noise V on the diagonal when diag_offset >= 0)
+    on gp_kv_f64 — the reference-precision operator (float64 end to end).
+    Xr64 / Xc64 are prescaled fp64 points. Returns (out, first non-finite
+    row or None)."""
+    T = _T()
+    V = V.to(T.float64)
+    if V.dim() == 1:
+        V = V[:, None]
+    V = V.contiguous()
+    nr, nc, t = Xr64.shape[0], Xc64.shape[0], V.shape[1]
+    if out is None:
+        out = T.empty((nr, t), dtype=T.float64, device=D.device())
+    L = _lib.lib()
+    nbytes = L.gp_kv_f64_workspace_bytes(nr, nc, t)
+    ws = _ws.bytes("kv_f64", nbytes) if nbytes else None
+    bad = T.full((1,), nr, dtype=T.int32, device=D.device())
+    _lib.check(L.gp_kv_f64(family_code, d, _lib.ptr(Xr64), Xr64.stride(0), nr, _lib.ptr(Xc64), Xc64.stride(0),
+                           nc, float(outputscale), float(noise), int(diag_offset), _lib.ptr(V), V.stride(0), t,
+                           _lib.ptr(out), out.stride(0), _lib.ptr(bad), _lib.ptr(ws), int(nbytes), _st()),
+               "gp_kv_f64")
+    first = int(bad.item())
+    return out, (None if first >= nr else first)
+
+
 def coldot(A, B):
     """Per-column sum(A * B) of two (n, t) fp64 tensors -> (t,) fp64."""
     T = _T()

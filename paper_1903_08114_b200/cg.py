@@ -222,6 +222,11 @@ class CudaPhases:
     def active(self):
         return self.ints[:self.t]
 
+    def zero_rhs_columns(self) -> bool:
+        """True if some column of B has ||b|| = 0 (bnorm after init, global
+        over ranks); one small device->host read per solve."""
+        return bool(D.to_host((self.vec[0] == 0).any()))
+
     def status(self):
         """(active columns, first non-PD column or >= t, its iteration); syncs."""
         self.status_host.copy_(self.ints[2 * self.t:], non_blocking=True)
@@ -278,6 +283,12 @@ class MbcgRun:
         self.ph.init_b()
         self._allreduce(2 * t + k * t, 3 * t + k * t)
         self.ph.init_c()
+        # cg.py:47-49: a zero right-hand-side column is an argument error
+        # (ValueError), whichever caller built the block (SolveRequest, the
+        # MLL's [y - mu | Z], or the variance solve's cross-kernel columns
+        # of a test point far from every training point)
+        if self.ph.zero_rhs_columns():
+            raise ValueError("every right-hand-side column must be non-zero")
 
     def _allreduce(self, a, b):
         if self.comm.world > 1 and b > a:

@@ -159,9 +159,14 @@ def _nonfinite_error(plan: PartitionPlan, row: int) -> NumericError:
     return NumericError(f"non-finite kernel entry in partition {idx} (rows [{s}, {e}))")
 
 
-def partitioned_mvm(row_block_fn, X, V, plan: PartitionPlan, pool: WorkerPool) -> np.ndarray:
-    """[row_block_fn(X, a, b) @ V for each range] (partition.py:186-241)."""
-    out = partitioned_mvm_device(row_block_fn, X, V, plan, pool)
+def partitioned_mvm(row_block_fn, X, V, plan: PartitionPlan, pool: WorkerPool, *,
+                    precision: str = "fp64") -> np.ndarray:
+    """[row_block_fn(X, a, b) @ V for each range] (partition.py:186-241).
+
+    precision "fp64" (default) keeps the reference's float64 contract for
+    the kernel oracles (gp_kv_f64, fused, ~1e-15 relative); "fp32" runs the
+    tcgen05 operator the mBCG solver uses (~1e-6 relative, SFU-bound)."""
+    out = partitioned_mvm_device(row_block_fn, X, V, plan, pool, precision=precision)
     return D.to_host(out)
 
 
@@ -175,9 +180,12 @@ def _validate(X_rows: int, V, plan, pool):
                          f"row block ({plan.block_entries} entries); repartition")
 
 
-def partitioned_mvm_device(row_block_fn, X, V, plan: PartitionPlan, pool: WorkerPool):
+def partitioned_mvm_device(row_block_fn, X, V, plan: PartitionPlan, pool: WorkerPool, *,
+                           precision: str = "fp64"):
     """Device-resident variant: returns a CUDA tensor (fp64)."""
     from .kernels import CrossOperator, TrainingOperator
+    if precision not in ("fp64", "fp32"):
+        raise ValueError(f"precision must be 'fp64' or 'fp32', got {precision!r}")
     T = D.torch()
     squeeze = np.ndim(V) == 1
     Vd = D.to_device(V)
@@ -191,20 +199,24 @@ def partitioned_mvm_device(row_block_fn, X, V, plan: PartitionPlan, pool: Worker
         if isinstance(row_block_fn, TrainingOperator):
             if Vd.shape[0] != ps.n:
                 raise ValueError(f"row blocks have {ps.n} columns but V has {Vd.shape[0]} rows")
-            Xr32, _ = ps.scaled(model.scale_for(ps.d))
-            op = _ops.FusedKernelOperator(model.family_code, ps.d, Xr32, Xr32, model.outputscale,
-                                          model.noise, 0)
+            cs, noise, diag = ps, model.noise, 0
         else:
             cs = D.points(row_block_fn.X_cols)
             if cs.d != ps.d:
                 raise ValueError(f"dimension mismatch: rows have d={ps.d}, cols have d={cs.d}")
             if Vd.shape[0] != cs.n:
                 raise ValueError(f"row blocks have {cs.n} columns but V has {Vd.shape[0]} rows")
-            ls = model.scale_for(ps.d)
-            Xr32, _ = ps.scaled(ls)
-            Xc32, _ = cs.scaled(ls)
-            op = _ops.FusedKernelOperator(model.family_code, ps.d, Xr32, Xc32, model.outputscale,
-                                          0.0, -1)
+            noise, diag = 0.0, -1
+        ls = model.scale_for(ps.d)
+        Xr32, Xr64 = ps.scaled(ls)
+        Xc32, Xc64 = cs.scaled(ls)
+        if precision == "fp64":
+            _note_device_block(min(plan.block_entries, 64 * cs.n))
+            out, bad = _ops.kv_f64(model.family_code, ps.d, Xr64, Xc64, model.outputscale, noise, diag, Vd)
+            if bad is not None:
+                raise _nonfinite_error(plan, bad)
+            return out[:, 0] if squeeze else out
+        op = _ops.FusedKernelOperator(model.family_code, ps.d, Xr32, Xc32, model.outputscale, noise, diag)
         _note_device_block(min(plan.block_entries, 64 * op.n_cols))
         out = op.apply32(Vd.to(T.float32).contiguous(), Vd.shape[1]).to(T.float64)
         bad = _ops.first_nonfinite_row(out)

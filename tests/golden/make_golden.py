@@ -188,18 +188,92 @@ def row_subsets():
     save("row_subsets", **out)
 
 
-def main():
+def large_pivots():
+    """Pivoted-Cholesky pivots (rank 100) at C5 and at the bench workload
+    M1e6 (precond.py:58-98 through likelihood.py:74-91)."""
+    out = {}
+    for key in ("C5", "M1e6"):
+        w = syn.WORKLOADS[key]
+        X = syn.whitened_inputs(w.n, w.d, seed=0)
+        model = blockgp.KernelModel(w.family, syn.OUTPUTSCALE, w.lengthscales(), syn.NOISE)
+        t0 = time.perf_counter()
+        fac = rpc.partial_pivoted_cholesky(
+            lambda i: rk.kernel_rows(model, X, i, i + 1, noise=False)[0],
+            np.full(w.n, model.outputscale), w.rank)
+        pc = rpc.build_preconditioner(fac, model.noise)
+        out[f"{key}_pivots"] = fac.pivots
+        out[f"{key}_L_rows"] = fac.factor[:8]
+        out[f"{key}_precond_logdet"] = pc.logdet
+        out[f"{key}_resid_diag_sum"] = float(fac.residual_diag.sum())
+        print(f"  {key}: pivchol rank {w.rank} in {time.perf_counter() - t0:.1f}s")
+    save("large_pivots", **out)
+
+
+def c4_grad():
+    """(dK/dtheta)[rows, :] @ R at C4 (d = 90, Matern-3/2 ARD) for every
+    geometric hyperparameter, from the reference's grad_row_products
+    (kernels.py:396-410). The GPU test contracts these with a seeded Y on the
+    same rows and compares with the fused gradient pass."""
+    w = syn.WORKLOADS["C4"]
+    X = syn.whitened_inputs(w.n, w.d, seed=0)
+    model = blockgp.KernelModel(w.family, syn.OUTPUTSCALE, w.lengthscales(), syn.NOISE)
+    rows, width = 32, 8
+    start = w.n // 2 - rows // 2
+    R = np.random.default_rng(5).standard_normal((w.n, width))
+    pids = [p for p in rk.param_ids(model) if p not in ("noise", "mean")]
     t0 = time.perf_counter()
-    print("known answers"); known_answers()
-    print("kv_small"); kv_small()
-    print("full cases")
-    full_case("c1_full", 4096, 8, "rbf", False, 0, 100)
-    full_case("matern_ard", 800, 5, "matern32", True, 11, 30, n_var=48)
-    full_case("noprecond", 300, 3, "rbf", False, 12, 0, n_var=32)
-    full_case("tight_tol", 500, 4, "matern32", False, 13, 20, tol=1e-6, with_prediction=False)
-    print("row subsets"); row_subsets()
+    prods = rk.grad_row_products(model, X, start, start + rows, R, pids)
+    print(f"  C4 grad rows: {len(pids)} params x {rows} rows in {time.perf_counter() - t0:.1f}s")
+    save("c4_grad", start=start, rows=rows, width=width, r_seed=5, pids=np.array(pids),
+         products=np.stack([prods[p] for p in pids]))
+
+
+def c2_mll():
+    """A full MLL + gradients at C2 (n = 65,536, d = 8, Matern-3/2 ARD,
+    rank-5 preconditioner, eps = 1, t = 10) through the reference's
+    mll_value_and_grad on all host cores (~12 min)."""
+    w = syn.WORKLOADS["C2"]
+    X = syn.whitened_inputs(w.n, w.d, seed=0)
+    y = syn.rff_target(X, seed=1)
+    model = blockgp.KernelModel(w.family, syn.OUTPUTSCALE, w.lengthscales(), syn.NOISE)
+    plan = blockgp.plan_from_budget(w.n)
+    pool = blockgp.WorkerPool(workers=os.cpu_count())
+    cfg = rl.CgConfig(tolerance=1.0, probes=10, precond_rank=w.rank)
+    t0 = time.perf_counter()
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):
+        res = rl.mll_value_and_grad(model, X, y, plan, pool, cfg, probe_seed=0)
+    secs = time.perf_counter() - t0
+    save("c2_mll", y_checksum=np.array([y.sum(), (y * y).sum(), y[5]]),
+         value=res.value, grad_keys=np.array(list(res.gradients.keys())),
+         grad_vals=np.array(list(res.gradients.values())),
+         iterations=res.diagnostics.iterations, final_residuals=res.diagnostics.final_residuals,
+         logdet=res.diagnostics.logdet_estimate, quad=res.diagnostics.quad_term,
+         ref_seconds=secs, workers=os.cpu_count())
+    print(f"  C2 MLL: value={res.value!r} iters={res.diagnostics.iterations} ({secs:.0f}s)")
+
+
+def main(which=()):
+    t0 = time.perf_counter()
+    if not which or "base" in which:
+        print("known answers"); known_answers()
+        print("kv_small"); kv_small()
+        print("full cases")
+        full_case("c1_full", 4096, 8, "rbf", False, 0, 100)
+        full_case("matern_ard", 800, 5, "matern32", True, 11, 30, n_var=48)
+        full_case("noprecond", 300, 3, "rbf", False, 12, 0, n_var=32)
+        full_case("tight_tol", 500, 4, "matern32", False, 13, 20, tol=1e-6, with_prediction=False)
+    if not which or "row_subsets" in which:
+        print("row subsets"); row_subsets()
+    if not which or "large_pivots" in which:
+        print("large pivots"); large_pivots()
+    if not which or "c4_grad" in which:
+        print("C4 gradient rows"); c4_grad()
+    if not which or "c2_mll" in which:
+        print("C2 MLL"); c2_mll()
     print(f"done in {time.perf_counter() - t0:.0f}s")
 
 
 if __name__ == "__main__":
-    main()
+    # python make_golden.py [base] [row_subsets] [large_pivots] [c4_grad] [c2_mll]
+    main(tuple(sys.argv[1:]))

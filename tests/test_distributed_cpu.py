@@ -148,6 +148,9 @@ class NumpyPhases:
     def active(self):
         return torch.from_numpy(self.act.astype(np.int32))
 
+    def zero_rhs_columns(self):
+        return bool(np.any(self.bnorm == 0))
+
     def status(self):
         return self.stat[0], self.stat[1], self.stat[2]
 

@@ -1,0 +1,233 @@
+"""GPU parity at the BASELINE.json configurations beyond C1 (round-2 goldens,
+tests/golden/make_golden.py: row_subsets, large_pivots, c4_grad, c2_mll).
+
+* C4 (n = 329,820, d = 90, Matern-3/2 ARD, l = sqrt(d) linspace(0.75, 1.5)):
+  the compensated tcgen05 distance path (3xTF32) of K̂·V at t = 1 and t = 11
+  against the oracle and the reference's rows, and the fused ARD gradient
+  pass against the reference's grad_row_products (kernels.py:396-410).
+* Pivoted-Cholesky pivots at C5 and at the bench workload M1e6
+  (precond.py:58-98), bit-exact.
+* A full C2 MLL + gradients (likelihood.py:104-163) against the reference
+  run on the build container's cores: same iteration count, value and
+  gradients within 1e-3 (north_star).
+* The fp64 reference-precision entry points (partitioned_mvm, predict_mean,
+  verify_cache) at 1e-12, like the reference's own test_partition.py.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1903_08114_b200 as gp
+from paper_1903_08114_b200 import kernels, likelihood, precond, synthetic as syn
+from conftest import hp_from, load_golden
+
+pytestmark = pytest.mark.gpu
+KV_RTOL = 1e-4
+
+
+def colrel(got, exp):
+    got, exp = np.atleast_2d(got.T).T, np.atleast_2d(exp.T).T
+    return np.max(np.linalg.norm(got - exp, axis=0) / np.linalg.norm(exp, axis=0))
+
+
+def _c4():
+    w = syn.WORKLOADS["C4"]
+    X = syn.whitened_inputs(w.n, w.d, 0)
+    m = gp.KernelModel(w.family, syn.OUTPUTSCALE, w.lengthscales(), syn.NOISE)
+    return w, X, m
+
+
+def _rows_op(m, X, start, rows, algo):
+    from paper_1903_08114_b200 import _device as D, _ops
+    ps = D.points(X)
+    Xs32, _ = ps.scaled(m.scale_for(ps.d))
+    return _ops.FusedKernelOperator(m.family_code, ps.d, Xs32[start:start + rows], Xs32, m.outputscale,
+                                    m.noise, start, algo=algo)
+
+
+@pytest.mark.parametrize("t", [1, 11])
+def test_c4_tcgen05_distance_vs_oracle(t):
+    """d = 90: the row-tiled tcgen05 kernel (3xTF32 distance GEMM, d <= 94)
+    against the fp64 oracle on 3 x 32 rows of the full C4 operator; the
+    off-diagonal part is ~100% of each column (non-degenerate kernel)."""
+    import torch
+    w, X, m = _c4()
+    V = syn.rhs_block(w.n, 11, 2)[:, :t]
+    hp = O.make_hp(w.family, m.outputscale, m.lengthscales, m.noise)
+    V32 = torch.from_numpy(np.ascontiguousarray(V, dtype=np.float32)).cuda()
+    for start in (0, w.n // 2 - 16, w.n - 32):
+        ref = O.kernel_rows(hp, X, start, start + 32) @ V
+        diag = (m.outputscale + m.noise) * V[start:start + 32]
+        assert np.linalg.norm(ref - diag) >= 0.5 * np.linalg.norm(ref)
+        for algo in (2, 0):
+            got = _rows_op(m, X, start, 32, algo).apply32(V32, t).double().cpu().numpy()
+            assert colrel(got, ref) <= KV_RTOL, (t, start, algo, colrel(got, ref))
+
+
+def test_c4_rows_against_reference_golden_off_diagonal_share():
+    """The reference's golden rows at C4 are dominated by the off-diagonal
+    part (the round-1 C4 instance was numerically diagonal)."""
+    g = load_golden("row_subsets")
+    w, X, m = _c4()
+    V = syn.rhs_block(w.n, 11, 2)
+    rows = int(g["C4_rows"])
+    for s, exp in zip(g["C4_starts"], g["C4_KV"]):
+        s = int(s)
+        diag = (m.outputscale + m.noise) * V[s:s + rows]
+        share = np.linalg.norm(exp - diag, axis=0) / np.linalg.norm(exp, axis=0)
+        assert share.min() >= 0.5, share
+
+
+def test_c4_ard_gradient_vs_reference_rows():
+    """Fused ARD gradient forms at d = 90 (csrc/grad_ard.cu, 128 x 32 tiles)
+    on 32 rows against all n columns, contracted with a seeded Y, against
+    sum_ic Y_ic ((dK/dtheta)[rows, :] R)_ic from the reference's
+    grad_row_products (kernels.py:396-410)."""
+    import torch
+    from paper_1903_08114_b200 import _device as D
+    g = load_golden("c4_grad")
+    w, X, m = _c4()
+    start, rows, width = int(g["start"]), int(g["rows"]), int(g["width"])
+    R = np.random.default_rng(int(g["r_seed"])).standard_normal((w.n, width))
+    Y = np.random.default_rng(6).standard_normal((rows, width))
+    pids = [str(p) for p in g["pids"]]
+    expected = np.einsum("ic,pic->p", Y, g["products"])
+    ps = D.points(X)
+    Xs32, _ = ps.scaled(m.scale_for(ps.d))
+    raw = likelihood._grad_forms_raw(m, ps.d, Xs32[start:start + rows], Xs32,
+                                     torch.from_numpy(Y).float().cuda().contiguous(),
+                                     torch.from_numpy(R).float().cuda().contiguous(), self_offset=start)
+    raw = raw.cpu().numpy()
+    got = {"outputscale": raw[0]}
+    for i, l in enumerate(m.lengthscales):
+        got[f"lengthscale_{i}"] = m.outputscale * raw[1 + i] / l
+    got = np.array([got[p] for p in pids])
+    scale = np.abs(expected).max()
+    err = np.abs(got - expected).max() / scale
+    assert err <= 1e-3, err
+    # every lengthscale form carries signal (not a vacuous comparison)
+    assert np.median(np.abs(expected[1:])) >= 1e-3 * scale
+
+
+@pytest.mark.parametrize("key", ["C5", "M1e6"])
+def test_pivots_at_c5_and_bench_workload(key):
+    g = load_golden("large_pivots")
+    w = syn.WORKLOADS[key]
+    X = syn.whitened_inputs(w.n, w.d, 0)
+    m = gp.KernelModel(w.family, syn.OUTPUTSCALE, w.lengthscales(), syn.NOISE)
+    fac = precond.partial_pivoted_cholesky(precond.KernelRowSource(m, X), np.full(w.n, 1.0), w.rank)
+    np.testing.assert_array_equal(fac.pivots, g[f"{key}_pivots"])
+    np.testing.assert_allclose(fac.factor[:8], g[f"{key}_L_rows"], rtol=1e-8, atol=1e-10)
+    assert float(fac.residual_diag.sum()) == pytest.approx(float(g[f"{key}_resid_diag_sum"]), rel=1e-8)
+    pc = gp.build_preconditioner(fac, m.noise)
+    assert pc.logdet == pytest.approx(float(g[f"{key}_precond_logdet"]), rel=1e-9)
+
+
+def test_c2_full_mll_and_gradients_vs_reference():
+    """mll_value_and_grad at C2 (n = 65,536, d = 8, Matern-3/2 ARD, rank 5,
+    eps = 1, 10 probes) against the reference's own run."""
+    import os
+    if not os.path.exists(os.path.join(os.path.dirname(__file__), "golden", "c2_mll.npz")):
+        pytest.skip("c2_mll golden not generated")
+    g = load_golden("c2_mll")
+    w = syn.WORKLOADS["C2"]
+    X = syn.whitened_inputs(w.n, w.d, 0)
+    y = syn.rff_target(X, seed=1)
+    np.testing.assert_array_equal(np.array([y.sum(), (y * y).sum(), y[5]]), g["y_checksum"])
+    m = gp.KernelModel(w.family, syn.OUTPUTSCALE, w.lengthscales(), syn.NOISE)
+    res = gp.mll_value_and_grad(m, X, y, gp.plan_from_budget(w.n), gp.WorkerPool(),
+                                likelihood.CgConfig(tolerance=1.0, probes=10, precond_rank=w.rank), 0)
+    assert res.diagnostics.iterations == int(g["iterations"])
+    assert res.value == pytest.approx(float(g["value"]), rel=1e-3)
+    keys = [str(k) for k in g["grad_keys"]]
+    assert list(res.gradients) == keys
+    ref = g["grad_vals"]
+    got = np.array([res.gradients[k] for k in keys])
+    assert np.abs(got - ref).max() <= 1e-3 * np.abs(ref).max(), (got, ref)
+    np.testing.assert_allclose(res.diagnostics.final_residuals, g["final_residuals"], rtol=1e-3)
+
+
+# --------------------------------------------------------------------------
+# fp64 reference-precision entry points (gp_kv_f64)
+# --------------------------------------------------------------------------
+
+def test_partitioned_mvm_fp64_matches_dense_reference_product():
+    """test_partition.py:71-90 restated: the kernel oracles through
+    partitioned_mvm equal the reference's dense fp64 product to 1e-12."""
+    g = load_golden("kv_small")
+    for c in range(int(g["ncases"])):
+        hp = hp_from(g, f"c{c}_")
+        m = gp.KernelModel(hp["family"], hp["s2"], hp["ls"], hp["noise"])
+        X, V = g[f"c{c}_X"], g[f"c{c}_V"]
+        n = X.shape[0]
+        for rows in (1, 7, n):
+            got = gp.partitioned_mvm(kernels.training_mvm_oracle(m), X, V, gp.plan_partitions(n, rows),
+                                     gp.WorkerPool(workers=2))
+            np.testing.assert_allclose(got, g[f"c{c}_KV"], rtol=1e-12, atol=1e-12 * np.abs(g[f"c{c}_KV"]).max())
+            f32 = gp.partitioned_mvm(kernels.training_mvm_oracle(m), X, V, gp.plan_partitions(n, rows),
+                                     gp.WorkerPool(), precision="fp32")
+            assert colrel(f32, g[f"c{c}_KV"]) <= KV_RTOL
+        got = gp.partitioned_mvm(kernels.cross_mvm_oracle(m, X), g[f"c{c}_Xt"], V[:, 0],
+                                 gp.plan_partitions(33, 5), gp.WorkerPool())
+        np.testing.assert_allclose(got, g[f"c{c}_Kxv"], rtol=1e-12, atol=1e-12 * np.abs(g[f"c{c}_Kxv"]).max())
+
+
+def test_kv_f64_large_and_wide_vs_oracle():
+    """Column splits (few rows), many RHS columns (t > 64 passes), d = 90."""
+    from paper_1903_08114_b200 import _device as D, _ops
+    import torch
+    rng = np.random.default_rng(11)
+    for nr, nc, d, t in ((5, 20_000, 3, 1), (300, 3000, 90, 70), (1000, 1000, 11, 11)):
+        Xr = rng.standard_normal((nr, d))
+        Xc = Xr if nr == nc else rng.standard_normal((nc, d))
+        V = rng.standard_normal((nc, t))
+        ls = np.linspace(0.75, 1.5, d) * np.sqrt(d)
+        for fam in ("rbf", "matern32"):
+            hp = O.make_hp(fam, 1.3, ls, 0.2)
+            _, R64 = D.points(Xr).scaled(ls)
+            _, C64 = D.points(Xc).scaled(ls)
+            diag = 0 if nr == nc else -1
+            out, bad = _ops.kv_f64(0 if fam == "rbf" else 1, d, R64, C64, 1.3, 0.2, diag,
+                                   torch.from_numpy(V).cuda())
+            ref = O.kernel_block(hp, Xr, Xc, add_noise=nr == nc) @ V
+            assert bad is None
+            np.testing.assert_allclose(out.cpu().numpy(), ref, rtol=1e-11, atol=1e-11 * np.abs(ref).max())
+
+
+def test_predict_mean_and_verify_cache_fp64():
+    g = load_golden("c1_full")
+    hp = hp_from(g)
+    m = gp.KernelModel(hp["family"], hp["s2"], hp["ls"], hp["noise"], mean=hp["mean"])
+    X, y = g["X"], g["y"]
+    pc = gp.PredictionCache(model=m, X_train=X, weights=g["cache_weights"], cache_tolerance=1e-3)
+    # the reference's means from the reference's weights: fp64 end to end
+    np.testing.assert_allclose(gp.predict_mean(pc, g["X_test"]), g["pred_mean"], rtol=1e-12,
+                               atol=1e-12 * np.abs(g["pred_mean"]).max())
+    got = gp.predict_mean(pc, g["X_test"], precision="fp32")
+    assert np.abs(got - g["pred_mean"]).max() <= 1e-5 * np.abs(g["pred_mean"]).max()
+    hpo = O.make_hp(hp["family"], hp["s2"], hp["ls"], hp["noise"])
+    yc = y - hp["mean"]
+    ref = np.linalg.norm(O.kernel_block(hpo, X, X, add_noise=True) @ g["cache_weights"] - yc) / np.linalg.norm(yc)
+    assert gp.verify_cache(pc, y) == pytest.approx(ref, rel=1e-9)
+
+
+# --------------------------------------------------------------------------
+# error contract: a zero right-hand-side column is a ValueError (cg.py:47-49)
+# --------------------------------------------------------------------------
+
+def test_zero_rhs_column_is_value_error_everywhere():
+    A = np.diag([1.0, 2.0, 3.0])
+    with pytest.raises(ValueError, match="non-zero"):
+        gp.mbcg_solve(lambda V: A @ V, gp.SolveRequest(rhs=np.array([[1.0, 0.0]] * 3), tolerance=1e-6))
+    rng = np.random.default_rng(2)
+    X = rng.uniform(size=(300, 2))
+    m = gp.KernelModel("rbf", 1.0, [0.05], 0.3)
+    y = np.zeros(300)  # y - mu = 0: the MLL's first RHS column
+    with pytest.raises(ValueError, match="non-zero"):
+        gp.mll_value_and_grad(m, X, y, gp.plan_partitions(300, 64), gp.WorkerPool(),
+                              likelihood.CgConfig(precond_rank=10), 0)
+    # a test point far from every training point: K(X, x*) underflows to 0
+    cache = gp.build_cache(m, X, rng.standard_normal(300), precond_rank=10)
+    with pytest.raises(ValueError, match="non-zero"):
+        gp.predict_variance(cache, np.array([[1e3, 1e3]]), precond_rank=10)

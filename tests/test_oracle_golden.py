@@ -100,3 +100,43 @@ def test_row_subsets_inputs_regenerate():
     pc, piv = O.kernel_precond(hp, X, w.rank)
     np.testing.assert_array_equal(piv, g["C2_pivots"])
     assert pc["logdet"] == pytest.approx(float(g["C2_precond_logdet"]), rel=1e-12)
+
+
+def test_c4_instance_and_gradient_rows_pin_the_oracle():
+    """C4 (d = 90) is non-degenerate (off-diagonal K̂·V carries the columns)
+    and the oracle's dK/dtheta blocks reproduce the reference's
+    grad_row_products (kernels.py:396-410) on the golden rows."""
+    from paper_1903_08114_b200 import synthetic as syn
+    g = load_golden("row_subsets")
+    w = syn.WORKLOADS["C4"]
+    X = syn.whitened_inputs(w.n, w.d, 0)
+    np.testing.assert_array_equal(np.array([X.sum(), (X * X).sum(), X[17].sum()]), g["C4_X_checksum"])
+    hp = O.make_hp(w.family, syn.OUTPUTSCALE, w.lengthscales(), syn.NOISE)
+    V = syn.rhs_block(w.n, 11, 2)
+    rows = int(g["C4_rows"])
+    s = int(g["C4_starts"][1])
+    exp = g["C4_KV"][1]
+    np.testing.assert_allclose(O.kernel_rows(hp, X, s, s + rows) @ V, exp, rtol=1e-10, atol=1e-10)
+    diag = (hp["s2"] + hp["noise"]) * V[s:s + rows]
+    assert (np.linalg.norm(exp - diag, axis=0) / np.linalg.norm(exp, axis=0)).min() >= 0.5
+    gg = load_golden("c4_grad")
+    start, r = int(gg["start"]), int(gg["rows"])
+    R = np.random.default_rng(int(gg["r_seed"])).standard_normal((w.n, int(gg["width"])))
+    pids = [str(p) for p in gg["pids"]]
+    blocks = O.grad_blocks(hp, X[start:start + 8], X)
+    for i in (0, 1, 45, 90):
+        np.testing.assert_allclose(blocks[pids[i]] @ R, gg["products"][i][:8], rtol=1e-9,
+                                   atol=1e-9 * np.abs(gg["products"][i]).max())
+
+
+def test_large_pivots_golden_pins_the_oracle():
+    """Rank-100 pivots at the bench workload (n = 10^6) from the oracle's
+    restatement of precond.py:58-98 equal the reference's."""
+    from paper_1903_08114_b200 import synthetic as syn
+    g = load_golden("large_pivots")
+    w = syn.WORKLOADS["M1e6"]
+    X = syn.whitened_inputs(w.n, w.d, 0)
+    hp = O.make_hp(w.family, syn.OUTPUTSCALE, w.lengthscales(), syn.NOISE)
+    pc, piv = O.kernel_precond(hp, X, w.rank)
+    np.testing.assert_array_equal(piv, g["M1e6_pivots"])
+    assert pc["logdet"] == pytest.approx(float(g["M1e6_precond_logdet"]), rel=1e-12)
