@@ -12,10 +12,15 @@ reported beside it.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 runs under torchrun (one process per GPU, NCCL): rows are sharded,
-P all-gathered and CG scalars all-reduced each iteration (strong scaling:
-total n fixed). `--impl reference` times the CPU reference path (the oracle
-port of blockgp's partitioned K̂·V + CG vector ops) on the host cores.
+N > 1 runs one process per GPU over NCCL (strong scaling: total n fixed).
+Without torchrun, `--gpus N` re-launches itself under torch.distributed.run
+with N local ranks (and fails loudly if fewer than N GPUs are visible). Each
+rank owns 128-aligned rows of every CG block; the symmetric K̂·P kernel's
+work items (unordered tile pairs) are dealt across the ranks, its int64
+fixed-point partial sums reduce-scattered (each rank keeps its rows), P
+all-gathered and the CG scalars all-reduced each iteration. `--impl
+reference` times the CPU reference path (the oracle port of blockgp's
+partitioned K̂·V + CG vector ops) on the host cores.
 """
 
 from __future__ import annotations
@@ -266,6 +271,8 @@ def run_ours(args):
     kv_ms = []
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = lib.gp_launch_count()
+    if comm:
+        comm.reset_bytes()
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         start.record()
@@ -275,6 +282,7 @@ def run_ours(args):
         end.record()
         torch.cuda.synchronize()
     launches = lib.gp_launch_count() - launches0
+    comm_bytes = {k: v // args.steps for k, v in comm.bytes.items()} if comm else None
     if comm:
         dist.barrier()
     ms = start.elapsed_time(end)
@@ -333,24 +341,34 @@ def run_ours(args):
             "data": "synthetic: seeded whitened U[0,1]^11 inputs, RFF target, probes ~ N(0, P)",
             "config": {"workload": f"{w.name}: n={n} d={w.d} {w.family} ARD mBCG iteration, "
                                    f"t={T_RHS} RHS, rank-{w.rank} pivoted-Cholesky preconditioner",
-                       "parallelism": f"row-shard x{world}" if world > 1 else "1 GPU",
+                       "parallelism": (f"{world} ranks: symmetric K·P work items dealt across ranks, "
+                                       "int64 partial sums reduce-scattered; CG rows sharded (128-aligned); "
+                                       "X replicated" if sym else
+                                       f"{world} ranks: K·P rows sharded, X replicated") if world > 1 else "1 GPU",
                        "l2": "inputs larger than L2 (per-step working set: L 800 MB + CG blocks "
                              "+ X/P fp32 > 126 MB L2)"},
             "kv_tflops": job_tflops,
             "kv_ms_per_launch": kv_ms_max,
-            "roofline": {"bound": "tensor", "achieved": tflops, "peak": peaks["bf16_tflops"],
-                         "unit": "TFLOP/s", "frac": tflops / peaks["bf16_tflops"], "traffic": traffic,
-                         "peak_source": f"{peak_kind} bf16 dense (MEASURED_PEAKS.json)",
-                         "binding_unit": {
-                             "bound": "sfu", "achieved": entries_per_s / 1e9,
-                             "peak": sfu_peak_entries / 1e9, "unit": "Gentries/s",
-                             "frac": entries_per_s / sfu_peak_entries,
-                             "kernel": "kv_sym_kernel" if sym else "kv_tc_kernel",
-                             "entries_per_launch": entries_launch,
-                             "note": f"{mufu_per_entry} MUFU op(s)/evaluated entry, 148 SM x 16/clk at "
-                                     f"{sm_mhz_max} MHz"
-                                     + ("; symmetric kernel: each unordered pair evaluated once "
-                                        "(~n^2/2 entries for the n^2-entry operator)" if sym else "")}},
+            # the binding unit at CG width is the SFU (MUFU: exp, and sqrt for
+            # Matern, per evaluated entry); the tensor-core
+            # figure is reported beside it
+            "roofline": {"bound": "sfu", "achieved": entries_per_s / 1e9,
+                         "peak": sfu_peak_entries / 1e9, "unit": "Gentries/s",
+                         "frac": entries_per_s / sfu_peak_entries, "traffic": traffic,
+                         "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch, "
+                                           "committed ncu --set full capture (profiles/)",
+                         "kernel": "kv_sym_kernel" if sym else "kv_tc_kernel",
+                         "entries_per_launch": entries_launch,
+                         "algorithmic_bytes_per_launch": 4 * n * (w.d + 2 * T_RHS),
+                         "note": f"{mufu_per_entry} MUFU op(s)/evaluated entry, peak = 148 SM x 16/clk at "
+                                 f"{sm_mhz_max} MHz"
+                                 + ("; symmetric kernel: each unordered pair evaluated once "
+                                    "(~n^2/2 entries for the n^2-entry operator)" if sym else ""),
+                         "tensor": {"bound": "tensor", "achieved": tflops, "peak": peaks["bf16_tflops"],
+                                    "unit": "TFLOP/s", "frac": tflops / peaks["bf16_tflops"],
+                                    "peak_source": f"{peak_kind} bf16 dense (MEASURED_PEAKS.json)",
+                                    "flops": "rows x n x (2d + 2t) per launch"}},
+            "comm_bytes_per_iter": comm_bytes,
             "clocks": clocks,
             "gpu_launches": int(launches),
             "e2e": e2e,
@@ -412,10 +430,38 @@ def e2e_run(args, w, n, X, y, model, comm, r0, r1):
                    "(median of 3 runs)"}
 
 
+def _free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_multi_rank(args):
+    """`bench.py --gpus N` outside torchrun: run N local ranks under
+    torch.distributed.run (one process per GPU) and return its exit code."""
+    import subprocess
+    import torch
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    ndev = torch.cuda.device_count()
+    if backend == "nccl" and ndev < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {ndev}\n")
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world == 0 and args.gpus > 1:
+        return relaunch_multi_rank(args)
+    if world and world != args.gpus:
+        sys.stderr.write(f"bench.py: launched with WORLD_SIZE={world} but --gpus {args.gpus}\n")
+        return 2
     return run_ours(args)
 
 

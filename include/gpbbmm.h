@@ -101,14 +101,21 @@ int gp_kv(const gp_kv_desc* desc, const float* V, int64_t ldv, int t,
  *   gp_kv_sym_partial  — 64-bit fixed-point sums of the work items
  *                        L = part (mod nparts) of the whole square operator
  *                        (Xr == Xc, all n rows, V = all n rows) into
- *                        acc (t x acc_ld int64, column-major; acc_ld =
- *                        gp_kv_sym_acc_ld) and per-row non-finite flags bad
+ *                        acc (t * acc_ld int64, acc_ld = gp_kv_sym_acc_ld =
+ *                        n rounded up to 128; row-block major: element
+ *                        (row i, column c) at ((i / 128) t + c) 128 + i % 128,
+ *                        so the rows [128 a, 128 b) are the contiguous slice
+ *                        [128 a t, 128 b t)) and per-row non-finite flags bad
  *                        (acc_ld int32); both are overwritten.
- *   (caller)           — element-wise integer sums of acc / bad over the parts
- *                        (e.g. an NCCL int64 all-reduce): deterministic, and
- *                        bitwise equal to the single-device gp_kv result.
+ *   (caller)           — element-wise integer sums of acc / bad over the parts,
+ *                        e.g. an NCCL int64 reduce-scatter that leaves each rank
+ *                        the slice of its own 128-aligned rows: deterministic,
+ *                        and bitwise equal to the single-device gp_kv result.
  *   gp_kv_sym_finalize — rows [row0, row1) of s2 K V (+ noise V[i + diag_offset])
- *                        from the summed accumulator, NaN rows where bad != 0.
+ *                        from the summed accumulator, NaN rows where bad != 0;
+ *                        acc / bad hold the rows from acc_row0 on (a multiple
+ *                        of 128, <= row0: 0 for the whole accumulator, the
+ *                        rank's first row for its reduce-scattered slice).
  * Workspace: gp_kv_workspace_bytes(desc, t). gp_kv_sym_supported tells
  * whether the descriptor qualifies (d <= 14, t <= 16, whole square operator). */
 int gp_kv_sym_supported(const gp_kv_desc* desc, int t);
@@ -120,8 +127,8 @@ int64_t gp_kv_sym_acc_ld(const gp_kv_desc* desc);
 int gp_kv_sym_partial(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, int part, int nparts,
                       int64_t* acc, int32_t* bad, void* workspace, size_t workspace_bytes, void* stream);
 int gp_kv_sym_finalize(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, const int64_t* acc,
-                       const int32_t* bad, int64_t row0, int64_t row1, float* out, int64_t ldo,
-                       void* workspace, size_t workspace_bytes, void* stream);
+                       const int32_t* bad, int64_t acc_row0, int64_t row0, int64_t row1, float* out,
+                       int64_t ldo, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Dense fp64 kernel block (kernels.py:247-270 kernel_block, :293-308
  * kernel_rows): out[i,j] = s2 kappa(xr_i, xc_j) (+ noise where

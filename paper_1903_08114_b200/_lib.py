@@ -54,8 +54,8 @@ _SIGS = {
     "gp_kv_sym_acc_ld": (c_i64, [C.POINTER(KvDesc)]),
     "gp_kv_sym_partial": (C.c_int, [C.POINTER(KvDesc), c_p, c_i64, C.c_int, C.c_int, C.c_int, c_p, c_p, c_p,
                                     c_sz, c_p]),
-    "gp_kv_sym_finalize": (C.c_int, [C.POINTER(KvDesc), c_p, c_i64, C.c_int, c_p, c_p, c_i64, c_i64, c_p,
-                                     c_i64, c_p, c_sz, c_p]),
+    "gp_kv_sym_finalize": (C.c_int, [C.POINTER(KvDesc), c_p, c_i64, C.c_int, c_p, c_p, c_i64, c_i64, c_i64,
+                                     c_p, c_i64, c_p, c_sz, c_p]),
     "gp_kernel_block": (C.c_int, [C.c_int, C.c_int, c_p, c_i64, c_i64, c_p, c_i64, c_i64, c_f64,
                                   c_f64, c_i64, c_p, c_i64, c_p]),
     "gp_kv_f64_workspace_bytes": (c_sz, [c_i64, c_i64, C.c_int]),

@@ -79,8 +79,8 @@ class SymShardedKernelOperator:
     s2*kappa(X, X) (+ noise I) with the symmetric kernel's work items split
     across the ranks of `comm` (include/gpbbmm.h, gp_kv_sym_partial): each rank
     forms the 64-bit fixed-point partial sums of its items for all n rows, the
-    integer sums are all-reduced (deterministic), and each rank finalises its
-    own rows — bitwise equal to the single-device gp_kv result. Every rank
+    integer sums are reduce-scattered (deterministic; each rank receives the
+    slice of its own 128-aligned rows), and each rank finalises its own rows — bitwise equal to the single-device gp_kv result. Every rank
     then evaluates ~n^2/(2 world) kernel entries instead of n^2/world. Falls
     back to the row-tiled kernel (`fallback`) where one device would not use
     the symmetric kernel either (t > 16, or too few points to fill the SMs,
@@ -115,21 +115,42 @@ class SymShardedKernelOperator:
         L = _lib.lib()
         if out32 is None:
             out32 = T.empty((self.n_rows, t), dtype=T.float32, device=D.device())
+        comm = self.comm
         ld = int(L.gp_kv_sym_acc_ld(self.desc))
-        if self._acc is None or self._acc[0].numel() < t * ld:
-            self._acc = (T.empty(t * ld, dtype=T.int64, device=D.device()),
-                         T.empty(ld, dtype=T.int32, device=D.device()))
-        acc, bad = self._acc[0][: t * ld], self._acc[1][:ld]
+        m = comm.rows_per_rank
+        # reduce-scatter when every rank's rows are whole 128-row blocks (the
+        # accumulator is row-block major): each rank receives only its own
+        # slice (8 m t bytes) instead of the full 8 n t sums
+        rs = m % 128 == 0
+        full_rows = max(ld, m * comm.world) if rs else ld
+        if self._acc is None or self._acc[0].numel() < t * full_rows:
+            self._acc = (T.zeros(t * full_rows, dtype=T.int64, device=D.device()),
+                         T.zeros(full_rows, dtype=T.int32, device=D.device()),
+                         T.empty(t * m, dtype=T.int64, device=D.device()),
+                         T.empty(m, dtype=T.int32, device=D.device()))
+        acc, bad = self._acc[0][: t * full_rows], self._acc[1][:full_rows]
         nbytes = L.gp_kv_workspace_bytes(self.desc, t)
         ws = _ws.bytes("kv", nbytes)
-        _lib.check(L.gp_kv_sym_partial(self.desc, _lib.ptr(V32_full), V32_full.stride(0), t, self.comm.rank,
-                                       self.comm.world, _lib.ptr(acc), _lib.ptr(bad), _lib.ptr(ws), int(nbytes),
+        _lib.check(L.gp_kv_sym_partial(self.desc, _lib.ptr(V32_full), V32_full.stride(0), t, comm.rank,
+                                       comm.world, _lib.ptr(acc), _lib.ptr(bad), _lib.ptr(ws), int(nbytes),
                                        _st()), "gp_kv_sym_partial")
-        self.comm.allreduce_(acc)
-        self.comm.allreduce_(bad)
-        _lib.check(L.gp_kv_sym_finalize(self.desc, _lib.ptr(V32_full), V32_full.stride(0), t, _lib.ptr(acc),
-                                        _lib.ptr(bad), self.row0, self.row1, _lib.ptr(out32), out32.stride(0),
-                                        _lib.ptr(ws), int(nbytes), _st()), "gp_kv_sym_finalize")
+        if rs:
+            # rows past ld (padding of the last rank): the kernel writes only
+            # t * ld entries, a previous wider call may have left values there
+            if full_rows > ld:
+                acc[t * ld:].zero_()
+                bad[ld:].zero_()
+            acc_l, bad_l = self._acc[2][: t * m], self._acc[3][:m]
+            comm.reduce_scatter_(acc_l, acc)
+            comm.reduce_scatter_(bad_l, bad)
+            acc_row0 = self.row0
+        else:
+            comm.allreduce_(acc)
+            comm.allreduce_(bad)
+            acc_l, bad_l, acc_row0 = acc, bad, 0
+        _lib.check(L.gp_kv_sym_finalize(self.desc, _lib.ptr(V32_full), V32_full.stride(0), t, _lib.ptr(acc_l),
+                                        _lib.ptr(bad_l), acc_row0, self.row0, self.row1, _lib.ptr(out32),
+                                        out32.stride(0), _lib.ptr(ws), int(nbytes), _st()), "gp_kv_sym_finalize")
         return out32
 
 
@@ -175,6 +196,24 @@ def kv_f64(family_code: int, d: int, Xr64, Xc64, outputscale: float, noise: floa
                "gp_kv_f64")
     first = int(bad.item())
     return out, (None if first >= nr else first)
+
+
+class Kv64Operator:
+    """Rows of s2*kappa(Xr, Xc) applied in fp64 by gp_kv_f64 (no noise: the
+    CG kernels add noise*P): the reference-precision operator an mBCG solve
+    uses when CgConfig.precision == "fp64". Xr64/Xc64 are prescaled fp64
+    points."""
+
+    def __init__(self, family_code: int, d: int, Xr64, Xc64, outputscale: float):
+        self.family_code, self.d = family_code, d
+        self.Xr64, self.Xc64 = Xr64, Xc64
+        self.outputscale = float(outputscale)
+        self.n_rows, self.n_cols = Xr64.shape[0], Xc64.shape[0]
+
+    def apply64(self, V64_full, t: int, out64=None):
+        out, bad = kv_f64(self.family_code, self.d, self.Xr64, self.Xc64, self.outputscale, 0.0, -1,
+                          V64_full[: self.n_cols, :t], out64)
+        return out
 
 
 def coldot(A, B):

@@ -117,6 +117,28 @@ class FusedOperator:
         return out if D.is_tensor(V) else D.to_host(out)
 
 
+class FusedOperator64:
+    """K̂ = s2 kappa(X, X) + noise I with the kernel part applied in fp64
+    (gp_kv_f64) on this device's rows: the precision of the reference's
+    partitioned_mvm (float64 end to end). `apply64(P64_full, t, out64)`
+    computes the noiseless K·P; the CG kernels add noise*P in fp64."""
+
+    fused = True
+    f64 = True
+
+    def __init__(self, kv64, noise: float, n_total: int):
+        self.kv = kv64
+        self.noise = float(noise)
+        self.n_total = n_total
+
+    def __call__(self, V):
+        Vd = D.to_device(V)
+        if Vd.dim() == 1:
+            Vd = Vd[:, None]
+        out = self.kv.apply64(Vd.contiguous(), Vd.shape[1]) + self.noise * Vd
+        return out if D.is_tensor(V) else D.to_host(out)
+
+
 def _tridiagonal(al, be) -> Tridiagonal:
     """cg.py:167-179: diag_i = 1/a_i + b_{i-1}/a_{i-1}, off_i = sqrt(b_i)/a_i."""
     m = len(al)
@@ -270,7 +292,14 @@ class MbcgRun:
         self.ph = factory(n, t, k, self.max_iters, float(mvm.noise) if self.fused else 0.0,
                           precond, L, rows32)
         self.U = self.ph.U
-        if self.fused:
+        self.f64 = self.fused and bool(getattr(mvm, "f64", False))
+        if self.f64:
+            P = self.ph.P
+            self.Q = T.empty((n, t), dtype=T.float64, device=P.device)
+            if self.comm.world > 1:
+                self.P64_loc = T.zeros((rows32, t), dtype=T.float64, device=P.device)
+                self.P64_full = T.zeros((rows32 * self.comm.world, t), dtype=T.float64, device=P.device)
+        elif self.fused:
             P32 = self.ph.P32
             self.Q = T.empty((n, t), dtype=T.float32, device=P32.device)
             total = mvm.n_total if self.comm.world == 1 else rows32 * self.comm.world
@@ -300,7 +329,18 @@ class MbcgRun:
         if it > self.max_iters:
             raise RuntimeError("mBCG iteration cap exceeded")
         t, k, ph = self.t, self.k, self.ph
-        if self.fused:
+        if self.f64:
+            P_full = ph.P
+            if self.comm.world > 1:
+                self.P64_loc[: self.n].copy_(ph.P)
+                P_full = self.comm.allgather_rows(self.P64_loc, self.P64_full)
+            if self.kv_events is not None:
+                self.kv_events[0].record()
+            self.mvm.kv.apply64(P_full, t, self.Q)
+            if self.kv_events is not None:
+                self.kv_events[1].record()
+            Q, qf64 = self.Q, True
+        elif self.fused:
             if self.comm.world > 1:
                 self.comm.allgather_rows(ph.P32, self.P32_full)
             if self.kv_events is not None:

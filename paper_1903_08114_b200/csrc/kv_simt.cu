@@ -449,8 +449,8 @@ int64_t kv_sym_acc_ld(const gp_kv_desc* desc);
 int kv_sym_partial(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, int part, int nparts,
                    long long* acc, int* bad, void* ws, size_t ws_bytes, cudaStream_t st);
 int kv_sym_finalize(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, const long long* acc,
-                    const int* bad, int64_t row0, int64_t row1, float* out, int64_t ldo, void* ws, size_t ws_bytes,
-                    cudaStream_t st);
+                    const int* bad, int64_t acc_row0, int64_t row0, int64_t row1, float* out, int64_t ldo, void* ws,
+                    size_t ws_bytes, cudaStream_t st);
 int kv_wide(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out, int64_t ldo,
             void* ws, size_t ws_bytes, cudaStream_t st);
 size_t kv_wide_workspace(const gp_kv_desc* desc, int t);
@@ -546,14 +546,14 @@ int gp_kv_sym_partial(const gp_kv_desc* desc, const float* V, int64_t ldv, int t
 }
 
 int gp_kv_sym_finalize(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, const int64_t* acc,
-                       const int32_t* bad, int64_t row0, int64_t row1, float* out, int64_t ldo, void* workspace,
-                       size_t workspace_bytes, void* stream) {
+                       const int32_t* bad, int64_t acc_row0, int64_t row0, int64_t row1, float* out, int64_t ldo,
+                       void* workspace, size_t workspace_bytes, void* stream) {
   GP_REQUIRE(desc != nullptr && V != nullptr && acc != nullptr && bad != nullptr && out != nullptr,
              "gp_kv_sym_finalize: null argument");
   GP_REQUIRE(t >= 1 && ldv >= t && ldo >= t, "gp_kv_sym_finalize: t=%d ldv=%lld ldo=%lld", t, (long long)ldv,
              (long long)ldo);
   return gp::kv_sym_finalize(desc, V, ldv, t, reinterpret_cast<const long long*>(acc),
-                             reinterpret_cast<const int*>(bad), row0, row1, out, ldo, workspace, workspace_bytes,
+                             reinterpret_cast<const int*>(bad), acc_row0, row0, row1, out, ldo, workspace, workspace_bytes,
                              (cudaStream_t)stream);
 }
 

@@ -100,7 +100,8 @@ struct Args {
   int part, nparts;                 // item sharding: this launch takes items L = part (mod nparts)
   int chunk;                        // items per chunk (item_chunk)
   const int* expo;                  // [TN] partials (in scaled units) summed as round(v 2^expo_c)
-  unsigned long long* acc;          // [TN][acc_ld] fixed-point sums (column-major)
+  unsigned long long* acc;          // [tiles][t][BT] fixed-point sums (row-block major: a
+                                    // contiguous row range owns a contiguous slice)
   int64_t acc_ld;
   int* bad;                         // [acc_ld] non-finite partial seen for the row
   long long* prof;                  // optional per-warp phase cycle counters (GP_SYM_PROF=1)
@@ -562,7 +563,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       drain_bar();
       if (issuer) {
         for (int c = 0; c < a.t; ++c)
-          bulk_red_u64(a.acc + (int64_t)c * a.acc_ld + row0, smem_u32(sb + c * BT), BT * 8u);
+          bulk_red_u64(a.acc + row0 * a.t + (int64_t)c * BT, smem_u32(sb + c * BT), BT * 8u);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
       ++nflush;
@@ -721,10 +722,11 @@ __global__ void __cluster_dims__(kScaleCtas, 1, 1) __launch_bounds__(1024)
   cl.sync();
 }
 
-// out[i, c] = s2 * acc[c][i] 2^-E_c (+ noise V[i + diag_offset, c]); NaN where a
+// out[i, c] = s2 * acc[i][c] 2^-E_c (+ noise V[i + diag_offset, c]); NaN where a
 // non-finite partial was seen (the host names the partition, partition.py:231-236)
-// rows [row0, row1) of the operator: out[i - row0, c]
-__global__ void sym_finalize_kernel(const long long* __restrict__ acc, int64_t acc_ld,
+// rows [row0, row1) of the operator: out[i - row0, c]. acc / bad hold the rows
+// from acc_row0 on (a multiple of BT: a rank's reduce-scattered slice)
+__global__ void sym_finalize_kernel(const long long* __restrict__ acc, int64_t acc_row0,
                                     const int* __restrict__ bad, const double* __restrict__ inv_scale,
                                     int64_t row0, int64_t row1, int t, float* out, int64_t ldo, double s2,
                                     double noise, const float* V, int64_t ldv, int64_t diag_offset) {
@@ -732,9 +734,10 @@ __global__ void sym_finalize_kernel(const long long* __restrict__ acc, int64_t a
   if (idx >= (row1 - row0) * t) return;
   const int64_t i = row0 + idx / t;
   const int c = (int)(idx % t);
-  double r = s2 * ((double)acc[(int64_t)c * acc_ld + i] * inv_scale[c]);
+  const int64_t li = i - acc_row0;
+  double r = s2 * ((double)acc[((li / BT) * t + c) * BT + (li % BT)] * inv_scale[c]);
   if (diag_offset >= 0) r += noise * (double)V[(i + diag_offset) * ldv + c];
-  out[(i - row0) * ldo + c] = bad[i] ? __int_as_float(0x7fc00000) : (float)r;
+  out[(i - row0) * ldo + c] = bad[li] ? __int_as_float(0x7fc00000) : (float)r;
 }
 
 struct Plan {
@@ -811,7 +814,7 @@ static WsView carve(const Plan& p, void* ws) {
 
 int64_t kv_sym_acc_ld(const gp_kv_desc* desc) { return tcs::make_plan(desc).acc_ld; }
 
-// fixed-point sums (t x acc_ld, column-major) of the items L = part (mod
+// fixed-point sums (tiles x t x 128, row-block major) of the items L = part (mod
 // nparts) of the symmetric schedule, written into acc / bad (zeroed here);
 // partial sums of disjoint item sets add up (int64) to the full product
 int kv_sym_partial(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, int part, int nparts,
@@ -876,12 +879,14 @@ namespace tcs {
 // accumulator; the scales are recomputed from V (the same V as the partials)
 // unless this workspace already holds them (the single-device product)
 static int finalize_rows(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, const long long* acc,
-                         const int* bad, int64_t row0, int64_t row1, float* out, int64_t ldo, void* ws,
-                         size_t ws_bytes, cudaStream_t st, bool scales_ready) {
+                         const int* bad, int64_t acc_row0, int64_t row0, int64_t row1, float* out, int64_t ldo,
+                         void* ws, size_t ws_bytes, cudaStream_t st, bool scales_ready) {
   using namespace tcs;
   GP_REQUIRE(kv_sym_supported(desc, t), "gp_kv_sym: shape unsupported by the symmetric kernel");
   GP_REQUIRE(0 <= row0 && row0 <= row1 && row1 <= desc->n_rows, "gp_kv_sym_finalize: rows [%lld, %lld)",
              (long long)row0, (long long)row1);
+  GP_REQUIRE(acc_row0 >= 0 && acc_row0 % BT == 0 && acc_row0 <= row0,
+             "gp_kv_sym_finalize: acc_row0=%lld must be a multiple of %d and <= row0", (long long)acc_row0, BT);
   Plan p = make_plan(desc);
   size_t need = kv_sym_workspace(desc, t);
   GP_REQUIRE(ws != nullptr && ws_bytes >= need, "gp_kv(symmetric): workspace of %zu bytes required, %zu given",
@@ -893,7 +898,7 @@ static int finalize_rows(const gp_kv_desc* desc, const float* V, int64_t ldv, in
   }
   const int64_t tot = (row1 - row0) * t;
   if (tot == 0) return GP_OK;
-  sym_finalize_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(acc, p.acc_ld, bad, w.inv_scale, row0, row1, t,
+  sym_finalize_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(acc, acc_row0, bad, w.inv_scale, row0, row1, t,
                                                                      out, ldo, desc->outputscale, desc->noise, V,
                                                                      ldv, desc->diag_offset);
   GP_LAUNCH_CHECK();
@@ -902,9 +907,9 @@ static int finalize_rows(const gp_kv_desc* desc, const float* V, int64_t ldv, in
 }  // namespace tcs
 
 int kv_sym_finalize(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, const long long* acc,
-                    const int* bad, int64_t row0, int64_t row1, float* out, int64_t ldo, void* ws, size_t ws_bytes,
-                    cudaStream_t st) {
-  return tcs::finalize_rows(desc, V, ldv, t, acc, bad, row0, row1, out, ldo, ws, ws_bytes, st, false);
+                    const int* bad, int64_t acc_row0, int64_t row0, int64_t row1, float* out, int64_t ldo, void* ws,
+                    size_t ws_bytes, cudaStream_t st) {
+  return tcs::finalize_rows(desc, V, ldv, t, acc, bad, acc_row0, row0, row1, out, ldo, ws, ws_bytes, st, false);
 }
 
 int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out, int64_t ldo, void* ws,
@@ -915,7 +920,7 @@ int kv_sym(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* ou
   WsView w = carve(make_plan(desc), ws);
   if (int rc = kv_sym_partial(desc, V, ldv, t, 0, 1, w.acc, w.bad, ws, ws_bytes, st)) return rc;
   // kv_sym_partial left this V's scales in the workspace
-  return finalize_rows(desc, V, ldv, t, w.acc, w.bad, 0, desc->n_rows, out, ldo, ws, ws_bytes, st, true);
+  return finalize_rows(desc, V, ldv, t, w.acc, w.bad, 0, 0, desc->n_rows, out, ldo, ws, ws_bytes, st, true);
 }
 
 }  // namespace gp

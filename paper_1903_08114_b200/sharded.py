@@ -18,7 +18,16 @@ Exchanges:
   rank runs the fused gradient pass on its rows against all columns and the
   1 + n_l + 2 partial sums are all-reduced (likelihood.py:166-216);
 * predictive mean: each rank contracts K(X*, X_local) a_local and the m test
-  outputs are all-reduced (predictor.py:113-132).
+  outputs are all-reduced (predictor.py:113-132);
+* prediction cache: the representer-weight solve runs row-sharded like the
+  MLL's, the weights are all-gathered (8 n bytes) (predictor.py:59-97);
+* predictive variance: each 256-point chunk's batched solve runs row-sharded
+  (rank r forms its rows of K(X, X*)), the m quadratic forms are all-reduced
+  (predictor.py:135-182).
+
+Under torch.distributed with world > 1 the reference-API entry points
+(likelihood.mll_value_and_grad, predictor.build_cache / predict_mean /
+predict_variance) dispatch here by themselves (distributed.active_comm).
 """
 
 from __future__ import annotations
@@ -28,7 +37,7 @@ import numpy as np
 from . import _device as D
 from . import _ops
 from . import precond as _pc
-from .cg import FusedOperator, mbcg_device, slq_logdet
+from .cg import FusedOperator, FusedOperator64, mbcg_device, slq_logdet
 from .distributed import TorchComm
 from .errors import NumericError
 from .kernels import KernelModel
@@ -74,10 +83,14 @@ def mll_value_and_grad_sharded(model: KernelModel, X, y, cg_config: CgConfig, pr
     yc = yd - model.mean
     cache = build_kernel_preconditioner(model, ps, cg_config.precond_rank)   # identical on every rank
     Z = draw_probes_device(n, t, probe_seed, cache)                          # identical on every rank
-    Xs32, _ = ps.scaled(model.scale_for(ps.d))
-    # symmetric schedule split across the ranks (row-tiled kernel for t > 16)
-    kv = _ops.training_operator(model.family_code, ps.d, Xs32, model.outputscale, 0.0, -1, comm)
-    op = FusedOperator(kv, model.noise, n)
+    Xs32, Xs64 = ps.scaled(model.scale_for(ps.d))
+    if cg_config.precision == "fp64":   # this rank's rows of the fp64 operator
+        op = FusedOperator64(_ops.Kv64Operator(model.family_code, ps.d, Xs64[r0:r1], Xs64, model.outputscale),
+                             model.noise, n)
+    else:
+        # symmetric schedule split across the ranks (row-tiled kernel for t > 16)
+        kv = _ops.training_operator(model.family_code, ps.d, Xs32, model.outputscale, 0.0, -1, comm)
+        op = FusedOperator(kv, model.noise, n)
     B = T.cat([yc[:, None], Z], dim=1)[r0:r1].contiguous()
     sol = mbcg_device(op, B, cg_config.tolerance, cg_config.max_iters, cache, comm=comm, row_offset=r0)
     a_loc = sol.U[:, 0].contiguous()
@@ -107,18 +120,116 @@ def mll_value_and_grad_sharded(model: KernelModel, X, y, cg_config: CgConfig, pr
     return MLLResult(value=value, gradients=gradients, diagnostics=diag)
 
 
-def predict_mean_sharded(model: KernelModel, X_train, weights, X_test, comm: TorchComm) -> np.ndarray:
+def _allgather_vector(local, comm: TorchComm, n: int):
+    """The full n-vector from each rank's rows (all-gather of the padded
+    slices)."""
+    T = D.torch()
+    m = comm.rows_per_rank
+    pad = T.zeros(m, dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    full = T.zeros(m * comm.world, dtype=local.dtype, device=local.device)
+    comm.allgather_rows(pad, full)
+    return full[:n].contiguous()
+
+
+def build_cache_sharded(model: KernelModel, X, y, comm: TorchComm, *, tolerance: float = 1e-3,
+                        max_iters: int = 1000, precond_rank: int = 100):
+    """build_cache (predictor.py:59-97) with the representer-weight solve
+    row-sharded over the ranks of `comm` (the paper's one-time 'precompute'
+    of the predictive cache); every rank returns the same PredictionCache."""
+    from .errors import ConvergenceError
+    from .predictor import PredictionCache
+    ps = D.points(X)
+    n = ps.n
+    if comm.n_total != n:
+        raise ValueError("communicator was built for a different training size")
+    yd = D.to_device(y)
+    if tuple(yd.shape) != (n,):
+        raise ValueError(f"y has shape {tuple(yd.shape)}, expected ({n},)")
+    r0, r1 = comm.row0, comm.row1
+    cache_p = build_kernel_preconditioner(model, ps, precond_rank)   # identical on every rank
+    Xs32, _ = ps.scaled(model.scale_for(ps.d))
+    kv = _ops.training_operator(model.family_code, ps.d, Xs32, model.outputscale, 0.0, -1, comm)
+    op = FusedOperator(kv, model.noise, n)
+    B = (yd - model.mean)[r0:r1, None].contiguous()
+    sol = mbcg_device(op, B, tolerance, max_iters, cache_p, comm=comm, row_offset=r0)
+    if not sol.converged.all():
+        raise ConvergenceError(
+            f"representer-weight solve stalled at relative residual {float(sol.rel[0]):.3e} "
+            f"(requested {tolerance:g})", residuals=sol.rel)
+    w_dev = _allgather_vector(sol.U[:, 0].contiguous(), comm, n)
+    pc = PredictionCache(model=model, X_train=X if not D.is_tensor(X) else D.to_host(X),
+                         weights=D.to_host(w_dev), cache_tolerance=tolerance,
+                         diagnostics={"iterations": sol.iterations, "residual": float(sol.rel[0]),
+                                      "precond_rank": precond_rank})
+    pc._w_dev = w_dev
+    return pc
+
+
+def predict_mean_sharded(model: KernelModel, X_train, weights, X_test, comm: TorchComm,
+                         precision: str = "fp64") -> np.ndarray:
     """mu + K(X*, X) a with the training columns sharded: each rank contracts
-    its columns, the m outputs are all-reduced (predictor.py:113-132)."""
+    its columns, the m test outputs are all-reduced (predictor.py:113-132).
+    fp64 (gp_kv_f64) by default, like the single-device predict_mean."""
     T = D.torch()
     tr = D.points(X_train)
     te = D.points(np.atleast_2d(X_test) if not D.is_tensor(X_test) else X_test)
+    if te.d != tr.d:
+        raise ValueError(f"test points have dimension {te.d}, training data has {tr.d}")
     r0, r1 = comm.row0, comm.row1
     ls = model.scale_for(tr.d)
-    Xr32, _ = te.scaled(ls)
-    Xc32, _ = tr.scaled(ls)
-    w = D.to_device(weights)[r0:r1, None].to(T.float32).contiguous()
-    kv = _ops.FusedKernelOperator(model.family_code, tr.d, Xr32, Xc32[r0:r1], model.outputscale, 0.0, -1)
-    part = kv.apply32(w, 1)[:, 0].to(T.float64).contiguous()
+    Xr32, Xr64 = te.scaled(ls)
+    Xc32, Xc64 = tr.scaled(ls)
+    w = D.to_device(weights)[r0:r1].contiguous()
+    if precision == "fp64":
+        part, _ = _ops.kv_f64(model.family_code, tr.d, Xr64, Xc64[r0:r1], model.outputscale, 0.0, -1, w)
+        part = part[:, 0].contiguous()
+    else:
+        kv = _ops.FusedKernelOperator(model.family_code, tr.d, Xr32, Xc32[r0:r1], model.outputscale, 0.0, -1)
+        part = kv.apply32(w[:, None].to(T.float32).contiguous(), 1)[:, 0].to(T.float64).contiguous()
     comm.allreduce_(part)
     return model.mean + D.to_host(part)
+
+
+def predict_variance_sharded(cache, X_test, comm: TorchComm, *, tolerance: float = 0.01,
+                             max_iters: int = 1000, precond_rank: int = 100, chunk: int = 256):
+    """predict_variance (predictor.py:135-182) with every batched solve
+    row-sharded: rank r forms its rows of B = K(X, X*_chunk), the solve runs
+    over all ranks (t = chunk right-hand sides: the row-tiled wide kernel on
+    this rank's rows against the all-gathered directions), and the
+    quadratic forms colsum(B o S) are all-reduced. Every rank returns the same
+    (variances, clamped)."""
+    from .errors import ConvergenceError
+    from .kernels import _dense_block
+    X_test = np.atleast_2d(X_test) if not D.is_tensor(X_test) else X_test
+    model = cache.model
+    tr = D.points(cache.X_train)
+    n = tr.n
+    if X_test.shape[1] != tr.d:
+        raise ValueError("test/train dimension mismatch")
+    if comm.n_total != n:
+        raise ValueError("communicator was built for a different training size")
+    r0, r1 = comm.row0, comm.row1
+    cache_p = build_kernel_preconditioner(model, tr, precond_rank)
+    Xs32, _ = tr.scaled(model.scale_for(tr.d))
+    kv = _ops.training_operator(model.family_code, tr.d, Xs32, model.outputscale, 0.0, -1, comm)
+    op = FusedOperator(kv, model.noise, n)
+    m = X_test.shape[0]
+    out = np.empty(m)
+    clamped = 0
+    for c0 in range(0, m, chunk):
+        c1 = min(c0 + chunk, m)
+        te = D.points(X_test[c0:c1])
+        Bm = _dense_block(model, tr, te, -1, (r0, r1)).contiguous()
+        sol = mbcg_device(op, Bm, tolerance, max_iters, cache_p, comm=comm, row_offset=r0)
+        if not sol.converged.all():
+            bad = np.flatnonzero(~sol.converged)
+            raise ConvergenceError(f"variance solves for {bad.size} test points did not reach "
+                                   f"tolerance {tolerance:g}", residuals=sol.rel)
+        quad = comm.allreduce_(_ops.coldot(Bm, sol.U))
+        var = model.outputscale - D.to_host(quad)
+        low = var < 1e-12
+        clamped += int(np.count_nonzero(low))
+        var[low] = 1e-12
+        out[c0:c1] = var
+    return out, clamped

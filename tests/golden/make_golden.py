@@ -244,7 +244,18 @@ def c2_mll():
     with threadpool_limits(1):
         res = rl.mll_value_and_grad(model, X, y, plan, pool, cfg, probe_seed=0)
     secs = time.perf_counter() - t0
+    # replay the solve through the reference's own stages to expose the
+    # per-column recurrence (residual history, tridiagonal orders)
+    cache = rl.build_kernel_preconditioner(model, X, w.rank)
+    Z = rl.draw_probes(w.n, 10, 0, cache)
+    oracle = rk.training_mvm_oracle(model)
+    with threadpool_limits(1):
+        rep = rcg.mbcg_solve(lambda V: blockgp.partitioned_mvm(oracle, X, V, plan, pool),
+                             rcg.SolveRequest(rhs=np.hstack([(y - model.mean)[:, None], Z]),
+                                              tolerance=1.0, preconditioner=cache))
     save("c2_mll", y_checksum=np.array([y.sum(), (y * y).sum(), y[5]]),
+         residual_history=rep.residual_history, diag_lens=np.array([T.order for T in rep.tridiagonals]),
+         rep_iterations=rep.iterations, Z_checksum=np.array([Z.sum(), (Z * Z).sum()]),
          value=res.value, grad_keys=np.array(list(res.gradients.keys())),
          grad_vals=np.array(list(res.gradients.values())),
          iterations=res.diagnostics.iterations, final_residuals=res.diagnostics.final_residuals,

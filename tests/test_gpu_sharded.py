@@ -121,3 +121,84 @@ def test_symmetric_items_split_across_ranks_bitwise_equal_single_device(world):
         got = np.vstack([np.load(os.path.join(tmp, f"kv{r}.npy")) for r in range(world)])
     assert got.shape == ref.shape
     assert np.array_equal(got, ref)
+
+
+def _pred_problem():
+    import paper_1903_08114_b200 as gp
+    from paper_1903_08114_b200 import synthetic as syn
+    X = syn.whitened_inputs(16384, 8, 0)   # >= 12,288 points: the symmetric K·P kernel
+    y = syn.rff_target(X, seed=1)
+    model = gp.KernelModel("matern32", 1.0, np.linspace(0.75, 1.5, 8) * 0.5, 0.1)
+    return X, y, model
+
+
+def _pred_rank_main(rank, world, port, outdir):
+    """The reference-API entry points under torch.distributed: build_cache,
+    predict_mean and predict_variance dispatch to their row-sharded forms."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    import paper_1903_08114_b200 as gp
+    from paper_1903_08114_b200 import distributed
+    X, y, model = _pred_problem()
+    comm = distributed.active_comm(X.shape[0])
+    assert comm is not None and comm.world == world
+    cache = gp.build_cache(model, X, y, precond_rank=30)
+    Xt = np.random.default_rng(2).uniform(size=(300, 8))
+    mean = gp.predict_mean(cache, Xt)
+    var, clamped = gp.predict_variance(cache, Xt[:40], precond_rank=30)
+    np.savez(os.path.join(outdir, f"p{rank}.npz"), w=cache.weights, iters=cache.diagnostics["iterations"],
+             mean=mean, var=var, clamped=clamped, rows=np.array([comm.row0, comm.row1]),
+             bytes_rs=comm.bytes["reduce_scatter"])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_reference_api_prediction_paths_shard_under_torch_distributed():
+    """build_cache / predict_mean / predict_variance, unchanged signatures,
+    run row-sharded over 2 ranks and agree with one device."""
+    import torch.multiprocessing as mp
+    import paper_1903_08114_b200 as gp
+    X, y, model = _pred_problem()
+    cache = gp.build_cache(model, X, y, precond_rank=30)
+    Xt = np.random.default_rng(2).uniform(size=(300, 8))
+    ref_mean = gp.predict_mean(cache, Xt)
+    ref_var, _ = gp.predict_variance(cache, Xt[:40], precond_rank=30)
+    with tempfile.TemporaryDirectory() as d:
+        port = 29900 + os.getpid() % 1000
+        mp.spawn(_pred_rank_main, args=(2, port, d), nprocs=2, join=True)
+        outs = [np.load(os.path.join(d, f"p{r}.npz")) for r in range(2)]
+    assert [tuple(o["rows"]) for o in outs] == [(0, 8192), (8192, 16384)]
+    for o in outs:
+        assert int(o["iters"]) == cache.diagnostics["iterations"]
+        np.testing.assert_allclose(o["w"], cache.weights, rtol=1e-7, atol=1e-9 * np.abs(cache.weights).max())
+        np.testing.assert_allclose(o["mean"], ref_mean, rtol=1e-7, atol=1e-9)
+        np.testing.assert_allclose(o["var"], ref_var, rtol=1e-6, atol=1e-9)
+        assert int(o["bytes_rs"]) > 0   # the int64 K·P sums were reduce-scattered
+    np.testing.assert_array_equal(outs[0]["w"], outs[1]["w"])
+    np.testing.assert_array_equal(outs[0]["var"], outs[1]["var"])
+
+
+def test_bench_two_ranks_end_to_end():
+    """`bench.py --gpus 2` launches two ranks itself (gloo so both share the
+    one GPU of the test box) and reports n_gpus 2 with the measured exchange."""
+    import json
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, BENCH_DIST_BACKEND="gloo")
+    r = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), "--gpus", "2", "--steps", "3",
+                        "--warmup", "3", "--points", "20000", "--no-cpu"], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2
+    assert line["value"] > 0 and line["e2e"]["value"] > 0
+    cb = line["comm_bytes_per_iter"]
+    n, t = 20000, 11
+    m = 10112  # ceil(20000 / 2) rounded up to 128 rows
+    assert cb["reduce_scatter"] == 8 * 2 * m * t + 4 * 2 * m   # int64 sums + int32 row flags
+    assert cb["all_gather"] == 4 * 2 * m * 12                   # fp32 P rows (ld 12)
+    assert line["roofline"]["bound"] == "sfu"
