@@ -421,7 +421,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       SYM_COUNT();
       SYM_T(5, mbar_wait(smem_u32(&vfull[vs]), vph));
       const bool mir = it.mirror();
-      if (mir) SYM_T(5, mbar_wait(smem_u32(&vi_full[rowc & 1]), (rowc >> 1) & 1));
+      // V_I is loaded for every row; a row of a diagonal item whose only tile
+      // is the diagonal one has no mirror product, but its load must still be
+      // awaited before vi_empty is committed (no bulk copy may be in flight
+      // when the barrier is re-armed or the CTA exits)
+      if (mir || (it.first_in_row() && it.last_in_row()))
+        SYM_T(5, mbar_wait(smem_u32(&vi_full[rowc & 1]), (rowc >> 1) & 1));
       tc_fence_after();
       if (leader) {
         // direct first, then release the S/K buffer: the mirror reads only

@@ -655,25 +655,26 @@ __global__ void v_colscale_kernel(const float* __restrict__ V, int64_t ldv, int6
 
 // V image for the wide kernel: rows 0..NW-1 V1, NW..2NW-1 V2 (canonical, 2NW rows)
 __global__ void v_image16w_kernel(const float* __restrict__ V, int64_t ldv, int t, int NW, int64_t ncols,
-                                  const float* __restrict__ vscale, __half* img, int64_t ntiles) {
+                                  const float* __restrict__ vscale, __half* img, int64_t ntiles, int TP) {
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= ntiles * BN * NW) return;
-  int64_t tile = idx / (BN * NW);
-  int rem = (int)(idx - tile * BN * NW);
+  if (idx >= ntiles * TP * NW) return;
+  int64_t tile = idx / (TP * NW);
+  int rem = (int)(idx - tile * TP * NW);
   int k = rem / NW, nn = rem - k * NW;
-  int64_t col = tile * BN + k;
+  int64_t col = tile * TP + k;
   float v = (col < ncols && nn < t) ? V[col * ldv + nn] * vscale[nn] : 0.f;
   __half h1 = __float2half_rn(v);
   __half h2 = __float2half_rn(v - __half2float(h1));
-  __half* base = img + tile * (2 * NW * BN);
+  __half* base = img + tile * (2 * NW * TP);
   base[canon16(nn, k, 2 * NW)] = h1;
   base[canon16(NW + nn, k, 2 * NW)] = h2;
 }
 
 int v_images16_wide(const float* V, int64_t ldv, int t, int NW, int64_t ncols, const float* vscale, __half* img,
-                    int64_t ntiles, cudaStream_t st) {
-  int64_t tot = ntiles * BN * NW;
-  v_image16w_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(V, ldv, t, NW, ncols, vscale, img, ntiles);
+                    int64_t ntiles, cudaStream_t st, int tile_points) {
+  int64_t tot = ntiles * tile_points * NW;
+  v_image16w_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(V, ldv, t, NW, ncols, vscale, img, ntiles,
+                                                                   tile_points);
   GP_LAUNCH_CHECK();
   return GP_OK;
 }

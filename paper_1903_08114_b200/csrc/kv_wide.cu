@@ -26,7 +26,6 @@ namespace tw {
 using namespace gp::tc;
 
 constexpr int BM = 128;
-constexpr int BN = 64;
 constexpr int TMAX = 256;          // widest right-hand-side block
 constexpr int CH = 32;             // column tiles per TMEM accumulation chain
 constexpr int NUM_EPI_WARPS = 8;   // two per TMEM lane quarter, 32 columns of a tile each
@@ -46,6 +45,7 @@ struct Args {
   int64_t diag_offset, self_offset;
   float* accw;            // [splits][NW][rows_pad] column-major fp32 partial sums
   int64_t rows_pad;
+  int nfold;              // fold staging buffers per epilogue warp (2, or 1 when SMEM is tight)
 };
 
 // accumulator layout (fp32): [split][row tile][lane quarter q][column][32 rows],
@@ -72,9 +72,14 @@ __device__ __forceinline__ uint32_t TMK1(uint32_t b) { return 128 + b * 64; }
 __device__ __forceinline__ uint32_t TMK2(uint32_t b) { return 160 + b * 64; }
 constexpr uint32_t TMO = 256;
 
-template <int FAM>
+// BNT: column tile width (64, or 32 when the augmented width DK > 32: the
+// d <= 94 images of C4-shaped inputs, whose 96-wide row image alone takes
+// 96 KB of SMEM). Each of the 8 epilogue warps covers CW = BNT / 2 columns.
+template <int FAM, int BNT>
 __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int BN = BNT;
+  constexpr int CW = BNT / 2;
   const int DK = a.DK, NW = a.NW;
   const uint32_t row_bytes = 2u * BM * DK * 4u;
   const uint32_t col_bytes = 2u * BN * DK * 4u;
@@ -98,7 +103,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
   uint64_t* xr_full = o_empty + 1;
   uint64_t* xr_empty = xr_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xr_empty + 1);
-  float* fold_s = reinterpret_cast<float*>(vring + NSV * v_bytes + 512);   // [8 warps][2][32 x 16]
+  float* fold_s = reinterpret_cast<float*>(vring + NSV * v_bytes + 512);   // [8 warps][nfold][32 x 16]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -269,16 +274,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
         mbar_wait(smem_u32(&s_full[sb]), sph);
         tc_fence_after();
         uint32_t v[32];
-        tmem_ld32(tmem + lane_base + TMS(sb) + half * 32, v);
+        if constexpr (CW == 32) {
+          tmem_ld32(tmem + lane_base + TMS(sb) + half * CW, v);
+        } else {
+          tmem_ld16(tmem + lane_base + TMS(sb) + half * CW, *reinterpret_cast<uint32_t(*)[16]>(v));
+        }
         tmem_wait_ld();
-        const int64_t e_diag = diag_col - ((int64_t)(ct0 + jj) * BN + half * 32);
-        if (__any_sync(0xffffffffu, e_diag >= 0 && e_diag < 32)) {
+        const int64_t e_diag = diag_col - ((int64_t)(ct0 + jj) * BN + half * CW);
+        if (__any_sync(0xffffffffu, e_diag >= 0 && e_diag < CW)) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
+          for (int e = 0; e < CW; ++e)
             if (e == e_diag) v[e] = 0u;   // same point on both sides: r2 = 0 exactly
         }
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
+        for (int e = 0; e < CW; ++e) {
           float sv = __uint_as_float(v[e]);
           float kap;
           if (FAM == GP_FAMILY_RBF) {
@@ -293,13 +302,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
         mbar_wait(smem_u32(&k_empty[kb]), kph ^ 1);   // K[kb] was read two tiles ago
         tc_fence_after();
 #pragma unroll
-        for (int s16 = 0; s16 < 2; ++s16) {
+        for (int s16 = 0; s16 < CW / 16; ++s16) {
           uint32_t p1[8], p2[8];
 #pragma unroll
           for (int k = 0; k < 8; ++k)
             split_pair(__uint_as_float(v[16 * s16 + 2 * k]), __uint_as_float(v[16 * s16 + 2 * k + 1]), p1[k], p2[k]);
-          tmem_st8(tmem + lane_base + TMK1(kb) + half * 16 + 8 * s16, p1);
-          tmem_st8(tmem + lane_base + TMK2(kb) + half * 16 + 8 * s16, p2);
+          tmem_st8(tmem + lane_base + TMK1(kb) + half * (CW / 2) + 8 * s16, p1);
+          tmem_st8(tmem + lane_base + TMK2(kb) + half * (CW / 2) + 8 * s16, p2);
         }
         tmem_wait_st();
         tc_fence_before();
@@ -316,12 +325,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
           // (keeps the per-element addition order fixed: deterministic)
           if (lane == 0) bulk_wait_all();
           __syncwarp();
-          float* stg0 = fold_s + (warp - 4) * 2 * (32 * 16);
+          float* stg0 = fold_s + (warp - 4) * a.nfold * (32 * 16);
           int buf = 0;
-          for (int c0 = half * 16; c0 < NW; c0 += 32, buf ^= 1) {
+          for (int c0 = half * 16; c0 < NW; c0 += 32, buf = a.nfold == 2 ? buf ^ 1 : 0) {
             uint32_t o[16];
             tmem_ld16(tmem + lane_base + TMO + c0, o);
-            if (lane == 0) bulk_wait_read1();   // staging buffer `buf` free again
+            if (lane == 0) {   // staging buffer `buf` free again
+              if (a.nfold == 2) bulk_wait_read1(); else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            }
             __syncwarp();
             tmem_wait_ld();
             float* stg = stg0 + buf * (32 * 16);
@@ -370,15 +381,42 @@ __global__ void kv_wide_finalize(const float* __restrict__ accw, int splits, int
 }
 
 struct Plan {
-  int DK, NW, row_tiles, col_tiles, splits, tiles_per_split, nsc, nsv;
+  int DK, NW, BN, nfold, row_tiles, col_tiles, splits, tiles_per_split, nsc, nsv;
   int64_t rows_pad;
   size_t row_img_bytes, col_img_bytes, v_img_bytes, split_bytes, smem;
 };
+
+// SMEM rings for column tile width bn with nfold staging buffers per
+// epilogue warp; false when a 2-deep column ring and 2-deep V ring do not fit
+static bool fit_rings(Plan& p, int bn, int nfold, size_t cap) {
+  const size_t row_b = 2u * BM * p.DK * 4, col_b = 2u * bn * p.DK * 4, v_b = 2u * p.NW * bn * 2;
+  const size_t fold_b = (size_t)NUM_EPI_WARPS * nfold * STAGE_FOLD_BYTES;
+  if (row_b + 512 + fold_b + 2 * col_b + 2 * v_b > cap) return false;
+  const size_t budget = cap - row_b - 512 - fold_b;
+  // V ring as deep as fits next to a 2-deep column ring (at most 4), then the
+  // column ring takes the rest (at most 8)
+  p.nsv = (int)std::min<size_t>(4, (budget - 2 * col_b) / v_b);
+  p.nsc = (int)std::min<size_t>(8, (budget - p.nsv * v_b) / col_b);
+  p.BN = bn;
+  p.nfold = nfold;
+  p.smem = row_b + p.nsc * col_b + p.nsv * v_b + 512 + fold_b;
+  return true;
+}
 
 static Plan make_plan(const gp_kv_desc* d, int t) {
   Plan p;
   p.DK = (d->d + 2 + 7) / 8 * 8;
   p.NW = (t + 15) / 16 * 16;
+  // 64-point column tiles with double-buffered fold staging (the tuned
+  // d <= 30 configuration); for large d (C4: DK = 96, a 96 KB row image)
+  // 32-point tiles and single-buffered staging in the full 227 KB
+  p.nsv = p.nsc = 0;
+  if (!fit_rings(p, 64, 2, 224 * 1024) && !fit_rings(p, 32, 2, 227 * 1024 - 1024) &&
+      !fit_rings(p, 32, 1, 227 * 1024 - 1024)) {
+    p.BN = 32;
+    p.nfold = 1;
+  }
+  const int BN = p.BN;
   p.row_tiles = (int)((d->n_rows + BM - 1) / BM);
   p.col_tiles = (int)((d->n_cols + BN - 1) / BN);
   // column splits depend on the column count only for the square training
@@ -395,14 +433,6 @@ static Plan make_plan(const gp_kv_desc* d, int t) {
   p.v_img_bytes = (size_t)p.col_tiles * 2 * p.NW * BN * 2;
   p.rows_pad = (int64_t)p.row_tiles * BM;
   p.split_bytes = (size_t)p.splits * p.NW * p.rows_pad * 4 + 256 * sizeof(double) + 2 * TMAX * sizeof(float);
-  const size_t row_b = 2u * BM * p.DK * 4, col_b = 2u * BN * p.DK * 4, v_b = 2u * p.NW * BN * 2;
-  const size_t fold_b = NUM_EPI_WARPS * 2 * STAGE_FOLD_BYTES;
-  const size_t budget = 224 * 1024 - row_b - 512 - fold_b;
-  // V ring as deep as fits next to a 2-deep column ring (at most 4), then the
-  // column ring takes the rest (at most 8)
-  p.nsv = (int)std::min<size_t>(4, budget >= 2 * col_b ? (budget - 2 * col_b) / v_b : 0);
-  p.nsc = p.nsv >= 2 ? (int)std::min<size_t>(8, (budget - p.nsv * v_b) / col_b) : 0;
-  p.smem = row_b + p.nsc * col_b + p.nsv * v_b + 512 + fold_b;
   return p;
 }
 
@@ -412,7 +442,7 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 bool kv_wide_supported(const gp_kv_desc* d, int t) {
   if (t <= 16 || t > tw::TMAX) return false;
-  if (d->d < 1 || d->d + 2 > 32) return false;
+  if (d->d < 1 || d->d + 2 > 96) return false;   // DK <= 96 (d <= 94, the kv_tc limit)
   const tw::Plan p = tw::make_plan(d, t);
   return p.nsv >= 2 && p.nsc >= 2;
 }
@@ -441,10 +471,10 @@ int kv_wide(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* o
   float* accw = reinterpret_cast<float*>(w);
   const double c = desc->family == GP_FAMILY_RBF ? 1.4426950408889634 : -6.0;
   if (int rc = tc::distance_images(desc->Xr, desc->ldr, desc->n_rows, desc->Xc, desc->ldc, desc->n_cols, desc->d,
-                                   p.DK, BM, BN, c, mean, row_img, col_img, st))
+                                   p.DK, BM, p.BN, c, mean, row_img, col_img, st))
     return rc;
   if (int rc = tc::v_colscale(V, ldv, desc->n_cols, t, vscale, inv_vscale, st)) return rc;
-  if (int rc = tc::v_images16_wide(V, ldv, t, p.NW, desc->n_cols, vscale, v_img, p.col_tiles, st)) return rc;
+  if (int rc = tc::v_images16_wide(V, ldv, t, p.NW, desc->n_cols, vscale, v_img, p.col_tiles, st, p.BN)) return rc;
   Args a;
   a.row_img = row_img; a.col_img = col_img; a.v_img = v_img; a.inv_vscale = inv_vscale;
   a.DK = p.DK; a.NW = p.NW;
@@ -453,11 +483,13 @@ int kv_wide(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* o
   a.tiles_per_split = p.tiles_per_split; a.nsc = p.nsc; a.nsv = p.nsv; a.t = t;
   a.s2 = (float)desc->outputscale; a.noise = (float)desc->noise; a.diag_offset = desc->diag_offset;
   a.self_offset = desc->self_offset;
-  a.accw = accw; a.rows_pad = p.rows_pad;
+  a.accw = accw; a.rows_pad = p.rows_pad; a.nfold = p.nfold;
   GP_CUDA_TRY(cudaMemsetAsync(accw, 0, (size_t)p.splits * p.NW * p.rows_pad * 4, st));
   int items = p.row_tiles * p.splits;
   int grid = std::min(items, num_sms());
-  auto kern = desc->family == GP_FAMILY_RBF ? kv_wide_kernel<GP_FAMILY_RBF> : kv_wide_kernel<GP_FAMILY_MATERN32>;
+  auto kern = desc->family == GP_FAMILY_RBF
+                  ? (p.BN == 64 ? kv_wide_kernel<GP_FAMILY_RBF, 64> : kv_wide_kernel<GP_FAMILY_RBF, 32>)
+                  : (p.BN == 64 ? kv_wide_kernel<GP_FAMILY_MATERN32, 64> : kv_wide_kernel<GP_FAMILY_MATERN32, 32>);
   GP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   kern<<<grid, NTHREADS, p.smem, st>>>(a);
   GP_LAUNCH_CHECK();

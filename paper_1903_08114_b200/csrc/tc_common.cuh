@@ -218,9 +218,9 @@ int v_images16(const float* V, int64_t ldv, int t, int64_t ncols, const float* v
                int64_t ntiles, cudaStream_t st);
 // tf32 V image: per 64-point tile a 32-row K-major operand [V_hi | V_lo]
 int v_images32(const float* V, int64_t ldv, int t, int64_t ncols, float* img, int64_t ntiles, cudaStream_t st);
-// fp16 V image for the wide kernel: rows 0..NW-1 V1, NW..2NW-1 V2 per 64-point tile
+// fp16 V image for the wide kernel: rows 0..NW-1 V1, NW..2NW-1 V2 per tile of tile_points points
 int v_images16_wide(const float* V, int64_t ldv, int t, int NW, int64_t ncols, const float* vscale, __half* img,
-                    int64_t ntiles, cudaStream_t st);
+                    int64_t ntiles, cudaStream_t st, int tile_points = 64);
 // per-column power-of-two scales 2^s_c with 2^s_c max|V_c| <= 2^14 (fp16 range) and their inverses
 int v_colscale(const float* V, int64_t ldv, int64_t n, int t, float* vscale, float* inv_vscale, cudaStream_t st);
 

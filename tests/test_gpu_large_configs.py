@@ -231,3 +231,53 @@ def test_zero_rhs_column_is_value_error_everywhere():
     cache = gp.build_cache(m, X, rng.standard_normal(300), precond_rank=10)
     with pytest.raises(ValueError, match="non-zero"):
         gp.predict_variance(cache, np.array([[1e3, 1e3]]), precond_rank=10)
+
+
+@pytest.mark.parametrize("t", [40, 256])
+def test_wide_rhs_large_d_tensor_core_vs_oracle(t):
+    """kv_wide at d = 90 (32-point column tiles, 96-wide 3xTF32 distance
+    images): the variance solves of C4 run on the tensor cores."""
+    from paper_1903_08114_b200 import _device as D, _ops, _lib
+    import torch
+    rng = np.random.default_rng(t)
+    n, d = 3000, 90
+    X = rng.standard_normal((n, d))
+    V = rng.standard_normal((n, t))
+    ls = np.linspace(0.75, 1.5, d) * np.sqrt(d)
+    for fam in ("rbf", "matern32"):
+        m = gp.KernelModel(fam, 1.3, ls, 0.2)
+        Xs32, _ = D.points(X).scaled(ls)
+        op = _ops.FusedKernelOperator(m.family_code, d, Xs32, Xs32, 1.3, 0.2, 0, algo=0)
+        got = op.apply32(torch.from_numpy(V).float().cuda(), t).double().cpu().numpy()
+        ref = O.kernel_mvm(O.make_hp(fam, 1.3, ls, 0.2), X, V)
+        assert colrel(got, ref) <= KV_RTOL, (fam, colrel(got, ref))
+        # cross block (test rows x training columns), as the variance RHS solve uses
+        Xt = rng.standard_normal((300, d))
+        Xt32, _ = D.points(Xt).scaled(ls)
+        cop = _ops.FusedKernelOperator(m.family_code, d, Xt32, Xs32, 1.3, 0.0, -1, algo=0)
+        got = cop.apply32(torch.from_numpy(V).float().cuda(), t).double().cpu().numpy()
+        ref = O.kernel_block(O.make_hp(fam, 1.3, ls, 0.2), Xt, X) @ V
+        assert colrel(got, ref) <= KV_RTOL, (fam, "cross", colrel(got, ref))
+    # the dispatcher ran the tensor-core kernel, not the SIMT FFMA fallback
+    # (different arithmetic: the two results are not bitwise equal)
+    simt = _ops.FusedKernelOperator(m.family_code, d, Xt32, Xs32, 1.3, 0.0, -1, algo=1)
+    assert not np.array_equal(simt.apply32(torch.from_numpy(V).float().cuda(), t).double().cpu().numpy(), got)
+
+
+def test_c4_shaped_predict_variance_vs_oracle():
+    """predict_variance at d = 90 (256-column batched solves on kv_wide)
+    against the oracle's restatement of predictor.py:135-182."""
+    rng = np.random.default_rng(9)
+    n, d = 4000, 90
+    X = rng.standard_normal((n, d))
+    ls = np.linspace(0.75, 1.5, d) * np.sqrt(d)
+    m = gp.KernelModel("matern32", 1.0, ls, 0.1)
+    hp = O.make_hp("matern32", 1.0, ls, 0.1)
+    y = rng.standard_normal(n)
+    w = np.linalg.solve(O.kernel_block(hp, X, X, add_noise=True), y)
+    cache = gp.PredictionCache(model=m, X_train=X, weights=w, cache_tolerance=1e-3)
+    Xt = rng.standard_normal((300, d))
+    var, clamped = gp.predict_variance(cache, Xt, tolerance=1e-4, precond_rank=50)
+    Kx = O.kernel_block(hp, X, Xt)
+    exact = 1.0 - np.einsum("ij,ij->j", Kx, np.linalg.solve(O.kernel_block(hp, X, X, add_noise=True), Kx))
+    assert np.abs(var - exact).max() <= 2e-4, np.abs(var - exact).max()
