@@ -116,7 +116,9 @@ def lib():
                     raise RuntimeError(
                         "paper_1903_08114_b200 needs a CUDA (sm_100a) device; "
                         "there is no CPU fallback")
-                _lib = load_library()
+                # GPBBMM_LIB: a variant build of the same library (A/B
+                # diagnostics, scripts/build_variant.py); default in-tree
+                _lib = load_library(os.environ.get("GPBBMM_LIB") or LIB_PATH)
     return _lib
 
 
