@@ -263,14 +263,26 @@ int gp_precond_factor(int64_t n, int k, const double* L, int64_t ldl, double noi
  * s2 and divides by l). fp64 output, deterministic fixed-order reduction. */
 size_t gp_grad_forms_workspace_bytes(int64_t n_rows, int64_t n_cols, int d, int ard, int w);
 /* self_offset: row i of Xr is column i + self_offset of Xc (-1 = unrelated);
- * algo: 0 = auto (ARD with d + 2 <= 32 and w <= 112: per-dimension sums on the tensor
- *       core, grad_ard.cu; otherwise tcgen05 when d + 2 <= 32 and w <= 128, else SIMT),
- *       1 = SIMT, 2 = tcgen05 per-entry epilogue, 3 = tcgen05 ARD (as auto) */
+ * algo: 0 = auto (tcgen05 per-entry epilogue, grad_tc.cu, when d + 2 <= 32 and
+ *       w <= 128; ARD beyond that: per-dimension sums on the tensor core, grad_ard.cu;
+ *       else SIMT), 1 = SIMT, 2 = tcgen05 per-entry epilogue, 3 = tcgen05 ARD sums */
 int gp_grad_forms(int family, int d, int ard, const float* Xr, int64_t ldr, int64_t n_rows,
                   const float* Xc, int64_t ldc, int64_t n_cols, double outputscale,
                   const float* Y, int64_t ldy, const float* R, int64_t ldrr, int w,
                   int64_t self_offset, int algo, double* out, void* workspace,
                   size_t workspace_bytes, void* stream);
+
+/* Symmetric schedule of the same forms for the square training operator
+ * (rows = columns = X, likelihood.py:166-216): the caller passes Y, R with
+ * Y R^T SYMMETRIC (e.g. Y_s = [a/2 | -(S-W)/(4t) | -W/(4t) | L B^-1/(2 noise)],
+ * R_s = [a | W | S-W | L], so Y_s R_s^T = (H + H^T)/2 has the same sums
+ * against every symmetric dK/dtheta as H); each unordered 128 x 128 block
+ * pair is evaluated once, halving the kernel-entry work. Replaces the
+ * reference's run_row_blocks(grad_row_products) pass (likelihood.py:182-189). */
+size_t gp_grad_forms_sym_workspace_bytes(int64_t n, int d, int ard, int w);
+int gp_grad_forms_sym(int family, int d, int ard, const float* X, int64_t ldx, int64_t n, double outputscale,
+                      const float* Y, int64_t ldy, const float* R, int64_t ldrr, int w, double* out,
+                      void* workspace, size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

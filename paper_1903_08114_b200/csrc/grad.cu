@@ -188,10 +188,10 @@ size_t grad_ard_workspace(int64_t nr, int64_t nc, int d, int w);
 int grad_ard(int family, int d, const float* Xr, int64_t ldr, int64_t nr, const float* Xc, int64_t ldc, int64_t nc,
              const float* Y, int64_t ldy, const float* R, int64_t ldrr, int w, int64_t self_offset, double* out,
              void* ws, size_t ws_bytes, cudaStream_t st);
-size_t grad_tc_workspace(int64_t nr, int64_t nc, int d, int ard, int w);
+size_t grad_tc_workspace(int64_t nr, int64_t nc, int d, int ard, int w, bool sym = false);
 int grad_tc(int family, int d, int ard, const float* Xr, int64_t ldr, int64_t nr, const float* Xc,
             int64_t ldc, int64_t nc, const float* Y, int64_t ldy, const float* R, int64_t ldrr, int w,
-            int64_t self_offset, double* out, void* ws, size_t ws_bytes, cudaStream_t st);
+            int64_t self_offset, double* out, void* ws, size_t ws_bytes, cudaStream_t st, bool sym = false);
 
 static int grad_splits(int64_t nr, int64_t nc) {
   int64_t row_tiles = (nr + gBM - 1) / gBM;
@@ -213,7 +213,7 @@ size_t gp_grad_forms_workspace_bytes(int64_t n_rows, int64_t n_cols, int d, int 
   // SIMT: blocks = row_tiles * S with S <= ceil(2*SMs / row_tiles)
   int64_t row_tiles = (n_rows + gBM - 1) / gBM;
   size_t simt = (size_t)((row_tiles + 2LL * num_sms() + 1) * 17) * sizeof(double);
-  size_t tcw = grad_tc_supported(n_rows, n_cols, d, ard, w) ? grad_tc_workspace(n_rows, n_cols, d, ard, w) : 0;
+  size_t tcw = grad_tc_supported(n_rows, n_cols, d, ard, w) ? grad_tc_workspace(n_rows, n_cols, d, ard, w, false) : 0;
   size_t gaw = ard && grad_ard_supported(n_rows, n_cols, d, w) ? grad_ard_workspace(n_rows, n_cols, d, w) : 0;
   simt = simt > tcw ? simt : tcw;
   return simt > gaw ? simt : gaw;
@@ -233,12 +233,16 @@ int gp_grad_forms(int family, int d, int ard, const float* Xr, int64_t ldr, int6
     GP_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double) * nparams, st));
     return GP_OK;
   }
-  // ARD: per-dimension sums on the tensor core (grad_ard.cu); algo 2 forces
-  // the per-entry tcgen05 epilogue (grad_tc.cu), algo 1 the SIMT kernel
-  if (ard && (algo == 0 || algo == 3) && grad_ard_supported(n_rows, n_cols, d, w))
+  // default: the per-entry tcgen05 epilogue (grad_tc.cu, fp32 differences);
+  // ARD beyond its d + 2 <= 32 reach uses the tensor-core per-dimension sums
+  // (grad_ard.cu: the expansion x_i^2 - 2 x_i x_j + x_j^2 in bf16 two-term
+  // products loses digits to cancellation when lengthscales are short
+  // relative to the data spread: 5.5e-3 of max|g| at C2,
+  // scripts/c2_grad_check.py). algo 1 SIMT, 2 grad_tc, 3 grad_ard.
+  const bool tc_ok = grad_tc_supported(n_rows, n_cols, d, ard, w);
+  if (ard && (algo == 3 || (algo == 0 && !tc_ok)) && grad_ard_supported(n_rows, n_cols, d, w))
     return grad_ard(family, d, Xr, ldr, n_rows, Xc, ldc, n_cols, Y, ldy, R, ldrr, w, self_offset, out, workspace,
                     workspace_bytes, st);
-  const bool tc_ok = grad_tc_supported(n_rows, n_cols, d, ard, w);
   if (algo == 2 || (algo == 0 && tc_ok)) {
     GP_REQUIRE(tc_ok, "gp_grad_forms: shape unsupported by the tcgen05 kernel (d=%d w=%d)", d, w);
     return grad_tc(family, d, ard, Xr, ldr, n_rows, Xc, ldc, n_cols, Y, ldy, R, ldrr, w, self_offset, out,
@@ -282,6 +286,25 @@ int gp_grad_forms(int family, int d, int ard, const float* Xr, int64_t ldr, int6
     GP_LAUNCH_CHECK();
   }
   return GP_OK;
+}
+
+size_t gp_grad_forms_sym_workspace_bytes(int64_t n, int d, int ard, int w) {
+  if (grad_tc_supported(n, n, d, ard, w)) return grad_tc_workspace(n, n, d, ard, w, true);
+  return gp_grad_forms_workspace_bytes(n, n, d, ard, w);
+}
+
+int gp_grad_forms_sym(int family, int d, int ard, const float* X, int64_t ldx, int64_t n, double outputscale,
+                      const float* Y, int64_t ldy, const float* R, int64_t ldrr, int w, double* out,
+                      void* workspace, size_t workspace_bytes, void* stream) {
+  GP_REQUIRE(family == 0 || family == 1, "gp_grad_forms_sym: family %d", family);
+  GP_REQUIRE(d >= 1 && d <= 256 && w >= 1 && w <= 1024, "gp_grad_forms_sym: d=%d w=%d", d, w);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n > 0 && grad_tc_supported(n, n, d, ard, w))
+    return grad_tc(family, d, ard, X, ldx, n, X, ldx, n, Y, ldy, R, ldrr, w, 0, out, workspace, workspace_bytes, st,
+                   true);
+  // beyond the per-entry kernel's reach: the full square (same sum)
+  return gp_grad_forms(family, d, ard, X, ldx, n, X, ldx, n, outputscale, Y, ldy, R, ldrr, w, 0, 0, out,
+                       workspace, workspace_bytes, stream);
 }
 
 }  // extern "C"

@@ -38,7 +38,25 @@ struct GArgs {
   int row_tiles, col_tiles, splits, tiles_per_split, nstages;
   int64_t self_offset;
   double* partials;       // [gridDim.x][1 + G_MAXNL]
+  // symmetric schedule (square operator, Y R^T symmetric): items are
+  // (row tile, first column tile) pairs over the upper triangle of 128 x 128
+  // blocks (column tiles ct >= 2 rt); tiles off the diagonal block count twice
+  const int2* items;      // [n_items] or nullptr (rectangular: rt = it / splits)
+  int n_items;
 };
+
+// item -> row tile and column-tile range
+__device__ __forceinline__ void g_item(const GArgs& a, int it, int& rt, int& ct0, int& ct1) {
+  if (a.items) {
+    const int2 e = a.items[it];
+    rt = e.x;
+    ct0 = e.y;
+  } else {
+    rt = it / a.splits;
+    ct0 = (it - rt * a.splits) * a.tiles_per_split;
+  }
+  ct1 = min(a.col_tiles, ct0 + a.tiles_per_split);
+}
 
 // TMEM map: S_b at 64b, H_b at 128 + 64b, Y_hi at 256, Y_lo at 256 + WKP
 __device__ __forceinline__ uint32_t G_TS(uint32_t b) { return b * 64; }
@@ -94,16 +112,15 @@ __global__ void __launch_bounds__(G_NTHREADS, 1) grad_tc_kernel(const GArgs a) {
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t TY_HI = 256, TY_LO = 256 + a.WKP;
-  const int n_items = a.row_tiles * a.splits;
+  const int n_items = a.n_items;
 
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
       uint32_t s = 0, ph = 0, itc = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++itc) {
-        const int rt = it / a.splits, sp = it - rt * a.splits;
-        const int ct0 = sp * a.tiles_per_split;
-        const int ct1 = min(a.col_tiles, ct0 + a.tiles_per_split);
+        int rt, ct0, ct1;
+        g_item(a, it, rt, ct0, ct1);
         mbar_wait(smem_u32(xr_empty), (itc & 1) ^ 1);
         mbar_expect_tx(smem_u32(xr_full), row_bytes);
         bulk_g2s(smem_u32(xr_s), a.row_img + (int64_t)rt * (row_bytes / 4), row_bytes, smem_u32(xr_full));
@@ -136,9 +153,8 @@ __global__ void __launch_bounds__(G_NTHREADS, 1) grad_tc_kernel(const GArgs a) {
     const bool leader = elect_one();
     uint32_t s = 0, ph = 0, b = 0, bph = 0, itc = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++itc) {
-      const int sp = it % a.splits;
-      const int ct0 = sp * a.tiles_per_split;
-      const int ct1 = min(a.col_tiles, ct0 + a.tiles_per_split);
+      int rt, ct0, ct1;
+      g_item(a, it, rt, ct0, ct1);
       mbar_wait(smem_u32(xr_full), itc & 1);
       mbar_wait(smem_u32(y_full), itc & 1);
       tc_fence_after();
@@ -188,9 +204,8 @@ __global__ void __launch_bounds__(G_NTHREADS, 1) grad_tc_kernel(const GArgs a) {
     for (int p = 0; p < NP; ++p) acc64[p] = 0.0;
     uint32_t s = 0, ph = 0, b = 0, bph = 0, itc = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++itc) {
-      const int rt = it / a.splits, sp = it - rt * a.splits;
-      const int ct0 = sp * a.tiles_per_split;
-      const int ct1 = min(a.col_tiles, ct0 + a.tiles_per_split);
+      int rt, ct0, ct1;
+      g_item(a, it, rt, ct0, ct1);
       const int64_t row = (int64_t)rt * GBM + q * 32 + lane;
       // ---- Y rows -> TMEM (half 0: hi, half 1: lo); previous item's H MMAs must be done
       mbar_wait(smem_u32(y_empty), (itc & 1) ^ 1);
@@ -284,8 +299,11 @@ __global__ void __launch_bounds__(G_NTHREADS, 1) grad_tc_kernel(const GArgs a) {
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
         }
+        // symmetric schedule: a tile outside the diagonal 128 x 128 block
+        // stands for itself and its mirror
+        const double wt = (a.items && ct >= 2 * rt + 2) ? 2.0 : 1.0;
 #pragma unroll
-        for (int p = 0; p < NP; ++p) acc64[p] += (double)acc[p];
+        for (int p = 0; p < NP; ++p) acc64[p] += wt * (double)acc[p];
         if (++s == (uint32_t)NS) { s = 0; ph ^= 1; }
         if (++b == 2) { b = 0; bph ^= 1; }
       }
@@ -353,6 +371,31 @@ __global__ void col_xy_kernel(const float* __restrict__ X, int64_t ldx, int64_t 
   img[idx] = (row < n && k < d) ? X[row * ldx + k] : 0.f;
 }
 
+// the symmetric schedule's item table, in row-tile order: row tile rt owns
+// ceil((col_tiles - 2 rt) / tps) items starting at column tiles 2 rt + k tps
+// (one block: per-thread row ranges, then an exclusive scan of their counts)
+__global__ void sym_items_kernel(int row_tiles, int col_tiles, int tps, int2* items) {
+  __shared__ int cnt[1024];
+  const int per = (row_tiles + blockDim.x - 1) / blockDim.x;
+  const int r0 = min(row_tiles, (int)threadIdx.x * per), r1 = min(row_tiles, r0 + per);
+  int c = 0;
+  for (int rt = r0; rt < r1; ++rt) c += (col_tiles - 2 * rt + tps - 1) / tps;
+  cnt[threadIdx.x] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int t = 0; t < (int)blockDim.x; ++t) {
+      const int v = cnt[t];
+      cnt[t] = acc;
+      acc += v;
+    }
+  }
+  __syncthreads();
+  int k = cnt[threadIdx.x];
+  for (int rt = r0; rt < r1; ++rt)
+    for (int ct = 2 * rt; ct < col_tiles; ct += tps) items[k++] = make_int2(rt, ct);
+}
+
 __global__ void grad_tc_finalize(const double* __restrict__ partials, int nblocks, int p0, int nl,
                                  int with_s2, double* out) {
   int p = threadIdx.x;
@@ -364,11 +407,11 @@ __global__ void grad_tc_finalize(const double* __restrict__ partials, int nblock
 }
 
 struct GPlan {
-  int DK, WK, WKP, DP, row_tiles, col_tiles, splits, tiles_per_split, nstages, grid;
-  size_t row_img, col_img, r_img, y_rows, col_xy, partials, smem;
+  int DK, WK, WKP, DP, row_tiles, col_tiles, splits, tiles_per_split, nstages, grid, n_items;
+  size_t row_img, col_img, r_img, y_rows, col_xy, partials, items, smem;
 };
 
-static GPlan gplan(int64_t nr, int64_t nc, int d, int ard, int w) {
+static GPlan gplan(int64_t nr, int64_t nc, int d, int ard, int w, bool sym = false) {
   GPlan p;
   p.DK = (d + 2 + 7) / 8 * 8;
   p.WK = (w + 7) / 8 * 8;
@@ -382,7 +425,21 @@ static GPlan gplan(int64_t nr, int64_t nc, int d, int ard, int w) {
                                                       (int64_t)p.col_tiles}));
   p.tiles_per_split = (int)((p.col_tiles + s - 1) / s);
   p.splits = (p.col_tiles + p.tiles_per_split - 1) / p.tiles_per_split;
-  p.grid = std::min(p.row_tiles * p.splits, num_sms());
+  p.n_items = p.row_tiles * p.splits;
+  p.items = 0;
+  if (sym) {
+    // upper triangle: row tile rt takes column tiles [2 rt, col_tiles), in
+    // pieces of tiles_per_split (about 4 items per SM in total)
+    int64_t total = 0;
+    for (int rt = 0; rt < p.row_tiles; ++rt) total += p.col_tiles - 2 * rt;
+    p.tiles_per_split = (int)std::max<int64_t>(1, std::min<int64_t>(p.col_tiles, total / (4LL * num_sms())));
+    int64_t ni = 0;
+    for (int rt = 0; rt < p.row_tiles; ++rt) ni += (p.col_tiles - 2 * rt + p.tiles_per_split - 1) / p.tiles_per_split;
+    p.n_items = (int)ni;
+    p.splits = 0;
+    p.items = (size_t)ni * sizeof(int2);
+  }
+  p.grid = std::min(p.n_items, num_sms());
   p.row_img = (size_t)p.row_tiles * 2 * GBM * p.DK * 4;
   p.col_img = (size_t)p.col_tiles * 2 * GBN * p.DK * 4;
   p.r_img = (size_t)p.col_tiles * 2 * GBN * p.WK * 4;
@@ -407,18 +464,21 @@ bool grad_tc_supported(int64_t nr, int64_t nc, int d, int ard, int w) {
   return p.nstages >= 2 && 2 * p.WKP <= 256;
 }
 
-size_t grad_tc_workspace(int64_t nr, int64_t nc, int d, int ard, int w) {
-  tc::GPlan p = tc::gplan(nr, nc, d, ard, w);
+size_t grad_tc_workspace(int64_t nr, int64_t nc, int d, int ard, int w, bool sym) {
+  tc::GPlan p = tc::gplan(nr, nc, d, ard, w, sym);
   return tc::al256(p.row_img) + tc::al256(p.col_img) + tc::al256(p.r_img) + tc::al256(p.y_rows) +
-         tc::al256(p.col_xy) + tc::al256(p.partials) + 256 * sizeof(double);
+         tc::al256(p.col_xy) + tc::al256(p.partials) + tc::al256(p.items) + 256 * sizeof(double);
 }
 
+// sym: the square operator (Xr = Xc, self_offset 0) with Y R^T symmetric;
+// only the upper triangle of 128 x 128 blocks is evaluated (half the entries)
 int grad_tc(int family, int d, int ard, const float* Xr, int64_t ldr, int64_t nr, const float* Xc,
             int64_t ldc, int64_t nc, const float* Y, int64_t ldy, const float* R, int64_t ldrr, int w,
-            int64_t self_offset, double* out, void* ws, size_t ws_bytes, cudaStream_t st) {
+            int64_t self_offset, double* out, void* ws, size_t ws_bytes, cudaStream_t st, bool sym) {
   using namespace tc;
-  GPlan p = gplan(nr, nc, d, ard, w);
-  GP_REQUIRE(ws_bytes >= grad_tc_workspace(nr, nc, d, ard, w), "gp_grad_forms(tcgen05): workspace too small");
+  GP_REQUIRE(!sym || (nr == nc && self_offset == 0), "gp_grad_forms_sym: square operator only");
+  GPlan p = gplan(nr, nc, d, ard, w, sym);
+  GP_REQUIRE(ws_bytes >= grad_tc_workspace(nr, nc, d, ard, w, sym), "gp_grad_forms(tcgen05): workspace too small");
   char* wp = static_cast<char*>(ws);
   float* row_img = reinterpret_cast<float*>(wp); wp += al256(p.row_img);
   float* col_img = reinterpret_cast<float*>(wp); wp += al256(p.col_img);
@@ -426,7 +486,12 @@ int grad_tc(int family, int d, int ard, const float* Xr, int64_t ldr, int64_t nr
   float* y_rows = reinterpret_cast<float*>(wp); wp += al256(p.y_rows);
   float* col_xy = reinterpret_cast<float*>(wp); wp += al256(p.col_xy);
   double* partials = reinterpret_cast<double*>(wp); wp += al256(p.partials);
+  int2* items = reinterpret_cast<int2*>(wp); wp += al256(p.items);
   double* mean = reinterpret_cast<double*>(wp);
+  if (sym) {
+    sym_items_kernel<<<1, 1024, 0, st>>>(p.row_tiles, p.col_tiles, p.tiles_per_split, items);
+    GP_LAUNCH_CHECK();
+  }
   const double c = family == GP_FAMILY_RBF ? 1.4426950408889634 : -6.0;
   if (int rc = distance_images(Xr, ldr, nr, Xc, ldc, nc, d, p.DK, GBM, GBN, c, mean, row_img, col_img, st))
     return rc;
@@ -450,6 +515,8 @@ int grad_tc(int family, int d, int ard, const float* Xr, int64_t ldr, int64_t nr
   a.n_rows = nr; a.n_cols = nc; a.row_tiles = p.row_tiles; a.col_tiles = p.col_tiles;
   a.splits = p.splits; a.tiles_per_split = p.tiles_per_split; a.nstages = p.nstages;
   a.self_offset = self_offset; a.partials = partials;
+  a.items = sym ? items : nullptr;
+  a.n_items = p.n_items;
   const int nchunks = ard ? (d + G_MAXNL - 1) / G_MAXNL : 1;
   for (int ch = 0; ch < nchunks; ++ch) {
     a.p0 = ch * G_MAXNL;

@@ -142,6 +142,34 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t x, uint32_t y, ui
                : "memory");
 }
 
+// mbarrier waits with a suspend-time hint (ns): the waiting thread sleeps
+// until the phase completes (or the hint expires) instead of re-polling,
+// which keeps SYNCS traffic out of the MIO queue the kappa warps' MUFU work
+// shares. P: producers and drain (off the critical path), C: MMA and kappa.
+#ifndef GP_SYM_HINT_P
+#define GP_SYM_HINT_P 1000000
+#endif
+#ifndef GP_SYM_HINT_C
+#define GP_SYM_HINT_C 0
+#endif
+__device__ __forceinline__ void mbar_wait_hint(uint32_t bar, uint32_t parity, uint32_t ns) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity), "r"(ns)
+      : "memory");
+}
+__device__ __forceinline__ void wait_p(uint32_t bar, uint32_t parity) {
+  if (GP_SYM_HINT_P) mbar_wait_hint(bar, parity, GP_SYM_HINT_P);
+  else mbar_wait(bar, parity);
+}
+__device__ __forceinline__ void wait_c(uint32_t bar, uint32_t parity) {
+  if (GP_SYM_HINT_C) mbar_wait_hint(bar, parity, GP_SYM_HINT_C);
+  else mbar_wait(bar, parity);
+}
+
 // item L -> block pair (P, Q), P <= Q, in row-major upper-triangular order:
 // start(P) = P NB - P (P - 1) / 2 <= L < start(P + 1)
 __device__ __forceinline__ void pair_of(int L, int NB, int& P, int& Q) {
@@ -292,13 +320,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
         const int J = it.J();
         // column slot cs holds tile Tn with Tn & 1 == cs (two slots), and the
         // distance product that reads it commits s_full[cs]: wait on that
-        mbar_wait(smem_u32(NSC == 2 ? &s_full[cs] : &cempty[cs]), cph ^ 1);
+        wait_p(smem_u32(NSC == 2 ? &s_full[cs] : &cempty[cs]), cph ^ 1);
         mbar_expect_tx(smem_u32(&cfull[cs]), img_bytes);
         bulk_g2s(smem_u32(cring + cs * img_bytes), a.col_img + (int64_t)J * img_f, img_bytes, smem_u32(&cfull[cs]));
         if (++cs == (uint32_t)NSC) { cs = 0; cph ^= 1; }
         // with a 2-deep V ring, slot vs is freed by the direct product of the
         // tile that used S/K buffer vs: wait on that release, no extra commit
-        mbar_wait(smem_u32(NSV == 2 ? &sk_empty[vs] : &vempty[vs]), vph ^ 1);
+        wait_p(smem_u32(NSV == 2 ? &sk_empty[vs] : &vempty[vs]), vph ^ 1);
         mbar_expect_tx(smem_u32(&vfull[vs]), V_TILE_BYTES);
         bulk_g2s(smem_u32(vring + vs * V_TILE_BYTES), a.v_img + (int64_t)J * vt_h, V_TILE_BYTES,
                  smem_u32(&vfull[vs]));
@@ -317,11 +345,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       const uint32_t img_f = img_bytes / 4, vt_h = V_TILE_BYTES / 2;
       while (it.ok) {
         const int I = it.I();
-        if (R >= 1) mbar_wait(smem_u32(xr_empty), (R - 1) & 1);
+        if (R >= 1) wait_p(smem_u32(xr_empty), (R - 1) & 1);
         mbar_expect_tx(smem_u32(xr_full), img_bytes);
         bulk_g2s(smem_u32(xr_s), a.row_img + (int64_t)I * img_f, img_bytes, smem_u32(xr_full));
         const uint32_t vb = R & 1, u = R >> 1;
-        if (u >= 1) mbar_wait(smem_u32(&vi_empty[vb]), (u - 1) & 1);
+        if (u >= 1) wait_p(smem_u32(&vi_empty[vb]), (u - 1) & 1);
         mbar_expect_tx(smem_u32(&vi_full[vb]), V_TILE_BYTES);
         bulk_g2s(smem_u32(vi_s + vb * V_TILE_BYTES), a.v_img + (int64_t)I * vt_h, V_TILE_BYTES,
                  smem_u32(&vi_full[vb]));
@@ -361,11 +389,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
     it.begin(a);
     auto dist = [&](const TileSeq& tt, uint32_t Tn) {
       const uint32_t b = Tn & 1;
-      if (Tn >= 2) SYM_T(0, mbar_wait(smem_u32(&sk_empty[b]), ((Tn >> 1) - 1) & 1));
+      if (Tn >= 2) SYM_T(0, wait_c(smem_u32(&sk_empty[b]), ((Tn >> 1) - 1) & 1));
       if (tt.first_in_row()) {
         // new row: row image SMEM -> TMEM buffer R & 1 (tcgen05.cp, in the
         // tensor pipe ahead of this row's distance products)
-        SYM_T(1, mbar_wait(smem_u32(xr_full), R & 1));
+        SYM_T(1, wait_c(smem_u32(xr_full), R & 1));
         tc_fence_after();
         if (leader) {
           for (int part = 0; part < 2; ++part)
@@ -379,7 +407,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
         ++R;
       }
       const uint32_t xb = (R - 1) & 1;
-      SYM_T(2, mbar_wait(smem_u32(&cfull[cs]), cph));
+      SYM_T(2, wait_c(smem_u32(&cfull[cs]), cph));
       tc_fence_after();
       if (leader) {
         const uint32_t d_tm = tmem + TSK(b);
@@ -407,26 +435,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       if (it.first_in_row()) {
         ++rowc;
         // O_I buffer rowc & 1 was last used by row rowc - 2
-        if (rowc >= 2) SYM_T(3, mbar_wait(smem_u32(&oi_empty[rowc & 1]), ((rowc >> 1) - 1) & 1));
+        if (rowc >= 2) SYM_T(3, wait_c(smem_u32(&oi_empty[rowc & 1]), ((rowc >> 1) - 1) & 1));
       }
       if (K >= 1) {
         // O_J[c] of the previous item must be read before tile (0, c) of this
         // one; columns this item does not have are waited for at its end, so
         // every oj_empty phase is consumed once per item
-        if (it.r == 0) SYM_T(3, mbar_wait(smem_u32(&oj_empty[it.c]), (K - 1) & 1));
+        if (it.r == 0) SYM_T(3, wait_c(smem_u32(&oj_empty[it.c]), (K - 1) & 1));
         if (it.last_in_item())
-          for (int cc = it.cols_in; cc < RB; ++cc) mbar_wait(smem_u32(&oj_empty[cc]), (K - 1) & 1);
+          for (int cc = it.cols_in; cc < RB; ++cc) wait_c(smem_u32(&oj_empty[cc]), (K - 1) & 1);
       }
-      SYM_T(4, mbar_wait(smem_u32(&k_full[b]), (T >> 1) & 1));
+      SYM_T(4, wait_c(smem_u32(&k_full[b]), (T >> 1) & 1));
       SYM_COUNT();
-      SYM_T(5, mbar_wait(smem_u32(&vfull[vs]), vph));
+      SYM_T(5, wait_c(smem_u32(&vfull[vs]), vph));
       const bool mir = it.mirror();
       // V_I is loaded for every row; a row of a diagonal item whose only tile
       // is the diagonal one has no mirror product, but its load must still be
       // awaited before vi_empty is committed (no bulk copy may be in flight
       // when the barrier is re-armed or the CTA exits)
       if (mir || (it.first_in_row() && it.last_in_row()))
-        SYM_T(5, mbar_wait(smem_u32(&vi_full[rowc & 1]), (rowc >> 1) & 1));
+        SYM_T(5, wait_c(smem_u32(&vi_full[rowc & 1]), (rowc >> 1) & 1));
       tc_fence_after();
       if (leader) {
         // direct first, then release the S/K buffer: the mirror reads only
@@ -479,7 +507,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
     uint32_t T = 0, Mt = 0;   // tiles, mirror tiles
     while (it.ok) {
       const uint32_t b = T & 1;
-      SYM_T(0, mbar_wait(smem_u32(&s_full[b]), (T >> 1) & 1));
+      SYM_T(0, wait_c(smem_u32(&s_full[b]), (T >> 1) & 1));
       SYM_COUNT();
       tc_fence_after();
       const uint32_t sk = tmem + lane_base + TSK(b) + 32u * ch;
@@ -520,7 +548,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       if (mir) {
         // K^T operand: 8 consecutive j of point i = one 16-byte core-matrix row
         // the previous mirror tile's products have read the SMEM K
-        if (Mt >= 1) SYM_T(2, mbar_wait(smem_u32(ks_empty), (Mt - 1) & 1));
+        if (Mt >= 1) SYM_T(2, wait_c(smem_u32(ks_empty), (Mt - 1) & 1));
         ++Mt;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
@@ -596,7 +624,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
     while (itm.ok) {
       const int P = itm.P, Q = itm.Q, rows_in = itm.rows_in, cols_in = itm.cols_in;
       for (int r = 0; r < rows_in; ++r) {
-        SYM_T(2, mbar_wait(smem_u32(&oi_full[Rd & 1]), (Rd >> 1) & 1));
+        SYM_T(2, wait_p(smem_u32(&oi_full[Rd & 1]), (Rd >> 1) & 1));
         tc_fence_after();
         uint32_t o[32];
         tmem_ld32(tmem + lane_base + TOI(Rd & 1), o);
@@ -616,7 +644,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
           ar[j ^ sw] = x;
         }
       }
-      SYM_T(3, mbar_wait(smem_u32(oj_full), K & 1));
+      SYM_T(3, wait_p(smem_u32(oj_full), K & 1));
       SYM_COUNT();
       tc_fence_after();
       for (int cc = 0; cc < RB; ++cc) {

@@ -169,11 +169,53 @@ def gradient_operands(a, S, W, cache):
     return Y, R
 
 
+def symmetric_gradient_operands(a, S, W, cache):
+    """fp32 (Y_s, R_s) with Y_s R_s^T = (H + H^T)/2 for the H = Y R^T of
+    gradient_operands: only the probe block is asymmetric, so it appears
+    twice with half the weight. Every dK/dtheta is symmetric, so the forms
+    against H_s equal those against H while the kernel sums each unordered
+    pair of points once (gp_grad_forms_sym)."""
+    T = D.torch()
+    t = W.shape[1]
+    if cache is not None:
+        D_ = S - W
+        Yc = [0.5 * a[:, None], -D_ / (4.0 * t), -W / (4.0 * t)]
+        Rc = [a[:, None], W, D_]
+        if cache.rank:
+            LB = _ops.lowrank_mul(cache.factor_device, cache.binv_device)
+            Yc.append(LB / (2.0 * cache.noise))
+            Rc.append(cache.factor_device)
+    else:
+        Yc = [0.5 * a[:, None], -S / (4.0 * t), -W / (4.0 * t)]
+        Rc = [a[:, None], W, S]
+    Y = T.cat(Yc, dim=1).to(T.float32).contiguous()
+    R = T.cat(Rc, dim=1).to(T.float32).contiguous()
+    return Y, R
+
+
+def _grad_forms_sym_raw(model, d, Xs32, Y, R):
+    """Raw forms over the square operator with the symmetric schedule
+    (csrc/grad_tc.cu, gp_grad_forms_sym)."""
+    T = D.torch()
+    ard = 1 if model.ard else 0
+    npar = 1 + (d if ard else 1)
+    out = T.zeros(npar, dtype=T.float64, device=D.device())
+    lib = _lib.lib()
+    n, w = Xs32.shape[0], Y.shape[1]
+    nbytes = lib.gp_grad_forms_sym_workspace_bytes(n, d, ard, w)
+    ws = _ops.workspace().bytes("grad", nbytes)
+    _lib.check(lib.gp_grad_forms_sym(model.family_code, d, ard, _lib.ptr(Xs32), Xs32.stride(0), n,
+                                     float(model.outputscale), _lib.ptr(Y), Y.stride(0), _lib.ptr(R),
+                                     R.stride(0), w, _lib.ptr(out), _lib.ptr(ws), nbytes,
+                                     _lib.stream_handle()), "gp_grad_forms_sym")
+    return out
+
+
 def _gradients(model: KernelModel, ps, a, S, W, cache) -> dict:
     n, t = W.shape
     Xs32, _ = ps.scaled(model.scale_for(ps.d))
-    Y, R = gradient_operands(a, S, W, cache)
-    raw = _grad_forms_raw(model, ps.d, Xs32, Xs32, Y, R)
+    Y, R = symmetric_gradient_operands(a, S, W, cache)
+    raw = _grad_forms_sym_raw(model, ps.d, Xs32, Y, R)
     return assemble_gradients(model, raw, a, S, W, cache, n)
 
 

@@ -95,6 +95,17 @@ def main():
         gg = L.assemble_gradients(md, raw, cap["a"], cap["S"], cap["W"], cap["cache"], w.n)
         err = max(abs(gg[k] - dn[k][0]) for k in dn) / np.abs(g["grad_vals"]).max()
         print(f"algo {algo}: {e0.elapsed_time(e1):.2f} ms, max |g - dense64| / max|g| = {err:.2e}")
+    Ys, Rs = L.symmetric_gradient_operands(cap["a"], cap["S"], cap["W"], cap["cache"])
+    L._grad_forms_sym_raw(md, ps.d, Xs32, Ys, Rs)
+    T.cuda.synchronize()
+    e0, e1 = T.cuda.Event(enable_timing=True), T.cuda.Event(enable_timing=True)
+    e0.record()
+    raw = L._grad_forms_sym_raw(md, ps.d, Xs32, Ys, Rs)
+    e1.record()
+    T.cuda.synchronize()
+    gg = L.assemble_gradients(md, raw, cap["a"], cap["S"], cap["W"], cap["cache"], w.n)
+    err = max(abs(gg[k] - dn[k][0]) for k in dn) / np.abs(g["grad_vals"]).max()
+    print(f"symmetric grad_tc: {e0.elapsed_time(e1):.2f} ms, max |g - dense64| / max|g| = {err:.2e}")
     mx = np.abs(g["grad_vals"]).max()
     print(f"{'param':>14} {'reference':>12} {'fused':>12} {'simt':>12} {'dense64':>12}  quad exact resid")
     for k in keys:

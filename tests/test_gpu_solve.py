@@ -229,6 +229,55 @@ def test_grad_forms_tcgen05_vs_simt(fam, ard, d, w):
         np.testing.assert_allclose(c0 + c1, a, rtol=0, atol=1e-4 * scale + 1e-9)
 
 
+@pytest.mark.parametrize("fam,ard,d,n", [("matern32", True, 11, 3000), ("rbf", False, 3, 1000),
+                                         ("matern32", True, 5, 129), ("rbf", True, 8, 128),
+                                         ("matern32", False, 2, 64), ("rbf", True, 4, 1),
+                                         ("matern32", True, 20, 700)])
+def test_symmetric_gradient_schedule_matches_full_square(fam, ard, d, n):
+    """gp_grad_forms_sym (upper triangle of 128 x 128 blocks, off-diagonal
+    blocks weighted twice) equals the full-square SIMT pass for a symmetric
+    Y_s R_s^T = (Y R^T + R Y^T)/2, incl. ragged n and the diagonal blocks."""
+    import torch
+    from paper_1903_08114_b200 import _device as D
+    rng = np.random.default_rng(n + d)
+    w = 24
+    X = rng.standard_normal((n, d))
+    ls = np.linspace(0.3, 0.9, d) if ard else np.array([0.6])
+    m = gp.KernelModel(fam, 1.2, ls, 0.3)
+    Xs32, _ = D.points(X).scaled(ls)
+    Y = torch.from_numpy(rng.standard_normal((n, w))).float().cuda()
+    R = torch.from_numpy(rng.standard_normal((n, w))).float().cuda()
+    full = likelihood._grad_forms_raw(m, d, Xs32, Xs32, Y, R, 0, algo=1).cpu().numpy()
+    Ys = torch.cat([0.5 * Y, 0.5 * R], dim=1).contiguous()
+    Rs = torch.cat([R, Y], dim=1).contiguous()
+    sym = likelihood._grad_forms_sym_raw(m, d, Xs32, Ys, Rs).cpu().numpy()
+    scale = np.abs(full).max()
+    np.testing.assert_allclose(sym, full, rtol=0, atol=2e-5 * scale + 1e-9)
+
+
+def test_gradient_pass_short_lengthscales_c2():
+    """At C2 (d = 8, lengthscales short against the whitened spread) the MLL's
+    gradient pass agrees with the fp64-reduction SIMT pass to 1e-5 of the
+    largest form (the ARD tensor-core expansion lost 5.5e-3 here and is no
+    longer the default, scripts/c2_grad_check.py)."""
+    import torch
+    from paper_1903_08114_b200 import _device as D, synthetic as syn
+    w_ = syn.WORKLOADS["C2"]
+    X = syn.whitened_inputs(w_.n, w_.d, 0)
+    m = gp.KernelModel(w_.family, syn.OUTPUTSCALE, w_.lengthscales(), syn.NOISE)
+    Xs32, _ = D.points(X).scaled(m.lengthscales)
+    rng = np.random.default_rng(5)
+    Y = torch.from_numpy(rng.standard_normal((w_.n, 16)) / w_.n).float().cuda()
+    R = torch.from_numpy(rng.standard_normal((w_.n, 16))).float().cuda()
+    ref = likelihood._grad_forms_raw(m, w_.d, Xs32, Xs32, Y, R, 0, algo=1).cpu().numpy()
+    auto = likelihood._grad_forms_raw(m, w_.d, Xs32, Xs32, Y, R, 0, algo=0).cpu().numpy()
+    sym = likelihood._grad_forms_sym_raw(m, w_.d, Xs32, torch.cat([0.5 * Y, 0.5 * R], 1).contiguous(),
+                                         torch.cat([R, Y], 1).contiguous()).cpu().numpy()
+    scale = np.abs(ref).max()
+    np.testing.assert_allclose(auto, ref, rtol=0, atol=1e-5 * scale)
+    np.testing.assert_allclose(sym, ref, rtol=0, atol=1e-5 * scale)
+
+
 @pytest.mark.parametrize("tol,its", [(1e-300, 12), (1e-3, 200)])
 def test_wide_block_woodbury_matches_narrow_chunks(tol, its):
     """t >= 32 takes the register-tiled Woodbury kernels (cg_precond_z_wide,
