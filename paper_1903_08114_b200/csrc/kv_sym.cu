@@ -170,17 +170,78 @@ __device__ __forceinline__ void wait_c(uint32_t bar, uint32_t parity) {
   else mbar_wait(bar, parity);
 }
 
-// item L -> block pair (P, Q), P <= Q, in row-major upper-triangular order:
-// start(P) = P NB - P (P - 1) / 2 <= L < start(P + 1)
+// row-major upper triangle of an m x m block: local index l -> (p, q), p <= q,
+// start(p) = p m - p (p - 1) / 2 <= l < start(p + 1)
+__device__ __forceinline__ void tri_pair(int l, int m, int& p, int& q) {
+  const double b2 = 2.0 * m + 1.0;
+  int x = (int)floor((b2 - sqrt(b2 * b2 - 8.0 * (double)l)) * 0.5);
+  x = max(0, min(m - 1, x));
+  auto start = [&](int y) { return (long long)y * m - (long long)y * (y - 1) / 2; };
+  while (x > 0 && start(x) > l) --x;
+  while (x + 1 < m && start(x + 1) <= l) ++x;
+  p = x;
+  q = x + (int)(l - start(x));
+}
+
+// Item order: block pairs are grouped into bands of SB = 128 row blocks (SB x SB
+// super-items (U, V), U <= V, row-major; inside one, row-major pairs). The
+// ~150 chunks in flight then touch two bands of the fixed-point sums and
+// one band of column / V images (a few MB, L2-resident) instead of sweeping
+// all n columns per row block (which streamed the 88 MB sums and the
+// 190 MB images through DRAM: 202 GB per n = 10^6 launch). With NB <= SB
+// this is the plain row-major triangle.
+#ifndef GP_SYM_SB
+#define GP_SYM_SB 128
+#endif
+constexpr int SB = GP_SYM_SB;
 __device__ __forceinline__ void pair_of(int L, int NB, int& P, int& Q) {
-  const double b2 = 2.0 * NB + 1.0;
-  int p = (int)floor((b2 - sqrt(b2 * b2 - 8.0 * (double)L)) * 0.5);
-  p = max(0, min(NB - 1, p));
-  auto start = [&](int x) { return (long long)x * NB - (long long)x * (x - 1) / 2; };
-  while (p > 0 && start(p) > L) --p;
-  while (p + 1 < NB && start(p + 1) <= L) ++p;
-  P = p;
-  Q = p + (int)(L - start(p));
+  const int nb = (NB + SB - 1) / SB;
+  auto rows = [&](int b) { return min(SB, NB - b * SB); };
+  long long l = L;
+  int U = 0;
+  for (; U < nb - 1; ++U) {
+    const long long r = rows(U);
+    const long long row_items = r * (r + 1) / 2 + r * (long long)(NB - (U + 1) * SB);
+    if (l < row_items) break;
+    l -= row_items;
+  }
+  const int ru = rows(U);
+  const long long tri = (long long)ru * (ru + 1) / 2;
+  if (l < tri) {
+    int p, q;
+    tri_pair((int)l, ru, p, q);
+    P = U * SB + p;
+    Q = U * SB + q;
+    return;
+  }
+  l -= tri;
+  // off-diagonal super-items (U, V > U): ru x rows(V), all full but the last
+  const long long full = (long long)ru * SB;
+  int V = U + 1 + (int)(l / full);
+  long long lv = l - (long long)(V - U - 1) * full;
+  if (V >= nb) { V = nb - 1; lv = l - (long long)(V - U - 1) * full; }
+  const int rv = rows(V);
+  P = U * SB + (int)(lv / rv);
+  Q = V * SB + (int)(lv % rv);
+}
+
+// (P, Q) of item L + 1 from that of item L (the order of pair_of)
+__device__ __forceinline__ void step_pair(int NB, int& P, int& Q) {
+  const int U = P / SB, V = Q / SB;
+  const int q_end = min(NB, (V + 1) * SB);
+  if (Q + 1 < q_end) { ++Q; return; }
+  const int p_end = min(NB, (U + 1) * SB);
+  if (P + 1 < p_end) {   // next row of the super-item (on the diagonal one it starts at Q = P)
+    ++P;
+    Q = U == V ? P : V * SB;
+    return;
+  }
+  if (q_end < NB) {      // next super-item of the band row
+    P = U * SB;
+    Q = q_end;
+    return;
+  }
+  P = Q = (U + 1) * SB;  // next band row, its diagonal super-item
 }
 
 // The tile sequence of one CTA (every role walks the same sequence): chunks
@@ -193,6 +254,9 @@ struct TileSeq {
   bool ok;
   __device__ void set_item() {
     pair_of(L, NB, P, Q);
+    set_pair();
+  }
+  __device__ void set_pair() {
     rows_in = min(RB, tiles - RB * P);
     cols_in = min(RB, tiles - RB * Q);
     r = 0;
@@ -210,11 +274,13 @@ struct TileSeq {
   __device__ void next_item() {
     if (++i < CH && CH * k + i < n_items) {
       ++L;
-    } else {
-      k += G;
-      i = 0;
-      L = CH * k;
+      step_pair(NB, P, Q);   // the next item of the chunk: O(1), no pair_of
+      set_pair();
+      return;
     }
+    k += G;
+    i = 0;
+    L = CH * k;
     ok = L < n_items;
     if (ok) set_item();
   }
