@@ -534,15 +534,157 @@ __global__ void lowrank_kernel(int64_t n, int k, const double* __restrict__ L, i
   }
 }
 
+// Y = beta Y + alpha L M for wide M (t >= 32): 64 x 64 output tile per block,
+// 4 x 4 per thread, the tile's L rows (transposed) and M columns staged in
+// SMEM (the GEMM-shaped Woodbury products of the 256-column variance solves
+// and of the gradient operands L B^-1)
+__global__ void __launch_bounds__(256) lowrank_wide(int64_t n, int k, const double* __restrict__ L, int64_t ldl,
+                                                    const double* __restrict__ M, int64_t ldm, int t, double alpha,
+                                                    double beta, double* Y, int64_t ldy) {
+  extern __shared__ __align__(16) double dsm[];
+  double* sM = dsm;                    // [k][kWT]
+  double* sL = sM + (size_t)k * kWT;   // [k][kWLS]
+  const int c0 = blockIdx.y * kWT;
+  const int64_t rb = (int64_t)blockIdx.x * kWT;
+  const int nr = (int)min((int64_t)kWT, n - rb);
+  for (int p = threadIdx.x; p < k * kWT; p += 256) {
+    const int kk = p / kWT, c = p - kk * kWT;
+    sM[p] = c0 + c < t ? M[kk * ldm + c0 + c] : 0.0;
+  }
+  for (int p = threadIdx.x; p < kWT * k; p += 256) {
+    const int r = p / k, kk = p - r * k;
+    sL[kk * kWLS + r] = r < nr ? L[(rb + r) * ldl + kk] : 0.0;
+  }
+  __syncthreads();
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  for (int kk = 0; kk < k; ++kk) {
+    const double2 la = *reinterpret_cast<const double2*>(sL + kk * kWLS + 4 * ty);
+    const double2 lb = *reinterpret_cast<const double2*>(sL + kk * kWLS + 4 * ty + 2);
+    const double2 ma = *reinterpret_cast<const double2*>(sM + kk * kWT + 4 * tx);
+    const double2 mb = *reinterpret_cast<const double2*>(sM + kk * kWT + 4 * tx + 2);
+    const double l[4] = {la.x, la.y, lb.x, lb.y}, m[4] = {ma.x, ma.y, mb.x, mb.y};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = fma(l[i], m[j], acc[i][j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int rl = 4 * ty + i;
+    if (rl >= nr) continue;
+    const int64_t r = rb + rl;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = c0 + 4 * tx + j;
+      if (c >= t) continue;
+      const double y = beta == 0.0 ? 0.0 : beta * Y[r * ldy + c];
+      Y[r * ldy + c] = y + alpha * acc[i][j];
+    }
+  }
+}
+
 // In-place Cholesky of B = noise I + G (G = L^T L, k x k, row-major, lower
-// result), then Binv = B^{-1} = C^{-T} C^{-1}; out[0] = 2 sum log C_jj,
-// out[1] = tr(B^{-1}) (precond.py:114-122, :165-174). Single block.
-__global__ void precond_factor_kernel(int k, double noise, double* C, double* Binv, double* out,
-                                      int* info) {
+// result), then X = C^{-1} (lower) into Binv (xtx_kernel forms B^{-1} =
+// X^T X); out[0] = 2 sum log C_jj, out[1] = tr(B^{-1}) = ||X||_F^2
+// (precond.py:114-122, :165-174). Single block, the k x k matrix in shared
+// memory (k <= 160), so the k column steps and the substitution run at SMEM
+// latency; C is written back for the caller.
+__global__ void __launch_bounds__(1024) precond_factor_kernel(int k, double noise, double* C, double* Binv,
+                                                              double* out, int* info) {
+  extern __shared__ double Cs[];   // [k][k]
+  __shared__ int fail;
+  __shared__ double sred[1024];
+  if (threadIdx.x == 0) fail = 0;
+  for (int p = threadIdx.x; p < k * k; p += blockDim.x) {
+    const int i = p / k, j = p - i * k;
+    Cs[p] = C[p] + (i == j ? noise : 0.0);
+  }
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
+    if (threadIdx.x == 0) {
+      const double djj = Cs[j * k + j];
+      if (!(djj > 0.0) || !isfinite(djj)) fail = 1;
+      Cs[j * k + j] = sqrt(fmax(djj, 0.0));
+    }
+    __syncthreads();
+    if (fail) break;
+    const double cjj = Cs[j * k + j];
+    for (int i = j + 1 + threadIdx.x; i < k; i += blockDim.x) Cs[i * k + j] /= cjj;
+    __syncthreads();
+    const int m = k - j - 1;
+    for (int p = threadIdx.x; p < m * m; p += blockDim.x) {
+      const int i = j + 1 + p / m, l = j + 1 + p % m;
+      if (l <= i) Cs[i * k + l] -= Cs[i * k + j] * Cs[l * k + j];
+    }
+    __syncthreads();
+  }
+  if (fail) {
+    if (threadIdx.x == 0) info[0] = 1;
+    return;
+  }
+  for (int p = threadIdx.x; p < k * k; p += blockDim.x) {
+    const int i = p / k, j = p - i * k;
+    if (j > i) Cs[p] = 0.0;
+    C[p] = j > i ? 0.0 : Cs[p];
+  }
+  __syncthreads();
+  // X = C^{-1} (lower) row by row: X[i, c] = (delta_ic - sum_{c<=l<i} C[i,l]
+  // X[l,c]) / C[i,i] for every c <= i in parallel; X overwrites the strict
+  // upper triangle's storage transposed (Xt[c][i] at Cs[c * k + i], c < i)
+  // and its diagonal goes to a separate SMEM vector
+  double* xd = sred;   // X[i][i], i < k <= 160 (reuses the reduction buffer)
+  for (int i = 0; i < k; ++i) {
+    const double cii = Cs[i * k + i];
+    for (int c = threadIdx.x; c <= i; c += blockDim.x) {
+      double s = 0.0;
+      if (c == i) {
+        xd[i] = 1.0 / cii;
+      } else {
+        s = -Cs[i * k + c] * xd[c];   // l = c
+        for (int l = c + 1; l < i; ++l) s = fma(-Cs[i * k + l], Cs[c * k + l], s);
+        Cs[c * k + i] = s / cii;
+      }
+    }
+    __syncthreads();
+  }
+  double tr = 0.0;
+  for (int p = threadIdx.x; p < k * k; p += blockDim.x) {
+    const int i = p / k, c = p - i * k;
+    const double x = c > i ? 0.0 : (c == i ? xd[i] : Cs[c * k + i]);
+    Binv[p] = x;
+    tr += x * x;
+  }
+  __syncthreads();
+  double ld = 0.0;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) ld += log(Cs[j * k + j]);
+  sred[threadIdx.x] = tr;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int q = 0; q < (int)blockDim.x; ++q) s += sred[q];
+    out[1] = s;
+  }
+  __syncthreads();
+  sred[threadIdx.x] = ld;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int q = 0; q < (int)blockDim.x; ++q) s += sred[q];
+    out[0] = 2.0 * s;
+    info[0] = 0;
+  }
+}
+
+// global-memory form for k > 160 (the k x k matrix exceeds shared memory)
+__global__ void precond_factor_global(int k, double noise, double* C, double* Binv, double* out, int* info) {
   __shared__ int fail;
   if (threadIdx.x == 0) fail = 0;
   __syncthreads();
-  // shift the diagonal (only the lower triangle is read afterwards)
   for (int p = threadIdx.x; p < k * k; p += blockDim.x) {
     int i = p / k, j = p - i * k;
     if (i == j) C[p] += noise;
@@ -575,7 +717,6 @@ __global__ void precond_factor_kernel(int k, double noise, double* C, double* Bi
     if (j > i) C[p] = 0.0;
   }
   __syncthreads();
-  // X = C^{-1} (lower), column-parallel forward substitution into Binv scratch
   for (int c = threadIdx.x; c < k; c += blockDim.x) {
     for (int i = 0; i < k; ++i) {
       double s = (i == c) ? 1.0 : 0.0;
@@ -584,7 +725,6 @@ __global__ void precond_factor_kernel(int k, double noise, double* C, double* Bi
     }
   }
   __syncthreads();
-  // tr(B^{-1}) = ||X||_F^2 ; logdet = 2 sum log C_jj
   __shared__ double sred[1024];
   double tr = 0.0, ld = 0.0;
   for (int p = threadIdx.x; p < k * k; p += blockDim.x) tr += Binv[p] * Binv[p];
@@ -838,6 +978,11 @@ int gp_lt_mul(int64_t n, int k, const double* L, int64_t ldl, const double* V, i
   }
   int nb = nb_rows(n);
   GP_REQUIRE(partials_len >= (int64_t)nb * k * t, "gp_lt_mul: partials too small");
+  if (t >= kWideT) {   // GEMM-shaped (L^T L of the preconditioner factor, wide blocks)
+    ltr_wide<<<dim3(nb, (t + kWT - 1) / kWT), 256, 0, st>>>(n, k, t, L, ldl, V, ldv, partials, k * t, 0, nullptr);
+    GP_LAUNCH_CHECK();
+    return finalize(partials, nb, k * t, 0, k * t, out, st);
+  }
   size_t smem = ltmul_smem(k, t);
   if (int rc = set_smem(ltmul_kernel, smem)) return rc;
   ltmul_kernel<<<nb, kRT, smem, st>>>(n, k, L, ldl, V, ldv, t, partials);
@@ -849,6 +994,14 @@ int gp_lowrank_mul(int64_t n, int k, const double* L, int64_t ldl, const double*
                    int t, double alpha, double beta, double* Y, int64_t ldy, void* stream) {
   GP_REQUIRE(t >= 1 && k >= 0, "gp_lowrank_mul: k=%d t=%d", k, t);
   if (n == 0) return GP_OK;
+  const size_t wsm = (size_t)k * (kWT + kWLS) * sizeof(double);
+  if (t >= kWideT && k > 0 && wsm <= 227 * 1024) {
+    if (int rc = set_smem(lowrank_wide, wsm)) return rc;
+    lowrank_wide<<<dim3((unsigned)((n + kWT - 1) / kWT), (t + kWT - 1) / kWT), 256, wsm, (cudaStream_t)stream>>>(
+        n, k, L, ldl, M, ldm, t, alpha, beta, Y, ldy);
+    GP_LAUNCH_CHECK();
+    return GP_OK;
+  }
   size_t smem = (size_t)k * t * sizeof(double);
   if (int rc = set_smem(lowrank_kernel, smem)) return rc;
   int64_t tot = n * t;
@@ -865,7 +1018,13 @@ int gp_precond_factor(int64_t n, int k, const double* L, int64_t ldl, double noi
   GP_REQUIRE(k >= 1 && noise > 0.0, "gp_precond_factor: k=%d noise=%g", k, noise);
   // chol <- L^T L
   if (int rc = gp_lt_mul(n, k, L, ldl, L, ldl, k, chol, partials, partials_len, stream)) return rc;
-  precond_factor_kernel<<<1, 1024, 0, st>>>(k, noise, chol, Binv, logdet_tr_dev, info_dev);
+  const size_t fsm = (size_t)k * k * sizeof(double);
+  if (k <= 160) {
+    if (int rc = set_smem(precond_factor_kernel, fsm)) return rc;
+    precond_factor_kernel<<<1, 1024, fsm, st>>>(k, noise, chol, Binv, logdet_tr_dev, info_dev);
+  } else {
+    precond_factor_global<<<1, 1024, 0, st>>>(k, noise, chol, Binv, logdet_tr_dev, info_dev);
+  }
   GP_LAUNCH_CHECK();
   // Binv currently holds X = C^{-1}; form X^T X into partials then copy
   GP_REQUIRE(partials_len >= (int64_t)k * k, "gp_precond_factor: partials too small");

@@ -9,6 +9,8 @@
 // pivot from device memory: no host synchronisation inside the factorisation.
 #include "gp_common.cuh"
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 namespace gp {
@@ -162,6 +164,281 @@ __global__ void pivchol_finish(PivArgs a) {
   if (!*a.stop) a.info[0] = a.k;
 }
 
+// ---------------------------------------------------------------------------
+// Small n: the whole factorisation in ONE launch on an 8-CTA cluster. Each
+// step's argmax is combined over distributed shared memory (every CTA reads
+// the 8 partials in rank order: the same pivot everywhere) and one cluster
+// barrier (release / acquire, also ordering the global L writes) separates
+// the steps, instead of two kernel launches per step (C1: 200 launches,
+// ~1.9 ms). Per-row arithmetic is that of pivchol_step (8 lanes per row, same
+// accumulation and shuffle order), so pivots and factor are identical.
+// ---------------------------------------------------------------------------
+constexpr int kPivCl = 8;
+constexpr int kPivThreads = 1024;
+constexpr int64_t kPivClusterMaxN = 65536;
+
+__global__ void __cluster_dims__(kPivCl, 1, 1) __launch_bounds__(kPivThreads)
+    pivchol_cluster(PivArgs a) {
+  namespace cgr = cooperative_groups;
+  cgr::cluster_group cl = cgr::this_cluster();
+  extern __shared__ double sp[];           // 1 + d + k: pivot residual | x_p | L[p, :j]
+  __shared__ double slot_v[2];
+  __shared__ int64_t slot_i[2];
+  __shared__ double sv[32];
+  __shared__ int64_t si[32];
+  __shared__ int64_t s_piv;
+  __shared__ int s_stop;
+  const int rank = (int)cl.block_rank();
+  const int64_t per = (a.n + kPivCl - 1) / kPivCl;
+  const int64_t r0 = min(a.n, (int64_t)rank * per), r1 = min(a.n, r0 + per);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = threadIdx.x & 7, grp = threadIdx.x >> 3, ngrp = blockDim.x >> 3;
+  auto reduce_store = [&](double bv, int64_t bi, int slot) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      better(bv, bi, ov, oi);
+    }
+    if (lane == 0) { sv[w] = bv; si[w] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double v = -INFINITY; int64_t i = INT64_MAX;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) better(v, i, sv[q], si[q]);
+      slot_v[slot] = v;
+      slot_i[slot] = i;
+    }
+  };
+  // init: residual diagonal s2, L zero; every row is a candidate
+  {
+    double bv = -INFINITY; int64_t bi = INT64_MAX;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+      a.dres[i] = a.s2;
+      for (int m = 0; m < a.k; ++m) a.L[i * a.ldl + m] = 0.0;
+      better(bv, bi, a.s2, i);
+    }
+    reduce_store(bv, bi, 1);
+  }
+  cl.sync();
+  int j = 0;
+  for (; j < a.k; ++j) {
+    const int prev = (j + 1) & 1;   // slot written by the previous step (init: 1)
+    if (w == 0) {
+      // lane b reads CTA b's partial over DSMEM; the choice (largest, then
+      // lowest index) is associative, so the shuffle tree gives the same pivot
+      double v = -INFINITY; int64_t i = INT64_MAX;
+      if (lane < kPivCl) {
+        v = *cl.map_shared_rank(&slot_v[prev], lane);
+        i = *cl.map_shared_rank(&slot_i[prev], lane);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        int64_t oi = __shfl_xor_sync(0xffffffffu, i, o);
+        better(v, i, ov, oi);
+      }
+      if (lane == 0) {
+        s_stop = !(v > 0.0);
+        s_piv = i;
+        sp[0] = v;
+        if (rank == 0 && !s_stop) a.piv[j] = i;
+      }
+    }
+    __syncthreads();
+    if (s_stop) break;   // uniform over the cluster: every CTA read the same partials
+    const int64_t p = s_piv;
+    for (int q = threadIdx.x; q < a.d; q += blockDim.x) sp[1 + q] = a.X[p * a.ldx + q];
+    for (int m = threadIdx.x; m < j; m += blockDim.x) sp[1 + a.d + m] = a.L[p * a.ldl + m];
+    __syncthreads();
+    const double inv_sq = 1.0 / sqrt(sp[0]);
+    const double* xp = sp + 1;
+    const double* lp = sp + 1 + a.d;
+    double bv = -INFINITY; int64_t bi = INT64_MAX;
+    // RPG rows per 8-lane group and pass: their loads are independent and
+    // issue together (the step is load-latency bound at small n)
+    constexpr int RPG = 4;
+    for (int64_t i0 = r0; i0 < r1; i0 += (int64_t)ngrp * RPG) {
+      double r2[RPG], dot[RPG];
+#pragma unroll
+      for (int u = 0; u < RPG; ++u) {
+        const int64_t i = i0 + grp + (int64_t)u * ngrp;
+        r2[u] = 0.0;
+        dot[u] = 0.0;
+        if (i < r1) {
+          const double* xi = a.X + i * a.ldx;
+          for (int q = g; q < a.d; q += 8) {
+            double df = xi[q] - xp[q];
+            r2[u] = fma(df, df, r2[u]);
+          }
+          const double* li = a.L + i * a.ldl;
+          for (int m = g; m < j; m += 8) dot[u] = fma(li[m], lp[m], dot[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < RPG; ++u) {
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+          r2[u] += __shfl_xor_sync(0xffffffffu, r2[u], o);
+          dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], o);
+        }
+        const int64_t i = i0 + grp + (int64_t)u * ngrp;
+        if (i < r1 && g == 0) {
+          double row = a.s2 * kappa_f64(a.fam, r2[u]);
+          double col = (row - dot[u]) * inv_sq;
+          a.L[i * a.ldl + j] = col;
+          double di = a.dres[i] - col * col;
+          di = di > 0.0 ? di : 0.0;
+          if (i == p) di = 0.0;
+          a.dres[i] = di;
+          better(bv, bi, di, i);
+        }
+      }
+    }
+    reduce_store(bv, bi, j & 1);
+    cl.sync();   // release / acquire: L[:, j], dres and the slots visible cluster-wide
+  }
+  if (rank == 0 && threadIdx.x == 0) a.info[0] = j;
+}
+
+// Smaller still (rows per CTA x (k + d + 1) doubles within SMEM): a 16-CTA
+// cluster keeps its rows of L, X and the residual diagonal in shared memory
+// for the whole factorisation; the pivot's point and L row come from the
+// owning CTA over DSMEM. Same per-row arithmetic as pivchol_step.
+constexpr int kPivCl16 = 16;
+
+__host__ __device__ inline int piv_lds(int k) { return k | 1; }   // odd row stride: fewer bank conflicts
+
+__global__ void __launch_bounds__(kPivThreads) pivchol_cluster_smem(PivArgs a, int rpc) {
+  namespace cgr = cooperative_groups;
+  cgr::cluster_group cl = cgr::this_cluster();
+  extern __shared__ __align__(16) double smd[];
+  const int lds = piv_lds(a.k);
+  double* Ls = smd;                                // [rpc][lds]
+  double* Xs = Ls + (size_t)rpc * lds;             // [rpc][d]
+  double* ds = Xs + (size_t)rpc * a.d;             // [rpc]
+  double* sp = ds + rpc;                           // 1 + d + k
+  __shared__ double slot_v[2];
+  __shared__ int64_t slot_i[2];
+  __shared__ double sv[32];
+  __shared__ int64_t si[32];
+  __shared__ int64_t s_piv;
+  __shared__ int s_stop;
+  const int rank = (int)cl.block_rank(), ncl = (int)cl.num_blocks();
+  const int64_t r0 = min(a.n, (int64_t)rank * rpc), r1 = min(a.n, r0 + rpc);
+  const int nr = (int)(r1 - r0);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = threadIdx.x & 7, grp = threadIdx.x >> 3, ngrp = blockDim.x >> 3;
+  for (int p = threadIdx.x; p < rpc * lds; p += blockDim.x) Ls[p] = 0.0;
+  for (int p = threadIdx.x; p < nr * a.d; p += blockDim.x) {
+    const int r = p / a.d, q = p - r * a.d;
+    Xs[p] = a.X[(r0 + r) * a.ldx + q];
+  }
+  double bv = -INFINITY; int64_t bi = INT64_MAX;
+  for (int r = threadIdx.x; r < rpc; r += blockDim.x) {
+    ds[r] = a.s2;
+    if (r < nr) better(bv, bi, a.s2, r0 + r);
+  }
+  auto reduce_store = [&](double v, int64_t i, int slot) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, v, o);
+      int64_t oi = __shfl_xor_sync(0xffffffffu, i, o);
+      better(v, i, ov, oi);
+    }
+    if (lane == 0) { sv[w] = v; si[w] = i; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double x = -INFINITY; int64_t y = INT64_MAX;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) better(x, y, sv[q], si[q]);
+      slot_v[slot] = x;
+      slot_i[slot] = y;
+    }
+  };
+  reduce_store(bv, bi, 1);
+  cl.sync();
+  int j = 0;
+  for (; j < a.k; ++j) {
+    const int prev = (j + 1) & 1;
+    if (w == 0) {
+      double v = -INFINITY; int64_t i = INT64_MAX;
+      if (lane < ncl) {
+        v = *cl.map_shared_rank(&slot_v[prev], lane);
+        i = *cl.map_shared_rank(&slot_i[prev], lane);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        int64_t oi = __shfl_xor_sync(0xffffffffu, i, o);
+        better(v, i, ov, oi);
+      }
+      if (lane == 0) {
+        s_stop = !(v > 0.0);
+        s_piv = i;
+        sp[0] = v;
+        if (rank == 0 && !s_stop) a.piv[j] = i;
+      }
+    }
+    __syncthreads();
+    if (s_stop) break;
+    const int64_t p = s_piv;
+    {
+      const int owner = (int)(p / rpc), lr = (int)(p - (int64_t)owner * rpc);
+      const double* xo = cl.map_shared_rank(Xs, owner) + (size_t)lr * a.d;
+      const double* lo = cl.map_shared_rank(Ls, owner) + (size_t)lr * lds;
+      for (int q = threadIdx.x; q < a.d + j; q += blockDim.x) sp[1 + q] = q < a.d ? xo[q] : lo[q - a.d];
+    }
+    __syncthreads();
+    const double inv_sq = 1.0 / sqrt(sp[0]);
+    const double* xp = sp + 1;
+    const double* lp = sp + 1 + a.d;
+    bv = -INFINITY; bi = INT64_MAX;
+    for (int r = grp; r - grp < nr; r += ngrp) {   // warp-uniform trip count (shuffles)
+      const bool in = r < nr;
+      double r2 = 0.0, dot = 0.0;
+      if (in) {
+        const double* xi = Xs + (size_t)r * a.d;
+        for (int q = g; q < a.d; q += 8) {
+          double df = xi[q] - xp[q];
+          r2 = fma(df, df, r2);
+        }
+        const double* li = Ls + (size_t)r * lds;
+        for (int m = g; m < j; m += 8) dot = fma(li[m], lp[m], dot);
+      }
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+        dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      }
+      if (in && g == 0) {
+        const int64_t i = r0 + r;
+        double row = a.s2 * kappa_f64(a.fam, r2);
+        double col = (row - dot) * inv_sq;
+        Ls[(size_t)r * lds + j] = col;
+        double di = ds[r] - col * col;
+        di = di > 0.0 ? di : 0.0;
+        if (i == p) di = 0.0;
+        ds[r] = di;
+        better(bv, bi, di, i);
+      }
+    }
+    reduce_store(bv, bi, j & 1);
+    cl.sync();   // the step's L column, residuals and argmax slots visible cluster-wide
+  }
+  // the factor and residual diagonal out to global memory (coalesced)
+  for (int p = threadIdx.x; p < nr * a.k; p += blockDim.x) {
+    const int r = p / a.k, m = p - r * a.k;
+    a.L[(r0 + r) * a.ldl + m] = Ls[(size_t)r * lds + m];
+  }
+  for (int r = threadIdx.x; r < nr; r += blockDim.x) a.dres[r0 + r] = ds[r];
+  if (rank == 0 && threadIdx.x == 0) a.info[0] = j;
+  cl.sync();   // no CTA exits while another may still read its SMEM
+}
+
+static size_t piv_smem16(int64_t n, int d, int k) {
+  const int64_t rpc = (n + kPivCl16 - 1) / kPivCl16;
+  return (size_t)(rpc * (piv_lds(k) + d + 1) + 1 + d + k) * sizeof(double);
+}
+
 // row blocks of >= 64 rows (two passes of the 32 row groups of a block), at
 // most 1024 of them (the select kernel's single block reduces their partials):
 // small n spreads over many SMs instead of a few long blocks
@@ -198,6 +475,33 @@ int gp_pivchol(int family, int d, const double* Xs64, int64_t ldx, int64_t n, do
   a.pidx = reinterpret_cast<int64_t*>(w); w += sizeof(int64_t) * a.nb;
   a.pinfo = reinterpret_cast<double*>(w); w += sizeof(double) * (1 + 256 + k);
   a.stop = reinterpret_cast<int*>(w);
+  // small n x k: the SMEM-resident 16-CTA cluster (non-portable size; if the
+  // launch is refused the 8-CTA global-memory cluster below takes it)
+  const size_t smem16 = piv_smem16(n, d, k);
+  if (smem16 + 1024 <= 227 * 1024) {
+    cudaFuncSetAttribute(pivchol_cluster_smem, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(pivchol_cluster_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem16);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kPivCl16; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(kPivCl16); cfg.blockDim = dim3(kPivThreads);
+    cfg.dynamicSmemBytes = smem16; cfg.stream = st; cfg.attrs = at; cfg.numAttrs = 1;
+    const int rpc = (int)((n + kPivCl16 - 1) / kPivCl16);
+    if (cudaLaunchKernelEx(&cfg, pivchol_cluster_smem, a, rpc) == cudaSuccess) {
+      GP_LAUNCH_CHECK();
+      return GP_OK;
+    }
+    cudaGetLastError();
+  }
+  if (n <= kPivClusterMaxN) {
+    const size_t smem = sizeof(double) * (1 + d + k);
+    if (smem > 48 * 1024)
+      GP_CUDA_TRY(cudaFuncSetAttribute(pivchol_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    pivchol_cluster<<<kPivCl, kPivThreads, smem, st>>>(a);
+    GP_LAUNCH_CHECK();
+    return GP_OK;
+  }
   pivchol_init<<<a.nb, 256, 0, st>>>(a);
   GP_LAUNCH_CHECK();
   size_t smem_max = sizeof(double) * (1 + d + k);

@@ -74,23 +74,28 @@ class MLLResult:
     diagnostics: MLLDiagnostics = field(repr=False)
 
 
-def build_kernel_preconditioner(model: KernelModel, X, rank: int):
+def build_kernel_preconditioner(model: KernelModel, X, rank: int, overlap=None):
     """Rank-min(rank, n) pivoted-Cholesky preconditioner of the noiseless
-    kernel (likelihood.py:74-91); None when rank <= 0."""
+    kernel (likelihood.py:74-91); None when rank <= 0. `overlap` runs on the
+    host while the device factorises."""
     if rank <= 0:
         return None
     src = _pc.KernelRowSource(model, X)
     n = src.points.n
     k = min(rank, n)
-    factor = _pc.partial_pivoted_cholesky(src, np.full(n, model.outputscale), k)
+    factor = _pc.partial_pivoted_cholesky(src, np.full(n, model.outputscale), k, overlap)
     return _pc.build_preconditioner(factor, model.noise)
 
 
-def draw_probes_device(n: int, t: int, seed: int, cache):
+def draw_probes_device(n: int, t: int, seed: int, cache, draws=None):
+    """`draws`: the (z1, z2) normals already taken from default_rng(seed) for
+    a rank-`cache.rank` preconditioner (drawn while the factor was built)."""
     rng = np.random.default_rng(seed)
     if cache is None:
         return D.to_device(rng.standard_normal((n, t)))
-    return _pc.precond_sample_device(cache, rng, t)
+    if draws is not None and draws[0].shape[0] != cache.rank:
+        draws = None   # the factorisation stopped early: the z2 stream position differs
+    return _pc.precond_sample_device(cache, rng, t, draws)
 
 
 def draw_probes(n: int, t: int, seed: int, cache) -> np.ndarray:
@@ -127,8 +132,18 @@ def mll_value_and_grad(model: KernelModel, X, y, plan: PartitionPlan, pool: Work
         return mll_value_and_grad_sharded(model, ps, yd, cg_config, probe_seed, comm)
     t = cg_config.probes
     yc = yd - model.mean
-    cache = build_kernel_preconditioner(model, ps, cg_config.precond_rank)
-    Z = draw_probes_device(n, t, probe_seed, cache)
+    # the probes' host normals (likelihood.py:94-101: z1 = k x t before
+    # z2 = n x t) are drawn while the device runs the pivoted Cholesky
+    k_req = min(cg_config.precond_rank, n) if cg_config.precond_rank > 0 else 0
+    draws = []
+
+    def host_draws():
+        rng = np.random.default_rng(probe_seed)
+        draws.append(rng.standard_normal((k_req, t)))
+        draws.append(rng.standard_normal((n, t)))
+
+    cache = build_kernel_preconditioner(model, ps, cg_config.precond_rank, overlap=host_draws)
+    Z = draw_probes_device(n, t, probe_seed, cache, tuple(draws) if draws else None)
     op = training_operator(model, ps, precision=cg_config.precision)
     B = T.cat([yc[:, None], Z], dim=1).contiguous()
     sol = mbcg_device(op, B, cg_config.tolerance, cg_config.max_iters, cache)

@@ -89,7 +89,7 @@ class KernelRowSource:
         return kernel_rows(self.model, self.points.X, i, i + 1, noise=False)[0]
 
 
-def _pivchol_device(src: KernelRowSource, k: int):
+def _pivchol_device(src: KernelRowSource, k: int, overlap=None):
     T = D.torch()
     ps, model = src.points, src.model
     n = ps.n
@@ -105,11 +105,13 @@ def _pivchol_device(src: KernelRowSource, k: int):
                               float(model.outputscale), k, _lib.ptr(L), k, _lib.ptr(piv),
                               _lib.ptr(resid), _lib.ptr(info), _lib.ptr(ws), nbytes,
                               _lib.stream_handle()), "gp_pivchol")
+    if overlap is not None:   # host work while the factorisation runs
+        overlap()
     rank = int(info.item())
     return PivotedFactor(L[:, :rank], D.to_host(piv[:rank]), resid)
 
 
-def partial_pivoted_cholesky(row_fn, diag, k: int) -> PivotedFactor:
+def partial_pivoted_cholesky(row_fn, diag, k: int, overlap=None) -> PivotedFactor:
     """Greedy rank-k pivoted Cholesky (precond.py:58-98). Kernel row sources
     run fully on the device; arbitrary row callables are evaluated per pivot
     and the factor updates run on the device."""
@@ -120,7 +122,7 @@ def partial_pivoted_cholesky(row_fn, diag, k: int) -> PivotedFactor:
         dg = np.asarray(diag, dtype=np.float64)
         if dg.shape != (n,) or not np.all(dg == row_fn.model.outputscale):
             raise ValueError("kernel row source expects the constant diagonal outputscale")
-        return _pivchol_device(row_fn, k)
+        return _pivchol_device(row_fn, k, overlap)
     T = D.torch()
     d = D.to_device(diag).clone()
     n = d.shape[0]
@@ -212,11 +214,16 @@ def precond_matmul(cache: PreconditionerCache, V):
     return out[:, 0] if squeeze else out
 
 
-def precond_sample_device(cache: PreconditionerCache, rng: np.random.Generator, t: int):
+def precond_sample_device(cache: PreconditionerCache, rng: np.random.Generator, t: int, draws=None):
     """Z = L z1 + sqrt(noise) z2 with z1 (k x t) drawn before z2 (n x t)
-    from the host generator (precond.py:150-162) — bit-identical probes."""
-    z1 = rng.standard_normal((cache.rank, t))
-    z2 = D.to_device(rng.standard_normal((cache.n, t)))
+    from the host generator (precond.py:150-162) — bit-identical probes.
+    `draws` = (z1, z2) already taken from a generator in that order."""
+    if draws is None:
+        z1 = rng.standard_normal((cache.rank, t))
+        z2 = rng.standard_normal((cache.n, t))
+    else:
+        z1, z2 = draws
+    z2 = D.to_device(z2)
     if cache.rank == 0:
         return math.sqrt(cache.noise) * z2
     return _ops.lowrank_mul(cache.factor_device, D.to_device(z1), z2, alpha=1.0,
