@@ -272,6 +272,21 @@ int gp_grad_forms(int family, int d, int ard, const float* Xr, int64_t ldr, int6
                   int64_t self_offset, int algo, double* out, void* workspace,
                   size_t workspace_bytes, void* stream);
 
+/* ---- data preparation for the training protocol ---------------------------
+ * data.py:163-196 (split_and_whiten), trainer.py:323-330 (pretraining subset).
+ * Column mean and population std (ddof 0, two-pass, fp64, fixed-order
+ * reductions) over the m rows `rows` (nullptr: rows 0..m-1) of X; with
+ * unit_if_zero a zero std is reported as 1; std_out may be nullptr. */
+int64_t gp_column_moments_workspace_len(int64_t m, int d);
+int gp_column_moments(const double* X, int64_t ldx, int64_t m, int d, const int64_t* rows, double* mean,
+                      double* std_out, int unit_if_zero, double* workspace, int64_t workspace_len, void* stream);
+/* out = (X - mean) / std row-wise (the whitening of data.py:191-194) */
+int gp_standardize(const double* X, int64_t ldx, int64_t n, int d, const double* mean, const double* std_in,
+                   double* out, int64_t ldo, void* stream);
+/* out[i, :] = X[idx[i], :]; *bad_dev = 1 if an index is outside [0, n_src) */
+int gp_gather_rows(const double* X, int64_t ldx, int64_t n_src, const int64_t* idx, int64_t m, int d, double* out,
+                   int64_t ldo, int* bad_dev, void* stream);
+
 /* Symmetric schedule of the same forms for the square training operator
  * (rows = columns = X, likelihood.py:166-216): the caller passes Y, R with
  * Y R^T SYMMETRIC (e.g. Y_s = [a/2 | -(S-W)/(4t) | -W/(4t) | L B^-1/(2 noise)],

@@ -19,6 +19,7 @@ from .cg import SolveReport, SolveRequest, Tridiagonal, mbcg_solve, slq_logdet
 from .likelihood import CgConfig, MLLResult, mll_value_and_grad
 from .predictor import (CgPredictor, PredictionCache, PredOutput, build_cache, load_cache,
                         predict, predict_mean, predict_variance, save_cache, verify_cache)
+from .data import Dataset, RawTable, split_and_whiten
 from .trainer import AdamConfig, LbfgsConfig, MllObjective, TrainConfig, TrainTrace, train
 
 __version__ = "0.1.0"

@@ -83,6 +83,10 @@ _SIGS = {
     "gp_grad_forms": (C.c_int, [C.c_int, C.c_int, C.c_int, c_p, c_i64, c_i64, c_p, c_i64, c_i64,
                                 c_f64, c_p, c_i64, c_p, c_i64, C.c_int, c_i64, C.c_int, c_p, c_p,
                                 c_sz, c_p]),
+    "gp_column_moments_workspace_len": (c_i64, [c_i64, C.c_int]),
+    "gp_column_moments": (C.c_int, [c_p, c_i64, c_i64, C.c_int, c_p, c_p, c_p, C.c_int, c_p, c_i64, c_p]),
+    "gp_standardize": (C.c_int, [c_p, c_i64, c_i64, C.c_int, c_p, c_p, c_p, c_i64, c_p]),
+    "gp_gather_rows": (C.c_int, [c_p, c_i64, c_i64, c_p, c_i64, C.c_int, c_p, c_i64, c_p, c_p]),
     "gp_grad_forms_sym_workspace_bytes": (c_sz, [c_i64, C.c_int, C.c_int, C.c_int]),
     "gp_grad_forms_sym": (C.c_int, [C.c_int, C.c_int, C.c_int, c_p, c_i64, c_i64, c_f64, c_p, c_i64, c_p,
                                     c_i64, C.c_int, c_p, c_p, c_sz, c_p]),

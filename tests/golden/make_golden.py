@@ -264,6 +264,20 @@ def c2_mll():
     print(f"  C2 MLL: value={res.value!r} iters={res.diagnostics.iterations} ({secs:.0f}s)")
 
 
+def whiten():
+    """split_and_whiten (data.py:163-196) on a table with a constant feature
+    column and a wide value range, through the reference."""
+    from blockgp.data import RawTable, split_and_whiten
+    rng = np.random.default_rng(21)
+    n, d = 1001, 5
+    X = rng.standard_normal((n, d)) * np.array([1.0, 1e3, 1e-3, 0.0, 5.0]) + np.array([0.0, 7.0, -3.0, 2.5, 1e4])
+    y = 3.0 * rng.standard_normal(n) + 40.0
+    ds = split_and_whiten(RawTable(X, y, [f"x{i}" for i in range(d)], "y"), seed=5, name="w")
+    save("whiten", X_raw=X, y_raw=y, seed=np.array(5), X=ds.X, y=ds.y, train_idx=ds.train_idx,
+         val_idx=ds.val_idx, test_idx=ds.test_idx, feature_mean=ds.feature_mean, feature_std=ds.feature_std,
+         target_mean=np.array(ds.target_mean), target_std=np.array(ds.target_std))
+
+
 def main(which=()):
     t0 = time.perf_counter()
     if not which or "base" in which:
@@ -280,11 +294,13 @@ def main(which=()):
         print("large pivots"); large_pivots()
     if not which or "c4_grad" in which:
         print("C4 gradient rows"); c4_grad()
+    if not which or "whiten" in which:
+        print("whiten"); whiten()
     if not which or "c2_mll" in which:
         print("C2 MLL"); c2_mll()
     print(f"done in {time.perf_counter() - t0:.0f}s")
 
 
 if __name__ == "__main__":
-    # python make_golden.py [base] [row_subsets] [large_pivots] [c4_grad] [c2_mll]
+    # python make_golden.py [base] [row_subsets] [large_pivots] [c4_grad] [whiten] [c2_mll]
     main(tuple(sys.argv[1:]))

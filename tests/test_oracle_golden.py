@@ -140,3 +140,16 @@ def test_large_pivots_golden_pins_the_oracle():
     pc, piv = O.kernel_precond(hp, X, w.rank)
     np.testing.assert_array_equal(piv, g["M1e6_pivots"])
     assert pc["logdet"] == pytest.approx(float(g["M1e6_precond_logdet"]), rel=1e-12)
+
+
+def test_oracle_split_and_whiten_matches_reference():
+    """data.py:163-196 restated (oracle) against the reference's own output."""
+    g = load_golden("whiten")
+    Xs, ys, tr, va, te, fm, fs, tm, ts = O.split_and_whiten(g["X_raw"], g["y_raw"], int(g["seed"]))
+    for a, b in ((tr, g["train_idx"]), (va, g["val_idx"]), (te, g["test_idx"])):
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(Xs, g["X"])
+    np.testing.assert_array_equal(ys, g["y"])
+    np.testing.assert_array_equal(fs, g["feature_std"])
+    assert fs[3] == 1.0   # the constant column keeps a unit divisor
+    assert tm == float(g["target_mean"]) and ts == float(g["target_std"])
