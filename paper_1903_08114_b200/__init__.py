@@ -20,6 +20,7 @@ from .likelihood import CgConfig, MLLResult, mll_value_and_grad
 from .predictor import (CgPredictor, PredictionCache, PredOutput, build_cache, load_cache,
                         predict, predict_mean, predict_variance, save_cache, verify_cache)
 from .data import Dataset, RawTable, split_and_whiten
+from .love import LoveCache, build_love_cache, predict_variance_love
 from .trainer import AdamConfig, LbfgsConfig, MllObjective, TrainConfig, TrainTrace, train
 
 __version__ = "0.1.0"
