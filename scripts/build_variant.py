@@ -1,7 +1,7 @@
 """Build a variant of libgpbbmm.so with extra nvcc defines for one source
 (A/B diagnostics on the GPU box; the product build is _build.build()):
 
-  python scripts/build_variant.py NAME SRC.cu [-DFOO=1 ...]
+  [REPLACES=kv_sym.cu] python scripts/build_variant.py NAME SRC.cu [-DFOO=1 ...]
     -> scripts/variants/lib_NAME.so (other objects reused from _lib/)
 
 Run with GPBBMM_LIB=scripts/variants/lib_NAME.so to load it instead."""
@@ -28,7 +28,10 @@ def main():
     if r.returncode:
         sys.stderr.write(r.stdout + r.stderr)
         sys.exit(1)
-    objs = [obj if s == src else os.path.join(B.LIBDIR, s.replace(".cu", ".o")) for s in B.SOURCES]
+    # a source outside the product list stands in for REPLACES (default: src)
+    rep = os.environ.get("REPLACES", src)
+    assert rep in B.SOURCES, f"{rep} is not a library source"
+    objs = [obj if s == rep else os.path.join(B.LIBDIR, s.replace(".cu", ".o")) for s in B.SOURCES]
     lib = os.path.join(out, f"lib_{name}.so")
     r = subprocess.run([B.nvcc(), *B.ARCH, "-shared", "-o", lib, *objs, "-lcudart", "-Xlinker", "--no-undefined"],
                        capture_output=True, text=True)
