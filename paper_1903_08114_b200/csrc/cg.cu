@@ -8,7 +8,7 @@
 // All reductions are fixed-order: every block reduces a contiguous row range
 // in a fixed thread order into partials[block][slot]; a finalize kernel sums
 // the blocks in index order. Results are therefore run-to-run deterministic.
-#include "gp_common.cuh"
+#include "tc_common.cuh"
 
 #include <algorithm>
 
@@ -45,11 +45,125 @@ __device__ void block_colsum(int64_t r0, int64_t r1, int t, F f, double* out, do
   }
 }
 
+// rows [rc, rc + R) x columns [0, CP) of a row-major global matrix into SMEM
+// (zero outside nr x cols): warp w takes rows w, w + nwarps, ..., lane l the
+// columns l, l + 32, ...: coalesced loads, no index division, several loads
+// in flight per thread. transpose: dst[c * dld + r], else dst[r * dld + c].
+template <bool TRANSPOSE>
+__device__ __forceinline__ void stage_rows(const double* __restrict__ M, int64_t ld, int64_t rc, int nr, int cols,
+                                           int R, int CP, double* dst, int dld) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+#pragma unroll 4
+  for (int r = w; r < R; r += nw) {
+    for (int c = l; c < CP; c += 32) {
+      const double v = (r < nr && c < cols) ? M[(rc + r) * ld + c] : 0.0;
+      dst[TRANSPOSE ? c * dld + r : r * dld + c] = v;
+    }
+  }
+}
+
 // out[kk*t + c] (per block) = sum_{rows} L[r,kk] * A[r,c]
+// Narrow blocks (k <= 128, t <= 16, the CG width): 32-row chunks of L and A
+// staged in SMEM with coalesced loads, each thread accumulating a 4 x 4
+// (kk x c) register tile over its row group, groups combined in a fixed
+// order: every L row is read once per product and the FMA:SMEM-load ratio is
+// 2:1 (the one-output-per-thread form re-read L per output and ran at ~10 %
+// of HBM). Other shapes: the generic form. `sm` is a scratch of
+// ltmul_scratch(k, t) doubles.
+constexpr int kLtCR = 32;
+__host__ __device__ inline bool ltmul_tiled(int k, int t) { return k <= 128 && t <= 16; }
+__host__ __device__ inline int ltmul_scratch(int k, int t) {
+  if (ltmul_tiled(k, t)) {
+    const int KP = (k + 3) / 4 * 4, TP = (t + 3) / 4 * 4;
+    const int stage = 2 * kLtCR * (KP + TP), red = 256 * 16;
+    return stage > red ? stage : red;
+  }
+  return 16 * (k > 1 ? k : 1) + 16 * t;
+}
+__device__ __forceinline__ void cp_async8z(uint32_t dst, const void* src, bool in) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(in ? 8u : 0u) : "memory");
+}
 __device__ void block_ltmul(int64_t r0, int64_t r1, int k, int t, const double* __restrict__ L,
                             int64_t ldl, const double* __restrict__ A, int64_t lda, double* out,
-                            double* sL, double* sA, const int* colmask) {
+                            double* sm, const int* colmask) {
+  if (ltmul_tiled(k, t)) {
+    const int KQ = (k + 3) / 4, TQ = (t + 3) / 4, KP = 4 * KQ, TP = 4 * TQ;
+    const int units = KQ * TQ;                 // <= 128
+    const int G = kRT / units;                 // row groups (>= 2)
+    const int u = threadIdx.x % units, g = threadIdx.x / units;
+    const int kq = u / TQ, tq = u - (u / TQ) * TQ;
+    const int stage = kLtCR * (KP + TP);       // one buffer: [kLtCR][KP] L rows, [kLtCR][TP] A rows
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31, nw = kRT >> 5;
+    // chunk copies (8-byte cp.async, zero-filled outside the rows / columns),
+    // double buffered so the next chunk streams in during this one's FMAs
+    auto issue = [&](int64_t rc, int b) {
+      const int nr = (int)min((int64_t)kLtCR, r1 - rc);
+      const uint32_t bl = (uint32_t)__cvta_generic_to_shared(sm + (size_t)b * stage);
+      const uint32_t ba = bl + (uint32_t)(kLtCR * KP * 8);
+      for (int r = w; r < kLtCR; r += nw) {
+        const bool rin = r < nr;
+        const double* lr = L + (rin ? (rc + r) * ldl : 0);
+        const double* ar = A + (rin ? (rc + r) * lda : 0);
+        for (int c = ln; c < KP; c += 32) cp_async8z(bl + (uint32_t)((r * KP + c) * 8), lr + (rin && c < k ? c : 0), rin && c < k);
+        for (int c = ln; c < TP; c += 32) cp_async8z(ba + (uint32_t)((r * TP + c) * 8), ar + (rin && c < t ? c : 0), rin && c < t);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    __syncthreads();   // the caller's writes of A (and prior use of sm) are complete
+    int b = 0;
+    if (r0 < r1) issue(r0, 0);
+    for (int64_t rc = r0; rc < r1; rc += kLtCR, b ^= 1) {
+      const int nr = (int)min((int64_t)kLtCR, r1 - rc);
+      if (rc + kLtCR < r1) {
+        issue(rc + kLtCR, b ^ 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncthreads();
+      const double* sLc = sm + (size_t)b * stage;
+      const double* sAc = sLc + kLtCR * KP;
+      if (g < G) {
+        for (int r = g; r < nr; r += G) {
+          const double2 la = *reinterpret_cast<const double2*>(sLc + r * KP + 4 * kq);
+          const double2 lb = *reinterpret_cast<const double2*>(sLc + r * KP + 4 * kq + 2);
+          const double2 aa = *reinterpret_cast<const double2*>(sAc + r * TP + 4 * tq);
+          const double2 ab = *reinterpret_cast<const double2*>(sAc + r * TP + 4 * tq + 2);
+          const double l[4] = {la.x, la.y, lb.x, lb.y}, a[4] = {aa.x, aa.y, ab.x, ab.y};
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = fma(l[i], a[j], acc[i][j]);
+        }
+      }
+      __syncthreads();   // buffer b is refilled by the issue two chunks on
+    }
+    // groups in index order (deterministic): red[g][u][16]
+    if (g < G) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sm[((size_t)g * units + u) * 16 + 4 * i + j] = acc[i][j];
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < k * t; p += kRT) {
+      const int kk = p / t, c = p - kk * t;
+      const int uu = (kk >> 2) * TQ + (c >> 2), slot = 4 * (kk & 3) + (c & 3);
+      double v = 0.0;
+      for (int q = 0; q < G; ++q) v += sm[((size_t)q * units + uu) * 16 + slot];
+      out[p] = (colmask && !colmask[c]) ? 0.0 : v;
+    }
+    __syncthreads();
+    return;
+  }
   constexpr int CR = 16, PPT = 8;
+  double* sL = sm;
+  double* sA = sm + 16 * (k > 1 ? k : 1);
   const int KT = k * t;
   for (int p0 = 0; p0 < KT; p0 += kRT * PPT) {
     double acc[PPT];
@@ -138,10 +252,9 @@ __host__ __device__ inline int off_gam(int t, int k) { return 2 * t + k * t; }
 
 // init_a: R = B, U = 0; partial rn2 = ||B_j||^2 and L^T B
 __global__ void __launch_bounds__(kRT) cg_init_a(CgK s, const double* __restrict__ B, int64_t ldb) {
-  extern __shared__ double dsm[];
+  extern __shared__ __align__(16) double dsm[];
   double* sred = dsm;
-  double* sL = sred + kRT;
-  double* sA = sL + 16 * max(s.k, 1);
+  double* sL = sred + kRT;   // block_ltmul scratch
   int64_t r0, r1;
   row_range(s.n, r0, r1);
   const int t = s.t;
@@ -155,7 +268,7 @@ __global__ void __launch_bounds__(kRT) cg_init_a(CgK s, const double* __restrict
   }, part + t, sred);
   if (s.k > 0) {
     __syncthreads();
-    block_ltmul(r0, r1, s.k, t, s.L, s.ldl, s.R, s.ld, part + 2 * t, sL, sA, nullptr);
+    block_ltmul(r0, r1, s.k, t, s.L, s.ldl, s.R, s.ld, part + 2 * t, sL, nullptr);
   }
 }
 
@@ -177,7 +290,7 @@ __global__ void cg_cvec(CgK s, int use_active) {
 // k == 0: Z = R / pc_noise (precond.py:131-132).
 template <bool INIT>
 __global__ void __launch_bounds__(kRT) cg_precond_z(CgK s) {
-  extern __shared__ double dsm[];
+  extern __shared__ __align__(16) double dsm[];
   double* sred = dsm;
   double* sc = sred + kRT;  // k * t
   const int t = s.t, k = s.k;
@@ -206,6 +319,246 @@ __global__ void __launch_bounds__(kRT) cg_precond_z(CgK s) {
     }
     return rv * z;
   }, part + off_gam(t, k), sred);
+}
+
+// Narrow blocks (t <= 16, the CG width, with a rank-k preconditioner): the
+// block's rows in 64-row chunks, each chunk's L rows staged in SMEM with
+// coalesced loads and C = B^{-1} L^T R resident; a thread owns one row and
+// four columns, so each L row is read from HBM once per application (the
+// one-output-per-thread form above re-read it t times through L1). Same kk
+// order as cg_precond_z, hence the same z; fixed-order column sums.
+constexpr int kZR = 32;          // rows per chunk
+constexpr int kZLD = kZR + 1;    // transposed chunk [kk][row]: odd stride, conflict-free reads
+constexpr int kZT = 128;         // threads: a thread owns one row and four columns
+static size_t pz_narrow_smem(int k) {
+  return ((size_t)k * 16 + 2 * ((size_t)k * kZLD + kZR * 16) + 16 * kZR) * sizeof(double);
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+template <bool INIT>
+__global__ void __launch_bounds__(kZT) cg_precond_z_narrow(CgK s) {
+  extern __shared__ __align__(16) double dsm[];
+  const int t = s.t, k = s.k, TQ = (t + 3) / 4, TP = 4 * TQ;
+  double* sC = dsm;                          // [k][TP]
+  const size_t bstride = (size_t)k * kZLD + kZR * 16;
+  double* sLb = sC + (size_t)k * 16;         // [2] x ([k][kZLD] L rows transposed | [kZR][16] R rows)
+  double* sred = sLb + 2 * bstride;          // [TP][kZR]
+  for (int p = threadIdx.x; p < k * TP; p += blockDim.x) {
+    const int kk = p / TP, c = p - kk * TP;
+    sC[p] = c < t ? s.cbuf[kk * t + c] : 0.0;
+  }
+  int64_t r0, r1;
+  row_range(s.n, r0, r1);
+  const int rl = threadIdx.x % kZR, tq = threadIdx.x / kZR;   // row of the chunk, column quad
+  const bool worker = tq < TQ;
+  bool live[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = 4 * tq + j;
+    live[j] = worker && c < t && (INIT || s.active[c]);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  // chunk c's copies (8-byte cp.async, zero-filled past the block's rows):
+  // warp w rows w, w + nw, ..., lane l columns l, l + 32, ...
+  auto issue = [&](int64_t rc, int buf) {
+    const int nr = (int)min((int64_t)kZR, r1 - rc);
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sLb + (size_t)buf * bstride);
+    const uint32_t rbase = base + (uint32_t)((size_t)k * kZLD * 8);
+    for (int r = w; r < kZR; r += nw) {
+      const double* src = s.L + (r < nr ? (rc + r) * s.ldl : 0);
+      for (int kk = l; kk < k; kk += 32)
+        cp_async8(base + (uint32_t)((kk * kZLD + r) * 8), src + (r < nr ? kk : 0), r < nr ? 8u : 0u);
+      // the chunk's R rows too: z needs them right after the FMAs
+      const double* rsrc = s.R + (r < nr ? (rc + r) * s.ld : 0);
+      if (l < 16) cp_async8(rbase + (uint32_t)((r * 16 + l) * 8), rsrc + (r < nr && l < t ? l : 0),
+                            r < nr && l < t ? 8u : 0u);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double gam[4] = {0.0, 0.0, 0.0, 0.0};
+  int buf = 0;
+  if (r0 < r1) issue(r0, 0);
+  for (int64_t rc = r0; rc < r1; rc += kZR, buf ^= 1) {
+    const int nr = (int)min((int64_t)kZR, r1 - rc);
+    if (rc + kZR < r1) {
+      issue(rc + kZR, buf ^ 1);   // the next chunk streams in while this one is used
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double* sL = sLb + (size_t)buf * bstride;
+    const double* sR = sL + (size_t)k * kZLD;
+    if (worker && rl < nr) {
+      double lc[4] = {0.0, 0.0, 0.0, 0.0};
+      const double* cq = sC + 4 * tq;
+      for (int kk = 0; kk < k; ++kk) {
+        const double lv = sL[kk * kZLD + rl];
+        const double2 ca = *reinterpret_cast<const double2*>(cq + kk * TP);
+        const double2 cb = *reinterpret_cast<const double2*>(cq + kk * TP + 2);
+        lc[0] = fma(lv, ca.x, lc[0]);
+        lc[1] = fma(lv, ca.y, lc[1]);
+        lc[2] = fma(lv, cb.x, lc[2]);
+        lc[3] = fma(lv, cb.y, lc[3]);
+      }
+      const int64_t r = rc + rl;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!live[j]) continue;
+        const int c = 4 * tq + j;
+        const double rv = sR[rl * 16 + c];
+        const double z = (rv - lc[j]) / s.pc_noise;
+        s.Z[r * s.ld + c] = z;
+        if (INIT) {
+          s.P[r * s.ld + c] = z;
+          s.P32[r * s.ld32 + c] = (float)z;
+        }
+        gam[j] += rv * z;
+      }
+    }
+    __syncthreads();   // buffer `buf` is refilled by the issue two chunks on
+  }
+  if (worker) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) sred[(4 * tq + j) * kZR + rl] = gam[j];
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < t) {
+    double v = 0.0;
+    for (int q = 0; q < kZR; ++q) v += sred[threadIdx.x * kZR + q];
+    s.partials[(int64_t)blockIdx.x * (3 * t + k * t) + off_gam(t, k) + threadIdx.x] = v;
+  }
+}
+
+// The same with whole chunks moved by the TMA: when L is contiguous (ld = k)
+// and k is even (16-byte aligned chunk starts and sizes), thread 0 copies each
+// 32-row chunk of L (25.6 KB at k = 100) with one cp.async.bulk into a
+// double-buffered row-major tile; the R rows follow by cp.async. A warp owns 8
+// rows x 4 column quads, so the stride-k row reads are at most 2-way bank
+// conflicted. Even / odd kk accumulate separately (z differs from the forms
+// above in the last bits).
+constexpr int kZB = 32;           // rows per chunk
+static size_t pz_bulk_smem(int k) {
+  return ((size_t)k * 16 + 2 * ((size_t)kZB * k + kZB * 16) + 16 * kZB) * sizeof(double) + 64;
+}
+template <bool INIT>
+__global__ void __launch_bounds__(128) cg_precond_z_bulk(CgK s) {
+  extern __shared__ __align__(128) double dsm[];
+  const int t = s.t, k = s.k, TQ = (t + 3) / 4, TP = 4 * TQ;
+  double* sC = dsm;                               // [k][TP]
+  const size_t bstride = (size_t)kZB * k + kZB * 16;
+  double* sB = sC + (size_t)k * 16;               // [2] x ([kZB][k] L rows | [kZB][16] R rows)
+  double* sred = sB + 2 * bstride;                // [TP][kZB]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sred + 16 * kZB);   // [2]
+  for (int p = threadIdx.x; p < k * TP; p += blockDim.x) {
+    const int kk = p / TP, c = p - kk * TP;
+    sC[p] = c < t ? s.cbuf[kk * t + c] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    tc::mbar_init(tc::smem_u32(&bar[0]), 1);
+    tc::mbar_init(tc::smem_u32(&bar[1]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int64_t r0, r1;
+  row_range(s.n, r0, r1);
+  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  const int rl = 8 * w + (ln >> 2), tq = ln & 3;  // row of the chunk, column quad
+  const bool worker = tq < TQ;
+  bool live[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = 4 * tq + j;
+    live[j] = worker && c < t && (INIT || s.active[c]);
+  }
+  auto issue = [&](int64_t rc, int b) {
+    const int nr = (int)min((int64_t)kZB, r1 - rc);
+    double* dst = sB + (size_t)b * bstride;
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const uint32_t bytes = (uint32_t)(nr * k * 8);
+      tc::mbar_expect_tx(tc::smem_u32(&bar[b]), bytes);
+      tc::bulk_g2s(tc::smem_u32(dst), s.L + rc * k, bytes, tc::smem_u32(&bar[b]));
+    }
+    const uint32_t rb = tc::smem_u32(dst + (size_t)kZB * k);
+    for (int e = threadIdx.x; e < kZB * 16; e += blockDim.x) {
+      const int r = e >> 4, c = e & 15;
+      const bool in = r < nr && c < t;
+      cp_async8(rb + (uint32_t)(e * 8), s.R + (in ? (rc + r) * s.ld + c : 0), in ? 8u : 0u);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double gam[4] = {0.0, 0.0, 0.0, 0.0};
+  if (r0 < r1) issue(r0, 0);
+  int i = 0;
+  for (int64_t rc = r0; rc < r1; rc += kZB, ++i) {
+    const int b = i & 1;
+    const int nr = (int)min((int64_t)kZB, r1 - rc);
+    if (rc + kZB < r1) {
+      issue(rc + kZB, b ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    tc::mbar_wait(tc::smem_u32(&bar[b]), (i >> 1) & 1);
+    __syncthreads();
+    const double* sL = sB + (size_t)b * bstride;
+    const double* sR = sL + (size_t)kZB * k;
+    if (worker && rl < nr) {
+      // even and odd kk in separate accumulators (k is even here): twice
+      // the independent DFMA chains, the loop is latency-bound otherwise
+      double lc[4] = {0.0, 0.0, 0.0, 0.0}, lo[4] = {0.0, 0.0, 0.0, 0.0};
+      const double* lr = sL + (size_t)rl * k;
+      const double* cq = sC + 4 * tq;
+      for (int kk = 0; kk < k; kk += 2) {
+        const double2 lv = *reinterpret_cast<const double2*>(lr + kk);
+        const double2 ca = *reinterpret_cast<const double2*>(cq + kk * TP);
+        const double2 cb = *reinterpret_cast<const double2*>(cq + kk * TP + 2);
+        const double2 da = *reinterpret_cast<const double2*>(cq + (kk + 1) * TP);
+        const double2 db = *reinterpret_cast<const double2*>(cq + (kk + 1) * TP + 2);
+        lc[0] = fma(lv.x, ca.x, lc[0]);
+        lc[1] = fma(lv.x, ca.y, lc[1]);
+        lc[2] = fma(lv.x, cb.x, lc[2]);
+        lc[3] = fma(lv.x, cb.y, lc[3]);
+        lo[0] = fma(lv.y, da.x, lo[0]);
+        lo[1] = fma(lv.y, da.y, lo[1]);
+        lo[2] = fma(lv.y, db.x, lo[2]);
+        lo[3] = fma(lv.y, db.y, lo[3]);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) lc[j] += lo[j];
+      const int64_t r = rc + rl;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!live[j]) continue;
+        const int c = 4 * tq + j;
+        const double rv = sR[rl * 16 + c];
+        const double z = (rv - lc[j]) / s.pc_noise;
+        s.Z[r * s.ld + c] = z;
+        if (INIT) {
+          s.P[r * s.ld + c] = z;
+          s.P32[r * s.ld32 + c] = (float)z;
+        }
+        gam[j] += rv * z;
+      }
+    }
+    __syncthreads();   // buffer b is refilled by the issue two chunks on
+  }
+  if (worker) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) sred[(4 * tq + j) * kZB + rl] = gam[j];
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (4 * tq + j < TP) sred[(4 * tq + j) * kZB + rl] = 0.0;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < t) {
+    double v = 0.0;
+    for (int q = 0; q < kZB; ++q) v += sred[threadIdx.x * kZB + q];
+    s.partials[(int64_t)blockIdx.x * (3 * t + k * t) + off_gam(t, k) + threadIdx.x] = v;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -408,11 +761,10 @@ __global__ void cg_alpha(CgK s, int it) {
 template <typename QT>
 __global__ void __launch_bounds__(kRT) cg_update(CgK s, const QT* __restrict__ Q, int64_t ldq, int it,
                                                  int with_ltr) {
-  extern __shared__ double dsm[];
+  extern __shared__ __align__(16) double dsm[];
   double* sred = dsm;
   double* sal = sred + kRT;               // t
-  double* sL = sal + s.t;
-  double* sA = sL + 16 * max(s.k, 1);
+  double* sL = sal + ((s.t + 1) & ~1);   // block_ltmul scratch, 16-byte aligned
   const int t = s.t, k = s.k;
   for (int c = threadIdx.x; c < t; c += kRT)
     sal[c] = s.active[c] ? s.alpha_hist[(int64_t)(it - 1) * t + c] : 0.0;
@@ -435,7 +787,7 @@ __global__ void __launch_bounds__(kRT) cg_update(CgK s, const QT* __restrict__ Q
   }, part + t, sred);
   if (with_ltr && k > 0 && s.pc_noise > 0.0) {
     __syncthreads();
-    block_ltmul(r0, r1, k, t, s.L, s.ldl, s.R, s.ld, part + 2 * t, sL, sA, s.active);
+    block_ltmul(r0, r1, k, t, s.L, s.ldl, s.R, s.ld, part + 2 * t, sL, s.active);
   }
 }
 
@@ -504,11 +856,10 @@ __global__ void __launch_bounds__(kRT) coldot_kernel(int64_t n, int t, const dou
 __global__ void __launch_bounds__(kRT) ltmul_kernel(int64_t n, int k, const double* __restrict__ L,
                                                     int64_t ldl, const double* __restrict__ V,
                                                     int64_t ldv, int t, double* partials) {
-  extern __shared__ double dsm[];
+  extern __shared__ __align__(16) double dsm[];
   int64_t r0, r1;
   row_range(n, r0, r1);
-  block_ltmul(r0, r1, k, t, L, ldl, V, ldv, partials + (int64_t)blockIdx.x * k * t, dsm,
-              dsm + 16 * k, nullptr);
+  block_ltmul(r0, r1, k, t, L, ldl, V, ldv, partials + (int64_t)blockIdx.x * k * t, dsm, nullptr);
 }
 
 // Y = beta Y + alpha L M
@@ -775,13 +1126,24 @@ static int check_state(const gp_mbcg* s) {
   return GP_OK;
 }
 
-static size_t ltmul_smem(int k, int t) { return (size_t)(16 * std::max(k, 1) + 16 * t) * sizeof(double); }
+static size_t ltmul_smem(int k, int t) { return (size_t)ltmul_scratch(k, t) * sizeof(double); }
 
 static size_t pz_wide_smem(int k) { return ((size_t)k * (kWT + kWLS) + 16 * kWT) * sizeof(double); }
 // the register-tiled Woodbury forms apply to wide blocks with a preconditioner
 // whose C tile and L^T tile fit in SMEM (k <= ~200)
 static bool use_wide(const gp_mbcg* s) {
   return s->t >= kWideT && s->k > 0 && s->pc_noise > 0.0 && pz_wide_smem(s->k) <= 227 * 1024;
+}
+
+// the staged narrow Woodbury form: t <= 16 with a preconditioner whose L
+// chunk and C fit in SMEM (k <= ~340)
+static bool use_narrow(const gp_mbcg* s) {
+  return s->t <= 16 && s->k > 0 && s->pc_noise > 0.0 && pz_narrow_smem(s->k) <= 227 * 1024;
+}
+
+// whole-chunk TMA copies of L: contiguous L, even k (16-byte aligned chunks)
+static bool use_bulk(const gp_mbcg* s) {
+  return use_narrow(s) && s->ldl == s->k && s->k % 2 == 0 && pz_bulk_smem(s->k) <= 227 * 1024;
 }
 
 template <class K>
@@ -836,6 +1198,20 @@ int gp_mbcg_init_b(gp_mbcg* s, void* stream) {
     GP_LAUNCH_CHECK();
     return finalize(s->partials, nb, W, off_gam(t, k), off_gam(t, k) + t, s->red, st);
   }
+  if (s->n > 0 && use_bulk(s)) {
+    const size_t smem = pz_bulk_smem(k);
+    if (int rc = set_smem(cg_precond_z_bulk<true>, smem)) return rc;
+    cg_precond_z_bulk<true><<<nb, 128, smem, st>>>(v);
+    GP_LAUNCH_CHECK();
+    return finalize(s->partials, nb, W, off_gam(t, k), off_gam(t, k) + t, s->red, st);
+  }
+  if (s->n > 0 && use_narrow(s)) {
+    const size_t smem = pz_narrow_smem(k);
+    if (int rc = set_smem(cg_precond_z_narrow<true>, smem)) return rc;
+    cg_precond_z_narrow<true><<<nb, kZT, smem, st>>>(v);
+    GP_LAUNCH_CHECK();
+    return finalize(s->partials, nb, W, off_gam(t, k), off_gam(t, k) + t, s->red, st);
+  }
   if (s->n > 0) {
     size_t smem = (kRT + (size_t)k * t) * sizeof(double);
     if (int rc = set_smem(cg_precond_z<true>, smem)) return rc;
@@ -880,7 +1256,7 @@ int gp_mbcg_update(gp_mbcg* s, const void* Q, int64_t ldq, int q_is_f64, int ite
   cg_alpha<<<1, 256, 0, st>>>(v, iteration);
   GP_LAUNCH_CHECK();
   if (s->n > 0) {
-    size_t smem = (kRT + t) * sizeof(double) + ltmul_smem(k, t);
+    size_t smem = (kRT + ((t + 1) & ~1)) * sizeof(double) + ltmul_smem(k, t);
     const int in_kernel_ltr = use_wide(s) ? 0 : 1;
     if (q_is_f64) {
       if (int rc = set_smem(cg_update<double>, smem)) return rc;
@@ -917,6 +1293,20 @@ int gp_mbcg_precond(gp_mbcg* s, int iteration, double tolerance, void* stream) {
     const size_t smem = pz_wide_smem(k);
     if (int rc = set_smem(cg_precond_z_wide<false>, smem)) return rc;
     cg_precond_z_wide<false><<<dim3(nb, (t + kWT - 1) / kWT), 256, smem, st>>>(v);
+    GP_LAUNCH_CHECK();
+    return finalize(s->partials, nb, W, off_gam(t, k), off_gam(t, k) + t, s->red, st);
+  }
+  if (s->n > 0 && use_bulk(s)) {
+    const size_t smem = pz_bulk_smem(k);
+    if (int rc = set_smem(cg_precond_z_bulk<false>, smem)) return rc;
+    cg_precond_z_bulk<false><<<nb, 128, smem, st>>>(v);
+    GP_LAUNCH_CHECK();
+    return finalize(s->partials, nb, W, off_gam(t, k), off_gam(t, k) + t, s->red, st);
+  }
+  if (s->n > 0 && use_narrow(s)) {
+    const size_t smem = pz_narrow_smem(k);
+    if (int rc = set_smem(cg_precond_z_narrow<false>, smem)) return rc;
+    cg_precond_z_narrow<false><<<nb, kZT, smem, st>>>(v);
     GP_LAUNCH_CHECK();
     return finalize(s->partials, nb, W, off_gam(t, k), off_gam(t, k) + t, s->red, st);
   }
