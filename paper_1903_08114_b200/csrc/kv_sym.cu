@@ -592,16 +592,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
         const float sv = __uint_as_float(v[k]);
-        float kap;
-        // clamps written as selects so NaN inputs propagate
-        if (FAM == GP_FAMILY_RBF) {
-          kap = ex2_approx(min0_nan(sv));          // S = -log2(e) r2 / 2
-        } else {
-          const float u = sqrt_approx(max0_nan(sv));   // S = 3 r2, u = sqrt(3) r
-          const float ex = ex2_approx(u * -kLog2e);
-          kap = fmaf(u, ex, ex);                   // (1 + sqrt3 r) e^{-sqrt3 r}
-        }
-        v[k] = __float_as_uint(kap);
+        // x 2^12 for the fp16 split (clamps written as selects so NaN
+        // inputs propagate); the fixed-point exponents divide it out
+        v[k] = __float_as_uint(kappa_split_scaled<FAM>(sv));
       }
       uint32_t p1[16], p2[16];
 #pragma unroll
@@ -804,11 +797,12 @@ __global__ void __cluster_dims__(kScaleCtas, 1, 1) __launch_bounds__(1024)
         l1 += *cl.map_shared_rank(&psum[c], b);
         mx = fmaxf(mx, *cl.map_shared_rank(&pmax[c], b));
       }
-    int E = 61, S = 0;
+    // partials carry the 2^kKScaleLog2 K scaling: |partial| <= 2^(S+12) ||V_c||_1
+    int E = 61 - kKScaleLog2, S = 0;
     if (l1 > 0.0 && l1 < INFINITY) {
       int ex;
       frexp(l1, &ex);  // l1 < 2^ex
-      E = 61 - ex;
+      E = 61 - kKScaleLog2 - ex;
       frexp((double)mx, &ex);
       S = 14 - ex;
     }
@@ -816,7 +810,7 @@ __global__ void __cluster_dims__(kScaleCtas, 1, 1) __launch_bounds__(1024)
     S = max(-100, min(100, S));
     expo[c] = E - S;
     vscale[c] = ldexpf(1.0f, S);
-    inv_scale[c] = ldexp(1.0, -E);
+    inv_scale[c] = ldexp(1.0, -E - kKScaleLog2);
   }
   cl.sync();
 }

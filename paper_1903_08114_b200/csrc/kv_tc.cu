@@ -463,7 +463,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
             float kap;
             // clamps written as selects so NaN inputs propagate (the
             // reference raises on non-finite blocks, partition.py:231-236)
-            if (FAM == GP_FAMILY_RBF) {
+            if (KV_F16) {
+              kap = kappa_split_scaled<FAM>(sv);   // x 2^12, divided out by inv_vscale
+            } else if (FAM == GP_FAMILY_RBF) {
               kap = ex2_approx(min0_nan(sv));  // S = -log2(e) r2 / 2
             } else {
               float u = sqrt_approx(max0_nan(sv));  // S = 3 r2, u = sqrt(3) r
@@ -649,7 +651,7 @@ __global__ void v_colscale_kernel(const float* __restrict__ V, int64_t ldv, int6
       S = max(-100, min(100, 14 - ex));
     }
     vscale[c] = ldexpf(1.0f, S);
-    inv_vscale[c] = ldexpf(1.0f, -S);
+    inv_vscale[c] = ldexpf(1.0f, -S - kKScaleLog2);   // also undoes the 2^12 K scaling of the fp16 split
   }
 }
 

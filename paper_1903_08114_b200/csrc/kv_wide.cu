@@ -288,16 +288,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
         }
 #pragma unroll
         for (int e = 0; e < CW; ++e) {
-          float sv = __uint_as_float(v[e]);
-          float kap;
-          if (FAM == GP_FAMILY_RBF) {
-            kap = ex2_approx(min0_nan(sv));
-          } else {
-            float u = sqrt_approx(max0_nan(sv));
-            float ex = ex2_approx(u * -kLog2e);
-            kap = fmaf(u, ex, ex);
-          }
-          v[e] = __float_as_uint(kap);
+          // x 2^12 for the fp16 split; the finalize's inv_vscale divides it out
+          v[e] = __float_as_uint(kappa_split_scaled<FAM>(__uint_as_float(v[e])));
         }
         mbar_wait(smem_u32(&k_empty[kb]), kph ^ 1);   // K[kb] was read two tiles ago
         tc_fence_after();

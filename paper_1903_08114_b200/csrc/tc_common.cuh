@@ -193,6 +193,22 @@ __device__ __forceinline__ void tmem_st16x256_x4(uint32_t taddr, const uint32_t 
       "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
       : "memory");
 }
+// kappa / s2 scaled by 2^kKScaleLog2 for the fp16 split below: K1 and the
+// residual K2 = K - K1 (~2^-11 K) then stay in fp16's normal range down to
+// K ~ 2^-15 instead of 2^-3, so small kernel values keep their relative
+// precision (the scale folds into the ex2 argument: free for Matérn, one
+// FADD for RBF; the consumers divide it out with the V column scales)
+constexpr int kKScaleLog2 = 12;
+template <int FAM>
+__device__ __forceinline__ float kappa_split_scaled(float sv) {
+  if (FAM == GP_FAMILY_RBF) {
+    return ex2_approx(min0_nan(sv) + (float)kKScaleLog2);          // S = -log2(e) r2 / 2
+  } else {
+    const float u = sqrt_approx(max0_nan(sv));                       // S = 3 r2, u = sqrt(3) r
+    const float ex = ex2_approx(fmaf(u, -kLog2e, (float)kKScaleLog2));
+    return fmaf(u, ex, ex);                                          // 2^12 (1 + sqrt3 r) e^{-sqrt3 r}
+  }
+}
 // fp16 split of a pair: K1 = K truncated to 11 significant bits, K2 = fp16(K - K1)
 __device__ __forceinline__ void split_pair(float a, float b, uint32_t& k1, uint32_t& k2) {
   const float a1 = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);

