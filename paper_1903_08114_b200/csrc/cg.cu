@@ -1128,6 +1128,11 @@ static int check_state(const gp_mbcg* s) {
 
 static size_t ltmul_smem(int k, int t) { return (size_t)ltmul_scratch(k, t) * sizeof(double); }
 
+// the preconditioner application has a form for every (t, k) whose working
+// set fits shared memory: narrow (t <= 16, k <= ~340), wide (t >= 32, k <= 212)
+// or the per-element one ((256 + k t) doubles); beyond that the caller must
+// split the right-hand sides (predictor.py does, in blocks of 16)
+
 static size_t pz_wide_smem(int k) { return ((size_t)k * (kWT + kWLS) + 16 * kWT) * sizeof(double); }
 // the register-tiled Woodbury forms apply to wide blocks with a preconditioner
 // whose C tile and L^T tile fit in SMEM (k <= ~200)
@@ -1144,6 +1149,14 @@ static bool use_narrow(const gp_mbcg* s) {
 // whole-chunk TMA copies of L: contiguous L, even k (16-byte aligned chunks)
 static bool use_bulk(const gp_mbcg* s) {
   return use_narrow(s) && s->ldl == s->k && s->k % 2 == 0 && pz_bulk_smem(s->k) <= 227 * 1024;
+}
+
+static int check_precond_fits(const gp_mbcg* s) {
+  if (s->k == 0 || s->pc_noise <= 0.0 || use_narrow(s) || use_wide(s)) return GP_OK;
+  GP_REQUIRE((kRT + (size_t)s->k * s->t) * sizeof(double) <= 227 * 1024,
+             "preconditioner rank %d with %d right-hand sides exceeds the device's shared memory; "
+             "solve in blocks of at most 16 columns or use a rank of at most 212", s->k, s->t);
+  return GP_OK;
 }
 
 template <class K>
@@ -1167,6 +1180,7 @@ int64_t gp_mbcg_partials_len(int64_t n, int t, int k) {
 
 int gp_mbcg_init_a(gp_mbcg* s, const double* B, int64_t ldb, void* stream) {
   if (int rc = check_state(s)) return rc;
+  if (int rc = check_precond_fits(s)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   const int t = s->t, k = s->k, W = 3 * t + k * t, nb = cg_nblocks(s);
   if (s->n > 0) {

@@ -320,3 +320,27 @@ def test_wide_block_woodbury_matches_narrow_chunks(tol, its):
         assert len({tri.order for tri in wide.tridiagonals}) > 1
         res = np.linalg.norm(B - A @ wide.solutions, axis=0) / np.linalg.norm(B, axis=0)
         assert res.max() <= 1.5e-3, res.max()
+
+
+def test_large_preconditioner_rank_variance_and_clear_error():
+    """a rank beyond the 256-column Woodbury kernels' shared-memory
+    reach (k > 212) solves the variance chunk 16 columns at a time instead of
+    failing in a launch, and a raw solve that cannot fit is a ValueError."""
+    import torch
+    from paper_1903_08114_b200 import _device as D, cg as CG
+    rng = np.random.default_rng(31)
+    n, d = 600, 3
+    X = rng.uniform(size=(n, d))
+    y = rng.standard_normal(n)
+    hp = O.make_hp("rbf", 1.0, np.array([0.3]), 0.05)
+    m = gp.KernelModel("rbf", 1.0, np.array([0.3]), 0.05)
+    cache = gp.build_cache(m, X, y, precond_rank=250)
+    Xt = rng.uniform(size=(40, d))
+    got, _ = gp.predict_variance(cache, Xt, precond_rank=250, tolerance=1e-6)
+    ref, _ = O.predict_variance(hp, X, Xt, tol=1e-6, rank=250)
+    np.testing.assert_allclose(got, ref, rtol=1e-4, atol=1e-6)
+    pc = likelihood.build_kernel_preconditioner(m, D.points(X), 500)
+    B = D.to_device(rng.standard_normal((n, 64)))
+    op = likelihood.training_operator(m, D.points(X))
+    with pytest.raises(ValueError, match="shared memory"):
+        CG.mbcg_device(op, B, 1e-3, 100, pc)
