@@ -208,3 +208,67 @@ def test_bench_two_ranks_end_to_end():
     assert cb["reduce_scatter"] == 8 * 2 * m * t + 4 * 2 * m   # int64 sums + int32 row flags
     assert cb["all_gather"] == 4 * 2 * m * 12                   # fp32 P rows (ld 12)
     assert line["roofline"]["bound"] == "sfu"
+
+
+def _nccl_rank_main(rank, world, port, outdir):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    import paper_1903_08114_b200 as gp
+    from paper_1903_08114_b200 import _device as D, _ops, likelihood, sharded, synthetic as syn
+    from paper_1903_08114_b200.distributed import TorchComm
+    n, d = 20000, 8
+    X = syn.whitened_inputs(n, d, 0)
+    y = syn.rff_target(X, seed=1)
+    model = gp.KernelModel("matern32", 1.0, np.linspace(0.75, 1.5, d), 0.1)
+    comm = TorchComm(n)
+    assert comm.backend == "nccl"
+    cfg = likelihood.CgConfig(tolerance=0.01, probes=10, precond_rank=50)
+    res = sharded.mll_value_and_grad_sharded(model, X, y, cfg, 3, comm)
+    # the symmetric operator's exchange on NCCL: reduce-scatter of the int64
+    # sums, all-gather of the fp32 directions
+    ps = D.points(X)
+    Xs32, _ = ps.scaled(model.lengthscales)
+    op = _ops.SymShardedKernelOperator(model.family_code, d, Xs32, 1.0, 0.1, 0, comm, force=True)
+    V = torch.from_numpy(np.random.default_rng(5).standard_normal((n, 11)).astype(np.float32)).cuda()
+    kv = op.apply32(V, 11).cpu().numpy()
+    np.savez(os.path.join(outdir, f"n{rank}.npz"), value=res.value, iters=res.diagnostics.iterations,
+             grads=np.array(list(res.gradients.values())), kv=kv, rs=comm.bytes["reduce_scatter"],
+             ag=comm.bytes["all_gather"], ar=comm.bytes["all_reduce"])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_nccl_collectives_world_one_match_single_device():
+    """The NCCL branch of the exchange (all_gather_into_tensor,
+    reduce_scatter_tensor, all_reduce on CUDA tensors) executed for real: one
+    rank on the one GPU of the test box (NCCL refuses two ranks on one GPU),
+    the sharded MLL and symmetric operator against the single-device path."""
+    import torch
+    import torch.multiprocessing as mp
+    import paper_1903_08114_b200 as gp
+    from paper_1903_08114_b200 import _device as D, _ops, likelihood, synthetic as syn
+    with tempfile.TemporaryDirectory() as d:
+        port = 29700 + os.getpid() % 1000
+        mp.spawn(_nccl_rank_main, args=(1, port, d), nprocs=1, join=True)
+        o = np.load(os.path.join(d, "n0.npz"))
+    n, dd = 20000, 8
+    X = syn.whitened_inputs(n, dd, 0)
+    y = syn.rff_target(X, seed=1)
+    model = gp.KernelModel("matern32", 1.0, np.linspace(0.75, 1.5, dd), 0.1)
+    cfg = likelihood.CgConfig(tolerance=0.01, probes=10, precond_rank=50)
+    ref = gp.mll_value_and_grad(model, X, y, gp.plan_partitions(n, 2000), gp.WorkerPool(), cfg, 3)
+    assert int(o["iters"]) == ref.diagnostics.iterations
+    assert float(o["value"]) == pytest.approx(ref.value, rel=1e-9)
+    # the sharded gradient pass runs row shards of the full square (the
+    # single device the symmetric schedule): fp32 forms summed differently
+    gref = np.array(list(ref.gradients.values()))
+    np.testing.assert_allclose(o["grads"], gref, rtol=0, atol=1e-5 * np.abs(gref).max())
+    ps = D.points(X)
+    Xs32, _ = ps.scaled(model.lengthscales)
+    op = _ops.FusedKernelOperator(model.family_code, dd, Xs32, Xs32, 1.0, 0.1, 0, algo=3, self_offset=0)
+    V = torch.from_numpy(np.random.default_rng(5).standard_normal((n, 11)).astype(np.float32)).cuda()
+    np.testing.assert_array_equal(o["kv"], op.apply32(V, 11).cpu().numpy())   # bitwise
+    assert int(o["rs"]) > 0 and int(o["ag"]) > 0 and int(o["ar"]) > 0
