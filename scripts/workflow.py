@@ -2,7 +2,7 @@
 (blockgp-compatible): MLL + gradients, prediction cache, predictive mean and
 variance, for a BASELINE.json configuration. Prints one JSON line per stage.
 
-python scripts/workflow.py C2 [--m 1000] [--skip-variance] [--skip-cache]
+python scripts/workflow.py C2 [--m 1000] [--skip-variance] [--skip-cache] [--train] [--love RANK]
 """
 
 import json
@@ -64,6 +64,14 @@ def main():
                          lambda: predictor.predict_variance(cache, Xt, precond_rank=w.rank), m=m_test)
     print(json.dumps({"stage": "pred_summary", "mean_abs": float(np.abs(mean).mean()),
                       "var_min": float(var.min()), "var_max": float(var.max()), "clamped": clamped}), flush=True)
+    if "--love" in sys.argv:
+        from paper_1903_08114_b200 import love
+        rank = int(sys.argv[sys.argv.index("--love") + 1])
+        lc = timed(f"build_love_cache(rank={rank})", lambda: love.build_love_cache(model, X, rank=rank))
+        lv, _ = timed("predict_variance_love", lambda: love.predict_variance_love(lc, Xt), m=m_test)
+        print(json.dumps({"stage": "love_vs_cg", "max_abs_diff": float(np.abs(lv - var).max()),
+                          "median_abs_diff": float(np.median(np.abs(lv - var))),
+                          "mean_var": float(var.mean())}), flush=True)
 
 
 if __name__ == "__main__":
