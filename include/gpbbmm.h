@@ -220,6 +220,13 @@ int gp_mbcg_update(gp_mbcg* s, const void* Q, int64_t ldq, int q_is_f64, int ite
                    void* stream);
 int gp_mbcg_precond(gp_mbcg* s, int iteration, double tolerance, void* stream);
 int gp_mbcg_direction(gp_mbcg* s, int iteration, void* stream);
+/* The complete single-device solve after gp_mbcg_init_{a,b,c}: iterations of
+ * gp_kv (desc applied to P32 into Q32; desc must be the square operator of
+ * this state's n rows, noise added by the phases) and the four phases until
+ * every column is frozen or max_iters; *iterations_out = iterations run.
+ * The reference's mbcg_solve (cg.py:84-164) with a kernel operator. */
+int gp_mbcg_solve_kv(gp_mbcg* s, const gp_kv_desc* desc, float* Q32, int64_t ldq, void* kv_ws, size_t kv_ws_bytes,
+                     double tolerance, int32_t* iterations_out, void* stream);
 
 /* ---- column reductions / low-rank products (fp64) ----------------------- */
 /* out[j] = sum_i A[i,j] * B[i,j], deterministic fixed-order reduction */

@@ -83,6 +83,8 @@ _SIGS = {
     "gp_grad_forms": (C.c_int, [C.c_int, C.c_int, C.c_int, c_p, c_i64, c_i64, c_p, c_i64, c_i64,
                                 c_f64, c_p, c_i64, c_p, c_i64, C.c_int, c_i64, C.c_int, c_p, c_p,
                                 c_sz, c_p]),
+    "gp_mbcg_solve_kv": (C.c_int, [C.POINTER(MbcgState), C.POINTER(KvDesc), c_p, c_i64, c_p, c_sz, c_f64,
+                                   C.POINTER(c_i32), c_p]),
     "gp_column_moments_workspace_len": (c_i64, [c_i64, C.c_int]),
     "gp_column_moments": (C.c_int, [c_p, c_i64, c_i64, C.c_int, c_p, c_p, c_p, C.c_int, c_p, c_i64, c_p]),
     "gp_standardize": (C.c_int, [c_p, c_i64, c_i64, C.c_int, c_p, c_p, c_p, c_i64, c_p]),

@@ -367,9 +367,31 @@ class MbcgRun:
         return n_active
 
     def run(self) -> "DeviceSolve":
+        if self._c_loop_ok():
+            return self._run_c_loop()
         while self.iterations < self.max_iters:
             if self.step() == 0:
                 break
+        return self.finish()
+
+    def _c_loop_ok(self) -> bool:
+        """Single device, fused fp32 operator over this state's own rows:
+        the whole iteration loop runs in the library (gp_mbcg_solve_kv)."""
+        kv = getattr(self.mvm, "kv", None)
+        return (self.comm.world == 1 and self.fused and not self.f64 and isinstance(self.ph, CudaPhases)
+                and self.kv_events is None and isinstance(kv, _ops.FusedKernelOperator)
+                and kv.n_rows == self.n and kv.n_cols == self.n)
+
+    def _run_c_loop(self) -> "DeviceSolve":
+        kv, ph, t = self.mvm.kv, self.ph, self.t
+        lib = _lib.lib()
+        nbytes = lib.gp_kv_workspace_bytes(kv.desc, t)
+        ws = _ops.workspace().bytes("kv", nbytes) if nbytes else None
+        its = _lib.C.c_int32(0)
+        _lib.check(lib.gp_mbcg_solve_kv(ph.sp, _lib.C.byref(kv.desc), _lib.ptr(self.Q), self.Q.stride(0),
+                                        _lib.ptr(ws) if ws is not None else 0, int(nbytes), float(self.tol),
+                                        _lib.C.byref(its), _lib.stream_handle()), "gp_mbcg_solve_kv")
+        self.iterations = int(its.value)
         return self.finish()
 
     def finish(self) -> "DeviceSolve":

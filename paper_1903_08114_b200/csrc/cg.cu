@@ -1341,6 +1341,39 @@ int gp_mbcg_precond(gp_mbcg* s, int iteration, double tolerance, void* stream) {
   return GP_OK;
 }
 
+/* The whole single-device solve in one call (iterations after init_a/b/c):
+ * per iteration gp_kv (P32 -> Q32) and the four phases, with one 16-byte
+ * status read; the host loop stays in C, so a small-n solve pays ~10 kernel
+ * launches per iteration instead of five Python round trips. */
+int gp_mbcg_solve_kv(gp_mbcg* s, const gp_kv_desc* desc, float* Q32, int64_t ldq, void* kv_ws, size_t kv_ws_bytes,
+                     double tolerance, int32_t* iterations_out, void* stream) {
+  if (int rc = check_state(s)) return rc;
+  GP_REQUIRE(desc != nullptr && iterations_out != nullptr, "gp_mbcg_solve_kv: null argument");
+  GP_REQUIRE(desc->n_rows == s->n && desc->n_cols == s->n, "gp_mbcg_solve_kv: operator is %lld x %lld, state n=%lld",
+             (long long)desc->n_rows, (long long)desc->n_cols, (long long)s->n);
+  cudaStream_t st = (cudaStream_t)stream;
+  static thread_local int32_t* hstat = nullptr;
+  if (!hstat) GP_CUDA_TRY(cudaMallocHost(&hstat, 8 * sizeof(int32_t)));
+  int it = 0;
+  *iterations_out = 0;
+  while (it < s->max_iters) {
+    ++it;
+    if (int rc = gp_kv(desc, s->P32, s->ld32, s->t, Q32, ldq, kv_ws, kv_ws_bytes, stream)) return rc;
+    if (int rc = gp_mbcg_pv(s, Q32, ldq, 0, stream)) return rc;
+    if (int rc = gp_mbcg_update(s, Q32, ldq, 0, it, stream)) return rc;
+    if (int rc = gp_mbcg_precond(s, it, tolerance, stream)) return rc;
+    GP_CUDA_TRY(cudaMemcpyAsync(hstat, s->status, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    GP_CUDA_TRY(cudaStreamSynchronize(st));
+    *iterations_out = it;
+    if (hstat[1] < s->t)
+      return set_error(GP_ENOTPD, "operator is not positive definite: p^T A p <= 0 for column %d at iteration %d",
+                       hstat[1], hstat[2]);
+    if (hstat[0] == 0) break;
+    if (int rc = gp_mbcg_direction(s, it, stream)) return rc;
+  }
+  return GP_OK;
+}
+
 int gp_mbcg_direction(gp_mbcg* s, int iteration, void* stream) {
   if (int rc = check_state(s)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
