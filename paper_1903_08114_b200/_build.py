@@ -48,8 +48,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose:
             sys.stderr.write(r.stderr)
-        with open(obj + ".ptxas.txt", "w") as fh:
-            fh.write(r.stderr)
+        with open(obj + ".ptxas.txt", "w") as fh:   # without the (varying) compile times
+            fh.write("".join(l for l in r.stderr.splitlines(True) if "Compile time" not in l))
         objs.append(obj)
     cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-Xlinker", "--no-undefined"]
     r = subprocess.run(cmd, capture_output=True, text=True)
