@@ -17,9 +17,20 @@ def torch():
     return _t
 
 
+_devices = {}
+
+
 def device():
-    _lib.lib()  # raises if the CUDA library or a device is missing
-    return torch().device("cuda", torch().cuda.current_device())
+    """The current CUDA device (raises if the CUDA library or a device is
+    missing)."""
+    T = torch()
+    idx = T._C._cuda_getDevice() if _devices else None
+    dev = _devices.get(idx)
+    if dev is None:
+        _lib.lib()
+        idx = T.cuda.current_device()
+        dev = _devices[idx] = T.device("cuda", idx)
+    return dev
 
 
 def is_tensor(x) -> bool:

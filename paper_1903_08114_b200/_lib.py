@@ -151,5 +151,9 @@ def ptr(t) -> int:
 
 
 def stream_handle(device=None) -> int:
+    """The current CUDA stream of `device` (default: the current device) as
+    a raw handle, without building a torch Stream object per call."""
     import torch
+    if device is None:
+        return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
     return torch.cuda.current_stream(device).cuda_stream

@@ -17,10 +17,10 @@ Operators (`mvm`):
 from __future__ import annotations
 
 import math
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
-import scipy.linalg
 
 from . import _device as D
 from . import _lib
@@ -180,6 +180,18 @@ class DeviceSolve:
         return [_tridiagonal(a, b) for a, b in zip(self.alphas, self.betas)]
 
 
+_pinned = threading.local()
+
+
+def _pinned_status():
+    """A pinned 4 x int32 host buffer for the per-iteration status read,
+    allocated once per thread (pinned allocations are slow)."""
+    buf = getattr(_pinned, "status", None)
+    if buf is None:
+        buf = _pinned.status = D.torch().zeros(4, dtype=D.torch().int32).pin_memory()
+    return buf
+
+
 class CudaPhases:
     """The mBCG phase kernels of the C ABI (gp_mbcg_*) on this device's rows,
     owning the solver state in HBM. MbcgRun drives it; tests substitute a
@@ -194,13 +206,17 @@ class CudaPhases:
         self.n, self.t, self.k = n, t, k
         self.ld32 = ld32 = (t + 3) // 4 * 4
         f64 = dict(dtype=T.float64, device=dev)
-        self.U, self.R, self.P, self.Z = (T.empty((n, t), **f64) for _ in range(4))
+        self.U = T.empty((n, t), **f64)   # the solution (handed to the caller)
+        self.R, self.P, self.Z = T.empty((3, n, t), **f64).unbind(0)
         self.P32 = T.zeros((max(rows32, n), ld32), dtype=T.float32, device=dev)
-        self.red = T.zeros(3 * t + k * t, **f64)
-        self.cbuf = T.zeros(max(k * t, 1), **f64)
-        self.hist = T.zeros((3, max_iters, t), **f64)  # alpha, beta, rel
-        self.vec = T.zeros((3, t), **f64)  # bnorm, gamma, rel
-        self.ints = T.zeros(2 * t + 4, dtype=T.int32, device=dev)
+        # the small state in one zero-filled allocation (one fill per solve)
+        sizes = [3 * t + k * t, max(k * t, 1), 3 * max_iters * t, 3 * t, (2 * t + 4 + 1) // 2]
+        small = T.zeros(sum(sizes), **f64)
+        red, cbuf, hist, vec, ints = small.split(sizes)
+        self.red, self.cbuf = red, cbuf
+        self.hist = hist.view(3, max_iters, t)  # alpha, beta, rel
+        self.vec = vec.view(3, t)  # bnorm, gamma, rel
+        self.ints = ints.view(T.int32)[:2 * t + 4]
         plen = int(self.lib.gp_mbcg_partials_len(n, t, k))
         self.partials = _ops.workspace().f64("mbcg_partials", plen)
         self.state = _lib.MbcgState(
@@ -216,7 +232,7 @@ class CudaPhases:
             converged=_lib.ptr(self.ints[t:2 * t]), status=_lib.ptr(self.ints[2 * t:]),
             partials=_lib.ptr(self.partials), partials_len=plen, max_iters=max_iters, nblocks=0)
         self.sp = _lib.C.byref(self.state)
-        self.status_host = T.zeros(4, dtype=T.int32).pin_memory()
+        self.status_host = _pinned_status()
 
     def init_a(self, B):
         _lib.check(self.lib.gp_mbcg_init_a(self.sp, _lib.ptr(B), B.stride(0), self.st), "gp_mbcg_init_a")
@@ -257,8 +273,12 @@ class CudaPhases:
         return int(s[0]), int(s[1]), int(s[2])
 
     def history(self, its):
-        return (D.to_host(self.hist[:, :its]), D.to_host(self.vec[2]),
-                D.to_host(self.ints[self.t:2 * self.t]).astype(bool))
+        """(alpha/beta/rel history, final rel, converged) in one device->host read."""
+        T, t = self.T, self.t
+        flat = D.to_host(T.cat([self.hist[:, :its].reshape(-1), self.vec[2],
+                                self.ints[t:2 * t].to(T.float64)]))
+        h = 3 * its * t
+        return flat[:h].reshape(3, its, t), flat[h:h + t].copy(), flat[h + t:] != 0
 
 
 class MbcgRun:
@@ -465,16 +485,30 @@ def slq_logdet(report, preconditioner: PreconditionerCache | None = None, column
     n = (report.solutions.shape[0] if isinstance(report, SolveReport) else report.U.shape[0])
     if n_total is not None:
         n = int(n_total)
+    # the small eigenproblems of equal order in one batched LAPACK call
+    # (the per-column terms are then summed in column order, as before)
+    terms = {}
+    by_order = {}
+    for j in cols:
+        if tris[j].order == 0:
+            raise NumericError(f"column {j} has an empty recurrence")
+        by_order.setdefault(tris[j].order, []).append(j)
+    for m, js in by_order.items():
+        if m == 1:
+            for j in js:
+                terms[j] = (tris[j].diag.copy(), np.ones(1))
+            continue
+        A = np.zeros((len(js), m, m))
+        idx = np.arange(m)
+        for g, j in enumerate(js):
+            A[g, idx, idx] = tris[j].diag
+            A[g, idx[1:], idx[:-1]] = tris[j].offdiag
+        lam, vecs = np.linalg.eigh(A)   # lower triangle
+        for g, j in enumerate(js):
+            terms[j] = (lam[g], vecs[g, 0, :] ** 2)
     total = 0.0
     for j in cols:
-        Tj = tris[j]
-        if Tj.order == 0:
-            raise NumericError(f"column {j} has an empty recurrence")
-        if Tj.order == 1:
-            lam, w = Tj.diag.copy(), np.ones(1)
-        else:
-            lam, vecs = scipy.linalg.eigh_tridiagonal(Tj.diag, Tj.offdiag)
-            w = vecs[0, :] ** 2
+        lam, w = terms[j]
         if np.any(lam <= 0):
             raise NumericError(f"tridiagonal for column {j} has a non-positive eigenvalue; "
                                "the operator is not positive definite or the recurrence broke down")

@@ -279,16 +279,27 @@ __global__ void __launch_bounds__(kRT) cg_init_a(CgK s, const double* __restrict
 }
 
 // c = B^{-1} (L^T R) for the given columns (one output per thread, k-long dots)
+// C = B^{-1} (L^T R): one warp per output (kk, c), the length-k dot split
+// over the lanes and reduced by shuffles (fixed order)
 __global__ void cg_cvec(CgK s, int use_active) {
   const int t = s.t, k = s.k;
   const double* ltr = s.red + off_ltr(t);
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < k * t; p += gridDim.x * blockDim.x) {
-    int kk = p / t, c = p - kk * t;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t p = w0; p < (int64_t)k * t; p += nw) {
+    const int kk = (int)(p / t), c = (int)(p - (int64_t)kk * t);
     double acc = 0.0;
     if (!use_active || s.active[c])
-      for (int l = 0; l < k; ++l) acc = fma(s.Binv[kk * k + l], ltr[l * t + c], acc);
-    s.cbuf[p] = acc;
+      for (int l = lane; l < k; l += 32) acc = fma(s.Binv[kk * k + l], ltr[l * t + c], acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) s.cbuf[p] = acc;
   }
+}
+
+static unsigned cvec_blocks(int k, int t) {   // 8 warps per block, one warp per output
+  return (unsigned)std::max(1, std::min((k * t + 7) / 8, 4 * num_sms()));
 }
 
 // Z = P^{-1} R on (active) columns; partial gam = sum R o Z.
@@ -951,88 +962,94 @@ __global__ void __launch_bounds__(256) lowrank_wide(int64_t n, int k, const doub
 // (precond.py:114-122, :165-174). Single block, the k x k matrix in shared
 // memory (k <= 160), so the k column steps and the substitution run at SMEM
 // latency; C is written back for the caller.
+__device__ __forceinline__ double block_sum_1024(double v, double* sred) {
+  // fixed-order tree: warp shuffles, then warp 0 over the 32 warp sums
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? sred[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  }
+  __syncthreads();
+  return s;   // valid in warp 0
+}
+
 __global__ void __launch_bounds__(1024) precond_factor_kernel(int k, double noise, double* C, double* Binv,
                                                               double* out, int* info) {
-  extern __shared__ double Cs[];   // [k][k]
+  extern __shared__ double Cs[];   // [k][k]: lower = factor, strict upper (transposed) = inverse work
   __shared__ int fail;
-  __shared__ double sred[1024];
-  if (threadIdx.x == 0) fail = 0;
-  for (int p = threadIdx.x; p < k * k; p += blockDim.x) {
+  __shared__ double sred[32];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (tid == 0) fail = 0;
+  for (int p = tid; p < k * k; p += nt) {
     const int i = p / k, j = p - i * k;
     Cs[p] = C[p] + (i == j ? noise : 0.0);
   }
   __syncthreads();
+  // right-looking Cholesky with one barrier per column: step j updates the
+  // trailing lower triangle with the unscaled column j over d_jj and scales
+  // column j - 1 (which no thread reads in step j)
+  double dprev = 1.0;
   for (int j = 0; j < k; ++j) {
-    if (threadIdx.x == 0) {
-      const double djj = Cs[j * k + j];
-      if (!(djj > 0.0) || !isfinite(djj)) fail = 1;
-      Cs[j * k + j] = sqrt(fmax(djj, 0.0));
+    const double djj = Cs[j * k + j];
+    if (tid == 0 && (!(djj > 0.0) || !isfinite(djj))) fail = 1;
+    if (j >= 1) {
+      const double rs = 1.0 / sqrt(dprev);
+      for (int i = j + tid; i < k; i += nt) Cs[i * k + j - 1] *= rs;
+      if (tid == 0) Cs[(j - 1) * k + j - 1] = sqrt(dprev);
     }
-    __syncthreads();
-    if (fail) break;
-    const double cjj = Cs[j * k + j];
-    for (int i = j + 1 + threadIdx.x; i < k; i += blockDim.x) Cs[i * k + j] /= cjj;
-    __syncthreads();
+    const double inv = 1.0 / djj;
     const int m = k - j - 1;
-    for (int p = threadIdx.x; p < m * m; p += blockDim.x) {
+    for (int p = tid; p < m * m; p += nt) {
       const int i = j + 1 + p / m, l = j + 1 + p % m;
-      if (l <= i) Cs[i * k + l] -= Cs[i * k + j] * Cs[l * k + j];
+      if (l <= i) Cs[i * k + l] -= Cs[i * k + j] * Cs[l * k + j] * inv;
     }
+    dprev = djj;
     __syncthreads();
   }
+  if (tid == 0) Cs[(k - 1) * k + k - 1] = sqrt(dprev);
+  __syncthreads();
   if (fail) {
-    if (threadIdx.x == 0) info[0] = 1;
+    if (tid == 0) info[0] = 1;
     return;
   }
-  for (int p = threadIdx.x; p < k * k; p += blockDim.x) {
-    const int i = p / k, j = p - i * k;
-    if (j > i) Cs[p] = 0.0;
-    C[p] = j > i ? 0.0 : Cs[p];
+  // X = C^{-1} (lower), right-looking: W starts as I; step i finalises row i
+  // (X[i][c] = W[i][c] / C_ii) and subtracts C[r][i] X[i][:] from every row
+  // r > i. W[r][c] (c < r) lives at Cs[c k + r], the strict upper triangle;
+  // consecutive threads take consecutive r (conflict-free stores)
+  for (int p = tid; p < k * k; p += nt) {
+    const int c = p / k, r = p - c * k;
+    if (r > c) Cs[p] = 0.0;
   }
   __syncthreads();
-  // X = C^{-1} (lower) row by row: X[i, c] = (delta_ic - sum_{c<=l<i} C[i,l]
-  // X[l,c]) / C[i,i] for every c <= i in parallel; X overwrites the strict
-  // upper triangle's storage transposed (Xt[c][i] at Cs[c * k + i], c < i)
-  // and its diagonal goes to a separate SMEM vector
-  double* xd = sred;   // X[i][i], i < k <= 160 (reuses the reduction buffer)
-  for (int i = 0; i < k; ++i) {
-    const double cii = Cs[i * k + i];
-    for (int c = threadIdx.x; c <= i; c += blockDim.x) {
-      double s = 0.0;
-      if (c == i) {
-        xd[i] = 1.0 / cii;
-      } else {
-        s = -Cs[i * k + c] * xd[c];   // l = c
-        for (int l = c + 1; l < i; ++l) s = fma(-Cs[i * k + l], Cs[c * k + l], s);
-        Cs[c * k + i] = s / cii;
-      }
+  for (int i = 0; i + 1 < k; ++i) {
+    const double rinv = 1.0 / Cs[i * k + i];
+    const int m = k - 1 - i;
+    for (int p = tid; p < m * (i + 1); p += nt) {
+      const int c = p / m, r = i + 1 + (p - c * m);
+      const double xic = (c == i ? 1.0 : Cs[c * k + i]) * rinv;
+      Cs[c * k + r] -= Cs[r * k + i] * xic;
     }
     __syncthreads();
   }
-  double tr = 0.0;
-  for (int p = threadIdx.x; p < k * k; p += blockDim.x) {
+  // X out (scaled rows) to Binv, tr(B^{-1}) = ||X||_F^2, logdet = 2 sum log C_jj
+  double tr = 0.0, ld = 0.0;
+  for (int p = tid; p < k * k; p += nt) {
     const int i = p / k, c = p - i * k;
-    const double x = c > i ? 0.0 : (c == i ? xd[i] : Cs[c * k + i]);
+    const double cii = Cs[i * k + i];
+    const double x = c > i ? 0.0 : (c == i ? 1.0 / cii : Cs[c * k + i] / cii);
     Binv[p] = x;
+    C[p] = c > i ? 0.0 : Cs[p];
     tr += x * x;
   }
-  __syncthreads();
-  double ld = 0.0;
-  for (int j = threadIdx.x; j < k; j += blockDim.x) ld += log(Cs[j * k + j]);
-  sred[threadIdx.x] = tr;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int q = 0; q < (int)blockDim.x; ++q) s += sred[q];
-    out[1] = s;
-  }
-  __syncthreads();
-  sred[threadIdx.x] = ld;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int q = 0; q < (int)blockDim.x; ++q) s += sred[q];
-    out[0] = 2.0 * s;
+  for (int j = tid; j < k; j += nt) ld += log(Cs[j * k + j]);
+  const double trs = block_sum_1024(tr, sred);
+  const double lds = block_sum_1024(ld, sred);
+  if (tid == 0) {
+    out[1] = trs;
+    out[0] = 2.0 * lds;
     info[0] = 0;
   }
 }
@@ -1117,7 +1134,7 @@ __global__ void xtx_kernel(int k, const double* __restrict__ X, double* out) {
 
 static int cg_nblocks(const gp_mbcg* s) {
   if (s->nblocks > 0) return s->nblocks;
-  int64_t nb = std::min<int64_t>(3 * num_sms(), (s->n + 63) / 64);   // 3 resident blocks per SM
+  int64_t nb = std::min<int64_t>(3 * num_sms(), (s->n + 31) / 32);   // 3 resident blocks per SM, >= 32 rows each
   return (int)std::max<int64_t>(nb, 1);
 }
 
@@ -1176,10 +1193,14 @@ static int set_smem(K kern, size_t bytes) {
 
 using namespace gp;
 
+namespace gp {
+thread_local bool kv_images_current = false;
+}
+
 extern "C" {
 
 int64_t gp_mbcg_partials_len(int64_t n, int t, int k) {
-  int64_t nb = std::min<int64_t>(3 * num_sms(), (n + 63) / 64);
+  int64_t nb = std::min<int64_t>(3 * num_sms(), (n + 31) / 32);
   nb = std::max<int64_t>(nb, 1);
   return nb * (3 * (int64_t)t + (int64_t)k * t);
 }
@@ -1208,7 +1229,7 @@ int gp_mbcg_init_b(gp_mbcg* s, void* stream) {
   cg_bnorm<<<1, 256, 0, st>>>(v);
   GP_LAUNCH_CHECK();
   if (k > 0 && s->pc_noise > 0.0) {
-    cg_cvec<<<(k * t + 255) / 256, 256, 0, st>>>(v, 0);
+    cg_cvec<<<cvec_blocks(k, t), 256, 0, st>>>(v, 0);
     GP_LAUNCH_CHECK();
   }
   if (s->n > 0 && use_wide(s)) {
@@ -1306,7 +1327,7 @@ int gp_mbcg_precond(gp_mbcg* s, int iteration, double tolerance, void* stream) {
   cg_freeze<<<1, 256, 0, st>>>(v, iteration, tolerance);
   GP_LAUNCH_CHECK();
   if (k > 0 && s->pc_noise > 0.0) {
-    cg_cvec<<<(k * t + 255) / 256, 256, 0, st>>>(v, 1);
+    cg_cvec<<<cvec_blocks(k, t), 256, 0, st>>>(v, 1);
     GP_LAUNCH_CHECK();
   }
   if (s->n > 0 && use_wide(s)) {
@@ -1356,9 +1377,15 @@ int gp_mbcg_solve_kv(gp_mbcg* s, const gp_kv_desc* desc, float* Q32, int64_t ldq
   if (!hstat) GP_CUDA_TRY(cudaMallocHost(&hstat, 8 * sizeof(int32_t)));
   int it = 0;
   *iterations_out = 0;
+  struct ImagesScope {   // the flag never outlives this call
+    ~ImagesScope() { kv_images_current = false; }
+  } images_scope;
   while (it < s->max_iters) {
     ++it;
+    // iterations after the first reuse the distance images in kv_ws
+    kv_images_current = it > 1;
     if (int rc = gp_kv(desc, s->P32, s->ld32, s->t, Q32, ldq, kv_ws, kv_ws_bytes, stream)) return rc;
+    kv_images_current = false;
     if (int rc = gp_mbcg_pv(s, Q32, ldq, 0, stream)) return rc;
     if (int rc = gp_mbcg_update(s, Q32, ldq, 0, it, stream)) return rc;
     if (int rc = gp_mbcg_precond(s, it, tolerance, stream)) return rc;

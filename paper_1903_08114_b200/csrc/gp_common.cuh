@@ -12,6 +12,12 @@ namespace gp {
 
 int set_error(int code, const char* fmt, ...);
 
+// Set by a caller that applies the same operator (same points, same
+// workspace) repeatedly — the mBCG loop of gp_mbcg_solve_kv from its second
+// iteration on: the K·V kernels then keep the distance images already in the
+// workspace instead of rebuilding them from the points.
+extern thread_local bool kv_images_current;
+
 #define GP_CUDA_TRY(expr)                                                        \
   do {                                                                           \
     cudaError_t _e = (expr);                                                     \

@@ -926,9 +926,10 @@ int kv_sym_partial(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, i
   GP_CUDA_TRY(cudaMemsetAsync(bad, 0, p.bad_bytes, st));
   sym_scale_kernel<<<kScaleCtas, 1024, 0, st>>>(V, ldv, n, t, w.expo, w.vscale, w.inv_scale);
   GP_LAUNCH_CHECK();
-  if (int rc = tc::distance_images(desc->Xr, desc->ldr, n, desc->Xc, desc->ldc, n, desc->d, p.DK, BT, BT, c,
-                                   w.mean, w.row_img, w.col_img, st))
-    return rc;
+  if (!kv_images_current)
+    if (int rc = tc::distance_images(desc->Xr, desc->ldr, n, desc->Xc, desc->ldc, n, desc->d, p.DK, BT, BT, c,
+                                     w.mean, w.row_img, w.col_img, st))
+      return rc;
   // the 128-point V image is two consecutive 64-point tile images
   if (int rc = tc::v_images16(V, ldv, t, n, w.vscale, w.v_img, 2 * (int64_t)p.tiles, st)) return rc;
   Args a;

@@ -752,9 +752,10 @@ int kv_tc(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out
   float* split_ws = reinterpret_cast<float*>(w);
   const double c = desc->family == GP_FAMILY_RBF ? 1.4426950408889634 : -6.0;
   {
-    if (int rc = distance_images(desc->Xr, desc->ldr, desc->n_rows, desc->Xc, desc->ldc, desc->n_cols,
-                                 desc->d, p.DK, BM, BN, c, mean, row_img, col_img, st))
-      return rc;
+    if (!kv_images_current)
+      if (int rc = distance_images(desc->Xr, desc->ldr, desc->n_rows, desc->Xc, desc->ldc, desc->n_cols,
+                                   desc->d, p.DK, BM, BN, c, mean, row_img, col_img, st))
+        return rc;
     if (KV_F16) {
       if (int rc = v_colscale(V, ldv, desc->n_cols, t, vscale, inv_vscale, st)) return rc;
       if (int rc = v_images16(V, ldv, t, desc->n_cols, vscale, static_cast<__half*>(v_img), p.col_tiles, st))

@@ -347,11 +347,19 @@ __global__ void __launch_bounds__(kPivThreads) pivchol_cluster_smem(PivArgs a, i
     }
     if (lane == 0) { sv[w] = v; si[w] = i; }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      double x = -INFINITY; int64_t y = INT64_MAX;
-      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) better(x, y, sv[q], si[q]);
-      slot_v[slot] = x;
-      slot_i[slot] = y;
+    if (w == 0) {   // the warp partials, reduced by warp 0 (same choice in any order)
+      double x = lane < (int)(blockDim.x >> 5) ? sv[lane] : -INFINITY;
+      int64_t y = lane < (int)(blockDim.x >> 5) ? si[lane] : INT64_MAX;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        double ox = __shfl_xor_sync(0xffffffffu, x, o);
+        int64_t oy = __shfl_xor_sync(0xffffffffu, y, o);
+        better(x, y, ox, oy);
+      }
+      if (lane == 0) {
+        slot_v[slot] = x;
+        slot_i[slot] = y;
+      }
     }
   };
   reduce_store(bv, bi, 1);
@@ -371,6 +379,24 @@ __global__ void __launch_bounds__(kPivThreads) pivchol_cluster_smem(PivArgs a, i
         int64_t oi = __shfl_xor_sync(0xffffffffu, i, o);
         better(v, i, ov, oi);
       }
+      // every lane holds the choice: warp 0 also fetches the pivot's point
+      // and L row from the owning CTA, so one block barrier serves both
+      if (v > 0.0) {
+        const int owner = (int)(i / rpc), lr = (int)(i - (int64_t)owner * rpc);
+        const double* xo = cl.map_shared_rank(Xs, owner) + (size_t)lr * a.d;
+        const double* lo = cl.map_shared_rank(Ls, owner) + (size_t)lr * lds;
+        // up to 4 x 32 values: the remote loads issue together, then the stores
+        double pv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int q = lane + 32 * u;
+          pv[u] = q < a.d + j ? (q < a.d ? xo[q] : lo[q - a.d]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (lane + 32 * u < a.d + j) sp[1 + lane + 32 * u] = pv[u];
+        for (int q = lane + 128; q < a.d + j; q += 32) sp[1 + q] = q < a.d ? xo[q] : lo[q - a.d];
+      }
       if (lane == 0) {
         s_stop = !(v > 0.0);
         s_piv = i;
@@ -381,44 +407,57 @@ __global__ void __launch_bounds__(kPivThreads) pivchol_cluster_smem(PivArgs a, i
     __syncthreads();
     if (s_stop) break;
     const int64_t p = s_piv;
-    {
-      const int owner = (int)(p / rpc), lr = (int)(p - (int64_t)owner * rpc);
-      const double* xo = cl.map_shared_rank(Xs, owner) + (size_t)lr * a.d;
-      const double* lo = cl.map_shared_rank(Ls, owner) + (size_t)lr * lds;
-      for (int q = threadIdx.x; q < a.d + j; q += blockDim.x) sp[1 + q] = q < a.d ? xo[q] : lo[q - a.d];
-    }
-    __syncthreads();
     const double inv_sq = 1.0 / sqrt(sp[0]);
     const double* xp = sp + 1;
     const double* lp = sp + 1 + a.d;
     bv = -INFINITY; bi = INT64_MAX;
-    for (int r = grp; r - grp < nr; r += ngrp) {   // warp-uniform trip count (shuffles)
-      const bool in = r < nr;
-      double r2 = 0.0, dot = 0.0;
-      if (in) {
-        const double* xi = Xs + (size_t)r * a.d;
-        for (int q = g; q < a.d; q += 8) {
-          double df = xi[q] - xp[q];
-          r2 = fma(df, df, r2);
+    // two rows per 8-lane group and pass, their SMEM loads and FMA chains
+    // interleaved (the step is latency bound at small n)
+    for (int r = grp; r - grp < nr; r += 2 * ngrp) {   // warp-uniform trip count (shuffles)
+      double r2[2] = {0.0, 0.0}, dot[2] = {0.0, 0.0};
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int ru = r + u * ngrp;
+        if (ru < nr) {
+          const double* xi = Xs + (size_t)ru * a.d;
+          for (int q = g; q < a.d; q += 8) {
+            double df = xi[q] - xp[q];
+            r2[u] = fma(df, df, r2[u]);
+          }
         }
-        const double* li = Ls + (size_t)r * lds;
-        for (int m = g; m < j; m += 8) dot = fma(li[m], lp[m], dot);
+      }
+      {
+        const bool in0 = r < nr, in1 = r + ngrp < nr;
+        const double* l0 = Ls + (size_t)r * lds;
+        const double* l1 = Ls + (size_t)(r + ngrp) * lds;
+        for (int m = g; m < j; m += 8) {
+          const double pm = lp[m];
+          if (in0) dot[0] = fma(l0[m], pm, dot[0]);
+          if (in1) dot[1] = fma(l1[m], pm, dot[1]);
+        }
       }
 #pragma unroll
-      for (int o = 1; o < 8; o <<= 1) {
-        r2 += __shfl_xor_sync(0xffffffffu, r2, o);
-        dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      for (int u = 0; u < 2; ++u) {
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+          r2[u] += __shfl_xor_sync(0xffffffffu, r2[u], o);
+          dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], o);
+        }
       }
-      if (in && g == 0) {
-        const int64_t i = r0 + r;
-        double row = a.s2 * kappa_f64(a.fam, r2);
-        double col = (row - dot) * inv_sq;
-        Ls[(size_t)r * lds + j] = col;
-        double di = ds[r] - col * col;
-        di = di > 0.0 ? di : 0.0;
-        if (i == p) di = 0.0;
-        ds[r] = di;
-        better(bv, bi, di, i);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int ru = r + u * ngrp;
+        if (ru < nr && g == 0) {
+          const int64_t i = r0 + ru;
+          double row = a.s2 * kappa_f64(a.fam, r2[u]);
+          double col = (row - dot[u]) * inv_sq;
+          Ls[(size_t)ru * lds + j] = col;
+          double di = ds[ru] - col * col;
+          di = di > 0.0 ? di : 0.0;
+          if (i == p) di = 0.0;
+          ds[ru] = di;
+          better(bv, bi, di, i);
+        }
       }
     }
     reduce_store(bv, bi, j & 1);

@@ -149,12 +149,15 @@ def mll_value_and_grad(model: KernelModel, X, y, plan: PartitionPlan, pool: Work
     sol = mbcg_device(op, B, cg_config.tolerance, cg_config.max_iters, cache)
     a = sol.U[:, 0].contiguous()
     S = sol.U[:, 1:].contiguous()
+    # y^T a and sum(a) stay on the device until the gradients' read
+    qa_dev = T.stack([_ops.coldot(yc[:, None], a[:, None])[0], a.sum()])
     logdet = slq_logdet(sol, cache, columns=range(1, t + 1))
-    quad = float(_ops.coldot(yc[:, None], a[:, None])[0].item())
-    value = -0.5 * quad - 0.5 * logdet - 0.5 * n * LOG_TWO_PI
     W = _pc.precond_apply_device(cache, Z) if cache is not None else Z
     gradients = _gradients(model, ps, a, S, W, cache)
-    gradients["mean"] = float(a.sum().item())
+    qa = D.to_host(qa_dev)
+    quad = float(qa[0])
+    value = -0.5 * quad - 0.5 * logdet - 0.5 * n * LOG_TWO_PI
+    gradients["mean"] = float(qa[1])
     if not np.isfinite(value) or any(not np.isfinite(g) for g in gradients.values()):
         raise NumericError("non-finite likelihood value or gradient")
     diag = MLLDiagnostics(probe_seed=probe_seed, iterations=sol.iterations,

@@ -107,8 +107,9 @@ def _pivchol_device(src: KernelRowSource, k: int, overlap=None):
                               _lib.stream_handle()), "gp_pivchol")
     if overlap is not None:   # host work while the factorisation runs
         overlap()
-    rank = int(info.item())
-    return PivotedFactor(L[:, :rank], D.to_host(piv[:rank]), resid)
+    host = D.to_host(T.cat([piv, info.to(T.int64)]))   # pivots and rank in one read
+    rank = int(host[k])
+    return PivotedFactor(L[:, :rank], host[:rank].copy(), resid)
 
 
 def partial_pivoted_cholesky(row_fn, diag, k: int, overlap=None) -> PivotedFactor:
@@ -170,8 +171,9 @@ def build_preconditioner(factor, noise: float) -> PreconditionerCache:
                                             _lib.ptr(chol), _lib.ptr(binv), _lib.ptr(out),
                                             _lib.ptr(info), _lib.ptr(part), part.numel(),
                                             _lib.stream_handle()), "gp_precond_factor")
-    vals = D.to_host(out)
-    if int(info.item()) != 0 or not np.all(np.isfinite(vals)):
+    host = D.to_host(T.cat([out, info.to(T.float64)]))   # one device->host read
+    vals = host[:2]
+    if int(host[2]) != 0 or not np.all(np.isfinite(vals)):
         raise NumericError("inner factorization of the preconditioner failed; "
                            "the factor is non-finite or the noise is not positive")
     return PreconditionerCache(L, noise, chol, binv, (n - k) * math.log(noise) + vals[0], vals[1])
