@@ -36,6 +36,7 @@ extern "C" {
 #define GP_ENOTPD 3      /* p^T A p <= 0 / failed chol  -> NumericError      */
 #define GP_ECUDA 4       /* CUDA runtime failure        -> RuntimeError      */
 #define GP_EUNSUPPORTED 5 /* shape outside compiled kernels -> ValueError    */
+#define GP_ENCCL 6       /* NCCL failure                -> RuntimeError      */
 
 #define GP_FAMILY_RBF 0
 #define GP_FAMILY_MATERN32 1
@@ -305,6 +306,30 @@ size_t gp_grad_forms_sym_workspace_bytes(int64_t n, int d, int ard, int w);
 int gp_grad_forms_sym(int family, int d, int ard, const float* X, int64_t ldx, int64_t n, double outputscale,
                       const float* Y, int64_t ldy, const float* R, int64_t ldrr, int w, double* out,
                       void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- single-process multi-GPU collectives (NCCL) ------------------------
+ * One host thread drives every device with NCCL group calls (SURVEY §8(b)
+ * "Collectives"; the reference's equivalent is the thread WorkerPool that
+ * runs the row blocks of one MVM in parallel, partition.py:46-57, :155-183).
+ * The work items of gp_kv_sym_partial are split over the devices and the
+ * fixed-point partial sums reduce-scattered by row, so the product is
+ * bitwise that of one device. NCCL is resolved at run time (libnccl.so.2);
+ * gp_comm_available() reports whether it was found. Array arguments hold one
+ * entry per device of the communicator, in its device order (HOST arrays of
+ * device pointers / cudaStream_t). */
+typedef struct gp_comm gp_comm;
+int gp_comm_available(void);
+int gp_comm_init(int ndev, const int* devices_host, gp_comm** out);
+int gp_comm_destroy(gp_comm* comm);
+int gp_comm_size(const gp_comm* comm);
+int gp_comm_broadcast(gp_comm* comm, void* const* bufs, int64_t bytes, int root, void* const* streams);
+int gp_comm_allgather(gp_comm* comm, const void* const* send, void* const* recv, int64_t bytes_per_rank,
+                      void* const* streams);
+int gp_comm_reduce_scatter_i64(gp_comm* comm, const int64_t* const* send, int64_t* const* recv,
+                               int64_t count_per_rank, void* const* streams);
+int gp_comm_reduce_scatter_i32(gp_comm* comm, const int32_t* const* send, int32_t* const* recv,
+                               int64_t count_per_rank, void* const* streams);
+int gp_comm_allreduce_f64(gp_comm* comm, double* const* bufs, int64_t count, void* const* streams);
 
 #ifdef __cplusplus
 }

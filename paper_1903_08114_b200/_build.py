@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libgpbbmm.so")
-SOURCES = ["kv_simt.cu", "kv_tc.cu", "kv_sym.cu", "kv_wide.cu", "kv_f64.cu", "cg.cu", "pivchol.cu", "grad.cu", "grad_tc.cu", "grad_ard.cu", "data.cu"]
+SOURCES = ["kv_simt.cu", "kv_tc.cu", "kv_sym.cu", "kv_wide.cu", "kv_f64.cu", "cg.cu", "pivchol.cu", "grad.cu", "grad_tc.cu", "grad_ard.cu", "data.cu", "comm.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "--use_fast_math",
          "-Xptxas", "-v"]

@@ -89,6 +89,15 @@ _SIGS = {
     "gp_column_moments": (C.c_int, [c_p, c_i64, c_i64, C.c_int, c_p, c_p, c_p, C.c_int, c_p, c_i64, c_p]),
     "gp_standardize": (C.c_int, [c_p, c_i64, c_i64, C.c_int, c_p, c_p, c_p, c_i64, c_p]),
     "gp_gather_rows": (C.c_int, [c_p, c_i64, c_i64, c_p, c_i64, C.c_int, c_p, c_i64, c_p, c_p]),
+    "gp_comm_available": (C.c_int, []),
+    "gp_comm_init": (C.c_int, [C.c_int, c_p, C.POINTER(c_p)]),
+    "gp_comm_destroy": (C.c_int, [c_p]),
+    "gp_comm_size": (C.c_int, [c_p]),
+    "gp_comm_broadcast": (C.c_int, [c_p, c_p, c_i64, C.c_int, c_p]),
+    "gp_comm_allgather": (C.c_int, [c_p, c_p, c_p, c_i64, c_p]),
+    "gp_comm_reduce_scatter_i64": (C.c_int, [c_p, c_p, c_p, c_i64, c_p]),
+    "gp_comm_reduce_scatter_i32": (C.c_int, [c_p, c_p, c_p, c_i64, c_p]),
+    "gp_comm_allreduce_f64": (C.c_int, [c_p, c_p, c_i64, c_p]),
     "gp_grad_forms_sym_workspace_bytes": (c_sz, [c_i64, C.c_int, C.c_int, C.c_int]),
     "gp_grad_forms_sym": (C.c_int, [C.c_int, C.c_int, C.c_int, c_p, c_i64, c_i64, c_f64, c_p, c_i64, c_p,
                                     c_i64, C.c_int, c_p, c_p, c_sz, c_p]),

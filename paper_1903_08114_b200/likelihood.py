@@ -103,13 +103,20 @@ def draw_probes(n: int, t: int, seed: int, cache) -> np.ndarray:
     return D.to_host(draw_probes_device(n, t, seed, cache))
 
 
-def training_operator(model: KernelModel, ps, algo: int = 0, precision: str = "fp32"):
+def training_operator(model: KernelModel, ps, algo: int = 0, precision: str = "fp32", workers: int = 1,
+                      t: int = 1):
+    """K̂ as the mBCG operator. `workers` > 1 (a WorkerPool's thread count,
+    partition.py:46-57) spans that many GPUs of this process when the host
+    has them (multidev.py); `t` is the right-hand-side count it will see."""
     Xs32, Xs64 = ps.scaled(model.scale_for(ps.d))
     if precision == "fp64":
         return FusedOperator64(_ops.Kv64Operator(model.family_code, ps.d, Xs64, Xs64, model.outputscale),
                                model.noise, ps.n)
     kv = _ops.FusedKernelOperator(model.family_code, ps.d, Xs32, Xs32, model.outputscale, 0.0,
                                   -1, algo=algo, self_offset=0)
+    if workers > 1 and algo == 0:
+        from .multidev import training_operator as multi
+        kv = multi(model.family_code, ps.d, Xs32, model.outputscale, 0.0, -1, workers, t, kv)
     return FusedOperator(kv, model.noise, ps.n)
 
 
@@ -144,7 +151,7 @@ def mll_value_and_grad(model: KernelModel, X, y, plan: PartitionPlan, pool: Work
 
     cache = build_kernel_preconditioner(model, ps, cg_config.precond_rank, overlap=host_draws)
     Z = draw_probes_device(n, t, probe_seed, cache, tuple(draws) if draws else None)
-    op = training_operator(model, ps, precision=cg_config.precision)
+    op = training_operator(model, ps, precision=cg_config.precision, workers=pool.workers, t=t + 1)
     B = T.cat([yc[:, None], Z], dim=1).contiguous()
     sol = mbcg_device(op, B, cg_config.tolerance, cg_config.max_iters, cache)
     a = sol.U[:, 0].contiguous()
