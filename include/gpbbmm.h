@@ -302,6 +302,11 @@ int gp_gather_rows(const double* X, int64_t ldx, int64_t n_src, const int64_t* i
  * against every symmetric dK/dtheta as H); each unordered 128 x 128 block
  * pair is evaluated once, halving the kernel-entry work. Replaces the
  * reference's run_row_blocks(grad_row_products) pass (likelihood.py:182-189). */
+/* 1 if the symmetric per-entry tcgen05 kernel takes the shape (d + 2 <= 32,
+ * w <= 128); otherwise gp_grad_forms_sym evaluates the full square through
+ * gp_grad_forms, and the caller does better with the (narrower) non-symmetric
+ * operands Y = [a/2, -(S-W)/(2t), L B^-1/(2 noise)], R = [a, W, L] there. */
+int gp_grad_forms_sym_supported(int64_t n, int d, int ard, int w);
 size_t gp_grad_forms_sym_workspace_bytes(int64_t n, int d, int ard, int w);
 int gp_grad_forms_sym(int family, int d, int ard, const float* X, int64_t ldx, int64_t n, double outputscale,
                       const float* Y, int64_t ldy, const float* R, int64_t ldrr, int w, double* out,

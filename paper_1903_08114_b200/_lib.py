@@ -98,6 +98,7 @@ _SIGS = {
     "gp_comm_reduce_scatter_i64": (C.c_int, [c_p, c_p, c_p, c_i64, c_p]),
     "gp_comm_reduce_scatter_i32": (C.c_int, [c_p, c_p, c_p, c_i64, c_p]),
     "gp_comm_allreduce_f64": (C.c_int, [c_p, c_p, c_i64, c_p]),
+    "gp_grad_forms_sym_supported": (C.c_int, [c_i64, C.c_int, C.c_int, C.c_int]),
     "gp_grad_forms_sym_workspace_bytes": (c_sz, [c_i64, C.c_int, C.c_int, C.c_int]),
     "gp_grad_forms_sym": (C.c_int, [C.c_int, C.c_int, C.c_int, c_p, c_i64, c_i64, c_f64, c_p, c_i64, c_p,
                                     c_i64, C.c_int, c_p, c_p, c_sz, c_p]),

@@ -293,6 +293,10 @@ size_t gp_grad_forms_sym_workspace_bytes(int64_t n, int d, int ard, int w) {
   return gp_grad_forms_workspace_bytes(n, n, d, ard, w);
 }
 
+int gp_grad_forms_sym_supported(int64_t n, int d, int ard, int w) {
+  return n > 0 && grad_tc_supported(n, n, d, ard, w) ? 1 : 0;
+}
+
 int gp_grad_forms_sym(int family, int d, int ard, const float* X, int64_t ldx, int64_t n, double outputscale,
                       const float* Y, int64_t ldy, const float* R, int64_t ldrr, int w, double* out,
                       void* workspace, size_t workspace_bytes, void* stream) {

@@ -239,8 +239,18 @@ def _grad_forms_sym_raw(model, d, Xs32, Y, R):
 def _gradients(model: KernelModel, ps, a, S, W, cache) -> dict:
     n, t = W.shape
     Xs32, _ = ps.scaled(model.scale_for(ps.d))
-    Y, R = symmetric_gradient_operands(a, S, W, cache)
-    raw = _grad_forms_sym_raw(model, ps.d, Xs32, Y, R)
+    k = cache.rank if cache is not None else 0
+    w_sym = 1 + 2 * t + k
+    if _lib.lib().gp_grad_forms_sym_supported(n, ps.d, 1 if model.ard else 0, w_sym):
+        # each unordered pair of points once (the per-entry tcgen05 kernel)
+        Y, R = symmetric_gradient_operands(a, S, W, cache)
+        raw = _grad_forms_sym_raw(model, ps.d, Xs32, Y, R)
+    else:
+        # large d (e.g. C4, d = 90): the full square with the narrower
+        # non-symmetric operands (w = 1 + t + k), which the tensor-core ARD
+        # expansion takes (csrc/grad_ard.cu, w <= 112)
+        Y, R = gradient_operands(a, S, W, cache)
+        raw = _grad_forms_raw(model, ps.d, Xs32, Xs32, Y, R)
     return assemble_gradients(model, raw, a, S, W, cache, n)
 
 

@@ -19,6 +19,7 @@ def main():
     w = syn.WORKLOADS[key]
     n = int(sys.argv[2]) if len(sys.argv) > 2 else w.n
     reps = int(sys.argv[3]) if len(sys.argv) > 3 else 20
+    kstage = int(sys.argv[4]) if len(sys.argv) > 4 else 10   # repetitions per stage timing
     X = syn.whitened_inputs(n, w.d, 0)
     y = syn.rff_target(X, features=256)
     m = gp.KernelModel(w.family, 1.0, w.lengthscales(), 0.1)
@@ -26,12 +27,13 @@ def main():
     plan = gp.plan_partitions(n, max(1, n // 8))
     pool = gp.WorkerPool()
     ts = []
-    for r in range(reps + 3):
+    warm = 3 if reps > 1 else 1
+    for r in range(reps + warm):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = gp.mll_value_and_grad(m, X, y, plan, pool, cfg, 0)
         torch.cuda.synchronize()
-        if r >= 3:
+        if r >= warm:
             ts.append(time.perf_counter() - t0)
     print(f"{key} n={n} d={w.d} {w.family} rank={w.rank}: mll_value_and_grad median "
           f"{statistics.median(ts) * 1e3:.2f} ms (min {min(ts) * 1e3:.2f}), {res.diagnostics.iterations} "
@@ -39,7 +41,7 @@ def main():
     # stage split (warm)
     ps = D.points(X)
 
-    def timed(label, fn, k=10):
+    def timed(label, fn, k=kstage):
         fn()
         torch.cuda.synchronize()
         t0 = time.perf_counter()

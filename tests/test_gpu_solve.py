@@ -344,3 +344,34 @@ def test_large_preconditioner_rank_variance_and_clear_error():
     op = likelihood.training_operator(m, D.points(X))
     with pytest.raises(ValueError, match="shared memory"):
         CG.mbcg_device(op, B, 1e-3, 100, pc)
+
+
+def test_large_d_gradient_uses_the_narrow_operands():
+    """Beyond the symmetric per-entry kernel (d + 2 > 32) the MLL gradient
+    takes the non-symmetric operands (w = 1 + t + k <= 112, the tensor-core
+    ARD expansion) instead of the symmetric ones (w = 1 + 2t + k, which only
+    the SIMT kernel takes); both give the same forms."""
+    import numpy as np
+    import paper_1903_08114_b200 as gp
+    from paper_1903_08114_b200 import _device as D, _lib, likelihood as LK, synthetic as syn
+    L = _lib.lib()
+    assert L.gp_grad_forms_sym_supported(50_000, 8, 1, 121) == 1
+    assert L.gp_grad_forms_sym_supported(50_000, 90, 1, 121) == 0
+    n, d = 2048, 40
+    X = syn.whitened_inputs(n, d, 0)
+    y = syn.rff_target(X, seed=1)
+    m = gp.KernelModel("matern32", 1.0, np.sqrt(d) * np.linspace(0.75, 1.5, d), 0.1)
+    ps = D.points(X)
+    pc = LK.build_kernel_preconditioner(m, ps, 50)
+    Z = LK.draw_probes_device(n, 10, 0, pc)
+    import torch
+    B = torch.cat([(D.to_device(y) - m.mean)[:, None], Z], 1).contiguous()
+    sol = LK.mbcg_device(LK.training_operator(m, ps), B, 0.01, 1000, pc)
+    a, S = sol.U[:, 0].contiguous(), sol.U[:, 1:].contiguous()
+    W = LK._pc.precond_apply_device(pc, Z)
+    got = LK._gradients(m, ps, a, S, W, pc)
+    Xs32, _ = ps.scaled(m.scale_for(d))
+    Ys, Rs = LK.symmetric_gradient_operands(a, S, W, pc)
+    ref = LK.assemble_gradients(m, LK._grad_forms_sym_raw(m, d, Xs32, Ys, Rs), a, S, W, pc, n)
+    g = np.array([got[k] for k in ref]), np.array(list(ref.values()))
+    assert np.abs(g[0] - g[1]).max() <= 1e-3 * np.abs(g[1]).max()
