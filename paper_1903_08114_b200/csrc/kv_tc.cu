@@ -192,8 +192,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
   const uint32_t v_bytes = V_TILE;
   const uint32_t stage_bytes = col_bytes + v_bytes;
   const int NS = a.nstages;
-  uint8_t* xr_s = smem;
-  uint8_t* stages = smem + row_bytes;
+  uint8_t* xr_s = smem;                          // SS only: the row image (TS: TMEM, copied from global)
+  uint8_t* stages = smem + (TS ? 0u : row_bytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(stages + NS * stage_bytes);
   uint64_t* full = bars;             // [NS]
   uint64_t* empty = bars + NS;       // [NS]
@@ -246,9 +246,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
         const int rt = it / a.splits, sp = it - rt * a.splits;
         const int ct0 = sp * a.tiles_per_split;
         const int ct1 = min(a.col_tiles, ct0 + a.tiles_per_split);
-        mbar_wait(smem_u32(xr_empty), (itc & 1) ^ 1);
-        mbar_expect_tx(smem_u32(xr_full), row_bytes);
-        bulk_g2s(smem_u32(xr_s), a.row_img + (int64_t)rt * (row_bytes / 4), row_bytes, smem_u32(xr_full));
+        if (!TS) {   // TS: the epilogue copies the row image from global memory into TMEM
+          mbar_wait(smem_u32(xr_empty), (itc & 1) ^ 1);
+          mbar_expect_tx(smem_u32(xr_full), row_bytes);
+          bulk_g2s(smem_u32(xr_s), a.row_img + (int64_t)rt * (row_bytes / 4), row_bytes, smem_u32(xr_full));
+        }
         const float* cimg = a.col_img + (int64_t)ct0 * (col_bytes / 4);
         const uint8_t* vimg = static_cast<const uint8_t*>(a.v_img) + (int64_t)ct0 * v_bytes;
         for (int ct = ct0; ct < ct1; ++ct) {
@@ -295,8 +297,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
       const int ct0 = sp * a.tiles_per_split;
       const int ct1 = min(a.col_tiles, ct0 + a.tiles_per_split);
       const int J = ct1 - ct0;
-      mbar_wait(smem_u32(xr_full), itc & 1);
       if (TS) mbar_wait(smem_u32(xa_full), itc & 1);
+      else mbar_wait(smem_u32(xr_full), itc & 1);
       tc_fence_after();
       auto dist = [&]() {
         TC_T(0, mbar_wait(smem_u32(&full[ds]), dph));
@@ -416,10 +418,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
       const int64_t my_row = (int64_t)rt * BM + q * 32 + lane;
       const int64_t diag_col = (a.self_offset >= 0 && my_row < a.n_rows) ? my_row + a.self_offset : -1000;
       if (TS && g == 0 && half == 0) {
-        // TS mode: row image hi | lo -> TMEM (A operand of the distance product).
-        // xr_full of this item implies the previous item's MMAs completed.
-        mbar_wait(smem_u32(xr_full), itc & 1);
-        const float* xr = reinterpret_cast<const float*>(xr_s);
+        // TS mode: row image hi | lo -> TMEM (A operand of the distance
+        // product), read straight from global memory (once per row item; the
+        // SMEM it would take holds two more column stages instead).
+        // xr_empty of the previous item: its MMAs have completed.
+        mbar_wait(smem_u32(xr_empty), (itc & 1) ^ 1);
+        const float* xr = a.row_img + (int64_t)rt * (2 * BM * DK);
         const int i_loc = q * 32 + lane;
         for (int part = 0; part < 2; ++part)
           for (int k0 = 0; k0 < DK; k0 += 8) {
@@ -711,7 +715,10 @@ static Plan make_plan(const gp_kv_desc* d, int t) {
   p.v_img_bytes = (size_t)p.col_tiles * V_TILE;
   p.split_bytes = (p.splits > 1 ? (size_t)p.splits * d->n_rows * t * 4 : 0) + 256 * sizeof(double) +
                   2 * TN * sizeof(float);
-  size_t row_b = 2u * BM * p.DK * 4, stage_b = 2u * BN * p.DK * 4 + V_TILE;
+  // TS mode (KV_F16, DK >= 48): the row image lives in TMEM, copied there
+  // from global memory, so its SMEM goes to the column ring
+  const bool ts = KV_F16 && p.DK >= 48;
+  size_t row_b = ts ? 0 : 2u * BM * p.DK * 4, stage_b = 2u * BN * p.DK * 4 + V_TILE;
   size_t budget = 220 * 1024 - row_b - 256 - BM * TN * 4;
   p.nstages = (int)std::min<size_t>(4, budget / stage_b);
   p.smem = row_b + p.nstages * stage_b + 256 + BM * TN * 4;
