@@ -62,6 +62,7 @@ struct Args {
   const float* col_img;   // [col tiles][2][BN*DK]
   const void* v_img;      // [col tiles][32 x 64] [V1 | V2] (fp16 or tf32)
   const float* inv_vscale; // [TN] 2^-s_c (fp16 image scaling)
+  const float* dscale;    // TS: S = S' dscale (fp16 distance images, points_image16_kernel)
   int DK;
   int64_t n_rows, n_cols;
   int row_tiles, col_tiles, splits, tiles_per_split;
@@ -164,6 +165,80 @@ __global__ void points_image_kernel(const float* __restrict__ X, int64_t ldx, in
   }
 }
 
+// Large d (TS mode): the augmented points as fp16 hi + lo (22 significant
+// bits, like tf32 hi + lo) in the 16-bit canonical layout, so the distance
+// product runs at the f16 rate and a column tile takes half the SMEM. fp16
+// needs a range: each side is scaled by one power of two 2^-e chosen from the
+// largest |value| of that side (|value| 2^-e <= 2^14), and the epilogue
+// multiplies S by 2^(e_row + e_col) (`dscale`).
+// rng[0..1] = max |y_k|, max |y|^2 over the points (y = x - mean), as fp32
+// bits (non-negative floats order as integers: atomicMax)
+__global__ void points_range_kernel(const float* __restrict__ X, int64_t ldx, int64_t n, int d,
+                                    const double* __restrict__ mean, unsigned* rng) {
+  float m1 = 0.f, m2 = 0.f;
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    double nrm = 0.0, mx = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const double y = (double)X[row * ldx + k] - mean[k];
+      nrm += y * y;
+      mx = fmax(mx, fabs(y));
+    }
+    m1 = fmaxf(m1, (float)mx);
+    m2 = fmaxf(m2, (float)nrm);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+    m2 = fmaxf(m2, __shfl_xor_sync(0xffffffffu, m2, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&rng[0], __float_as_uint(m1));
+    atomicMax(&rng[1], __float_as_uint(m2));
+  }
+}
+
+// exponent e of one side: the largest |value| of its image times 2^-e is <= 2^14
+__device__ __forceinline__ int image_exp16(int role, double c, const unsigned* rng) {
+  const double m1 = __uint_as_float(rng[0]), m2 = __uint_as_float(rng[1]);
+  const double M = role == 0 ? fmax(fabs(c) * m1, fmax(0.5 * fabs(c) * m2, 0.5 * fabs(c))) : fmax(fmax(m1, m2), 1.0);
+  int ex;
+  frexp(M, &ex);   // M < 2^ex
+  return ex - 14;
+}
+
+__global__ void points_image16_kernel(const float* __restrict__ X, int64_t ldx, int64_t n, int d, int DK, int R,
+                                      int role, double c, const double* __restrict__ mean, const unsigned* rng,
+                                      const unsigned* rng_other, __half* img, int64_t ntiles, float* dscale) {
+  const int e = image_exp16(role, c, rng);
+  if (dscale && blockIdx.x == 0 && threadIdx.x == 0)   // S = S' 2^(e_row + e_col)
+    *dscale = ldexpf(1.f, e + image_exp16(1 - role, role == 0 ? 1.0 : c, rng_other));
+  int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= ntiles * R) return;
+  int64_t tile = row / R;
+  int r = (int)(row - tile * R);
+  __half* hi = img + tile * 2 * (int64_t)R * DK;
+  __half* lo = hi + (int64_t)R * DK;
+  double nrm = 0.0;
+  bool valid = row < n;
+  if (valid)
+    for (int k = 0; k < d; ++k) {
+      double x = (double)X[row * ldx + k] - mean[k];
+      nrm += x * x;
+    }
+  for (int k = 0; k < DK; ++k) {
+    double v = 0.0;
+    if (valid) {
+      if (k < d) v = ((double)X[row * ldx + k] - mean[k]) * (role == 0 ? c : 1.0);
+      else if (k == d) v = role == 0 ? -0.5 * c * nrm : 1.0;
+      else if (k == d + 1) v = role == 0 ? -0.5 * c : nrm;
+    }
+    v = ldexp(v, -e);
+    const __half h = __double2half(v);
+    hi[canon16(r, k, R)] = h;
+    lo[canon16(r, k, R)] = __double2half(v - (double)__half2float(h));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // the fused kernel
 //   TMEM: S_0..2 (3 x 64 cols, distance accumulators, 2 tiles of look-ahead),
@@ -174,9 +249,12 @@ __global__ void points_image_kernel(const float* __restrict__ X, int64_t ldx, in
 //   done reading K), o_full/o_empty[2], xr_full/xr_empty (row image).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t TMS(uint32_t b) { return b * 64; }           // 0, 64, 128
+// TS mode: S buffers 0, 1 at [0, 128) and the third past the fp16 row image
+// (DK <= 96 columns from TMXA = 320), at [416, 480)
+__device__ __forceinline__ uint32_t TMS_TS(uint32_t b) { return b < 2 ? b * 64 : 416u; }
 // TMEM layouts (columns):            S            K (x2)       O (x2)     row image
 //   SS distance (3 S buffers):   [0, 192)     192 + 128b   [448, 512)   -
-//   TS distance (2 S buffers):   [0, 128)     [128, 256)   [256, 320)   [320, 320 + 2 DK)
+//   TS distance (3 S buffers):   [0, 128) + [416, 480)   [128, 256)   [256, 320)   [320, 320 + DK) (fp16 pairs)
 // K buffer b, fp16 pairs: K1 [tm_k + 64b, +32) | K2 [+32, +64); tf32 (SS only): hi 64 | lo 64
 #define TMKH(b) ((TS ? 128u : 192u) + (uint32_t)(b) * (TS ? 64u : 128u))
 #define TMKL(b) (TMKH(b) + (KV_F16 ? 32u : 64u))
@@ -187,8 +265,9 @@ template <int FAM, bool TS>
 __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int DK = a.DK;
-  const uint32_t row_bytes = 2u * BM * DK * 4u;
-  const uint32_t col_bytes = 2u * BN * DK * 4u;
+  constexpr uint32_t EB = TS ? 2u : 4u;   // bytes per image element (TS: fp16, else tf32)
+  const uint32_t row_bytes = 2u * BM * DK * EB;
+  const uint32_t col_bytes = 2u * BN * DK * EB;
   const uint32_t v_bytes = V_TILE;
   const uint32_t stage_bytes = col_bytes + v_bytes;
   const int NS = a.nstages;
@@ -271,12 +350,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
     // lives in uniform registers; one elected lane issues tcgen05 ops.
     // Descriptors are built once; per-MMA work is a 32-bit add on the
     // start-address field (addresses advance in 16-byte units).
-    const uint32_t idesc_d = make_idesc(BM, BN);
+    const uint32_t idesc_d = TS ? idesc_f16(BM, BN) : make_idesc(BM, BN);
     const uint32_t idesc_c32 = KV_F16 ? idesc_f16(BM, 2 * TN) : make_idesc(BM, 2 * TN);
     const uint32_t idesc_c16 = KV_F16 ? idesc_f16(BM, TN) : make_idesc(BM, TN);
     const uint32_t lbo_a = (BM / 8) * 128, lbo_b = (BN / 8) * 128, lbo_v = (2 * TN / 8) * 128;
-    const uint32_t a_half16 = (BM * DK * 4) >> 4, b_half16 = (BN * DK * 4) >> 4;
-    const int ksteps = DK / 8;
+    const uint32_t a_half16 = (BM * DK * EB) >> 4, b_half16 = (BN * DK * EB) >> 4;
+    const int ksteps = TS ? DK / 16 : DK / 8;   // K per MMA: 16 fp16 / 8 tf32 (both 32 B per row)
     const uint64_t da0 = make_desc(smem_u32(xr_s), lbo_a, 128);
     const uint64_t db0 = make_desc(smem_u32(stages), lbo_b, 128);
     const uint64_t dv0 = make_desc(smem_u32(stages + col_bytes), lbo_v, 128);
@@ -303,16 +382,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
       auto dist = [&]() {
         TC_T(0, mbar_wait(smem_u32(&full[ds]), dph));
         tc_fence_after();
-        const uint32_t d_tm = tmem + TMS(sb_next);
+        const uint32_t d_tm = tmem + (TS ? TMS_TS(sb_next) : TMS(sb_next));
         const uint64_t db = db0 + (uint64_t)(ds * stage16);
         if (leader) {
           if (TS) {
 #pragma unroll
+            // fp16 pairs: hi at TMXA, lo at TMXA + DK/2 (one kstep = 8 columns)
             for (int pass = 0; pass < 3; ++pass) {
-              const uint32_t a_t = tmem + TMXA + (pass == 0 ? (uint32_t)DK : 0u);
+              const uint32_t a_t = tmem + TMXA + (pass == 0 ? (uint32_t)(DK / 2) : 0u);
               const uint64_t b_p = db + (pass == 1 ? b_half16 : 0u);
               for (int ks = 0; ks < ksteps; ++ks)
-                mma_ts(d_tm, a_t + ks * 8, b_p + (uint64_t)(ks * kstep_b16), idesc_d, (pass | ks) != 0);
+                mma16_ts(d_tm, a_t + ks * 8, b_p + (uint64_t)(ks * kstep_b16), idesc_d, (pass | ks) != 0);
             }
           } else {
 #pragma unroll
@@ -330,7 +410,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
         }
         __syncwarp();
         if (++ds == (uint32_t)NS) { ds = 0; dph ^= 1; }
-        if (++sb_next == (TS ? 2u : 3u)) sb_next = 0;
+        if (++sb_next == 3u) sb_next = 0;
       };
       for (int jj = 0; jj < LA && jj < J; ++jj) dist();
       for (int jj = 0; jj < J; ++jj) {
@@ -423,15 +503,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
         // SMEM it would take holds two more column stages instead).
         // xr_empty of the previous item: its MMAs have completed.
         mbar_wait(smem_u32(xr_empty), (itc & 1) ^ 1);
-        const float* xr = a.row_img + (int64_t)rt * (2 * BM * DK);
+        const __half* xr = reinterpret_cast<const __half*>(a.row_img) + (int64_t)rt * (2 * BM * DK);
         const int i_loc = q * 32 + lane;
         for (int part = 0; part < 2; ++part)
-          for (int k0 = 0; k0 < DK; k0 += 8) {
-            uint32_t w[8];
+          for (int k0 = 0; k0 < DK; k0 += 16) {
+            uint32_t w[8];   // 16 fp16 along K = 8 TMEM columns (one kstep)
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk)
-              w[kk] = __float_as_uint(xr[part * BM * DK + canon(i_loc, k0 + kk, BM)]);
-            tmem_st8(tmem + lane_base + TMXA + part * DK + k0, w);
+              w[kk] = *reinterpret_cast<const uint32_t*>(xr + part * BM * DK + canon16(i_loc, k0 + 2 * kk, BM));
+            tmem_st8(tmem + lane_base + TMXA + part * (DK / 2) + k0 / 2, w);
           }
         tmem_wait_st();
         tc_fence_before();
@@ -442,14 +522,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
       for (int c = 0; c < TN; ++c) acc[c] = 0.f;
       for (int jj = 0; jj < J; ++jj, ++T) {
         if ((int)(T & 1) != g) continue;
-        const uint32_t sb = T % (TS ? 2u : 3u), sph = (T / (TS ? 2u : 3u)) & 1;
+        const uint32_t sb = T % 3u, sph = (T / 3u) & 1;
         TC_T(0, mbar_wait(smem_u32(&s_full[sb]), sph));
         tacc[7] += 1;
         tc_fence_after();
         // this warp's 32 columns in one TMEM load (one round trip per tile)
         const int c0 = half * 32;
         uint32_t v[32];
-        TC_T(3, tmem_ld32(tmem + lane_base + TMS(sb) + c0, v); tmem_wait_ld());
+        TC_T(3, tmem_ld32(tmem + lane_base + (TS ? TMS_TS(sb) : TMS(sb)) + c0, v); tmem_wait_ld());
         {
           const int64_t e_diag = diag_col - ((int64_t)(ct0 + jj) * BN + c0);
           // self-diagonal entry (same point on both sides): r2 = 0 exactly
@@ -461,9 +541,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_tc_kernel(const Args a) {
         }
         const long long tk0 = a.prof ? clock64() : 0;
         {
+          const float dsc = TS ? *a.dscale : 1.f;
 #pragma unroll
           for (int k = 0; k < 32; ++k) {
-            float sv = __uint_as_float(v[k]);
+            float sv = TS ? __uint_as_float(v[k]) * dsc : __uint_as_float(v[k]);
             float kap;
             // clamps written as selects so NaN inputs propagate (the
             // reference raises on non-finite blocks, partition.py:231-236)
@@ -579,6 +660,36 @@ int distance_images(const float* Xr, int64_t ldr, int64_t nr, const float* Xc, i
   int64_t cols = col_tiles * BNc;
   points_image_kernel<<<(unsigned)((cols + 255) / 256), 256, 0, st>>>(Xc, ldc, nc, d, DK, BNc, 1, 1.0, mean,
                                                                      col_img, col_tiles);
+  GP_LAUNCH_CHECK();
+  return GP_OK;
+}
+
+// fp16 images of the large-d path: column means, the two sides' ranges,
+// then the scaled hi | lo images; dscale = 2^(e_row + e_col)
+int distance_images16(const float* Xr, int64_t ldr, int64_t nr, const float* Xc, int64_t ldc, int64_t nc,
+                      int d, int DK, int BMr, int BNc, double c, double* mean, unsigned* rng, __half* row_img,
+                      __half* col_img, float* dscale, cudaStream_t st) {
+  column_mean_kernel<<<kColClusterCtas, 1024, 0, st>>>(Xc, ldc, nc, d, mean);
+  GP_LAUNCH_CHECK();
+  GP_CUDA_TRY(cudaMemsetAsync(rng, 0, 4 * sizeof(unsigned), st));
+  const bool same = Xr == Xc && ldr == ldc && nr == nc;
+  auto range = [&](const float* X, int64_t ld, int64_t n, unsigned* out) -> int {
+    if (n <= 0) return GP_OK;
+    const unsigned nb = (unsigned)std::min<int64_t>((n + 255) / 256, 4LL * num_sms());
+    points_range_kernel<<<nb, 256, 0, st>>>(X, ld, n, d, mean, out);
+    GP_LAUNCH_CHECK();
+    return GP_OK;
+  };
+  if (int rc = range(Xc, ldc, nc, rng + 2)) return rc;
+  if (same) GP_CUDA_TRY(cudaMemcpyAsync(rng, rng + 2, 2 * sizeof(unsigned), cudaMemcpyDeviceToDevice, st));
+  else if (int rc = range(Xr, ldr, nr, rng)) return rc;
+  int64_t row_tiles = (nr + BMr - 1) / BMr, col_tiles = (nc + BNc - 1) / BNc;
+  int64_t rows = row_tiles * BMr, cols = col_tiles * BNc;
+  points_image16_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(Xr, ldr, nr, d, DK, BMr, 0, c, mean, rng,
+                                                                       rng + 2, row_img, row_tiles, dscale);
+  GP_LAUNCH_CHECK();
+  points_image16_kernel<<<(unsigned)((cols + 255) / 256), 256, 0, st>>>(Xc, ldc, nc, d, DK, BNc, 1, 1.0, mean,
+                                                                       rng + 2, rng, col_img, col_tiles, nullptr);
   GP_LAUNCH_CHECK();
   return GP_OK;
 }
@@ -714,13 +825,13 @@ static Plan make_plan(const gp_kv_desc* d, int t) {
   p.col_img_bytes = (size_t)p.col_tiles * 2 * BN * p.DK * 4;
   p.v_img_bytes = (size_t)p.col_tiles * V_TILE;
   p.split_bytes = (p.splits > 1 ? (size_t)p.splits * d->n_rows * t * 4 : 0) + 256 * sizeof(double) +
-                  2 * TN * sizeof(float);
+                  2 * TN * sizeof(float) + 8 * sizeof(float);
   // TS mode (KV_F16, DK >= 48): the row image lives in TMEM, copied there
   // from global memory, so its SMEM goes to the column ring
   const bool ts = KV_F16 && p.DK >= 48;
-  size_t row_b = ts ? 0 : 2u * BM * p.DK * 4, stage_b = 2u * BN * p.DK * 4 + V_TILE;
+  size_t row_b = ts ? 0 : 2u * BM * p.DK * 4, stage_b = 2u * BN * p.DK * (ts ? 2 : 4) + V_TILE;
   size_t budget = 220 * 1024 - row_b - 256 - BM * TN * 4;
-  p.nstages = (int)std::min<size_t>(4, budget / stage_b);
+  p.nstages = (int)std::min<size_t>(ts ? 6 : 4, budget / stage_b);
   p.smem = row_b + p.nstages * stage_b + 256 + BM * TN * 4;
   return p;
 }
@@ -756,13 +867,23 @@ int kv_tc(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out
   double* mean = reinterpret_cast<double*>(w); w += 256 * sizeof(double);
   float* vscale = reinterpret_cast<float*>(w); w += TN * sizeof(float);
   float* inv_vscale = reinterpret_cast<float*>(w); w += TN * sizeof(float);
+  unsigned* rng = reinterpret_cast<unsigned*>(w); w += 4 * sizeof(unsigned);   // TS: row, col ranges
+  float* dscale = reinterpret_cast<float*>(w); w += 4 * sizeof(float);
   float* split_ws = reinterpret_cast<float*>(w);
   const double c = desc->family == GP_FAMILY_RBF ? 1.4426950408889634 : -6.0;
+  const bool ts = KV_F16 && p.DK >= 48;   // large d: fp16 distance images, row image in TMEM
   {
-    if (!kv_images_current)
-      if (int rc = distance_images(desc->Xr, desc->ldr, desc->n_rows, desc->Xc, desc->ldc, desc->n_cols,
-                                   desc->d, p.DK, BM, BN, c, mean, row_img, col_img, st))
+    if (!kv_images_current) {
+      if (ts) {
+        if (int rc = distance_images16(desc->Xr, desc->ldr, desc->n_rows, desc->Xc, desc->ldc, desc->n_cols,
+                                       desc->d, p.DK, BM, BN, c, mean, rng, reinterpret_cast<__half*>(row_img),
+                                       reinterpret_cast<__half*>(col_img), dscale, st))
+          return rc;
+      } else if (int rc = distance_images(desc->Xr, desc->ldr, desc->n_rows, desc->Xc, desc->ldc, desc->n_cols,
+                                          desc->d, p.DK, BM, BN, c, mean, row_img, col_img, st)) {
         return rc;
+      }
+    }
     if (KV_F16) {
       if (int rc = v_colscale(V, ldv, desc->n_cols, t, vscale, inv_vscale, st)) return rc;
       if (int rc = v_images16(V, ldv, t, desc->n_cols, vscale, static_cast<__half*>(v_img), p.col_tiles, st))
@@ -773,15 +894,15 @@ int kv_tc(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* out
   }
   Args a;
   a.row_img = row_img; a.col_img = col_img; a.v_img = v_img; a.inv_vscale = inv_vscale; a.DK = p.DK;
+  a.dscale = dscale;
   a.n_rows = desc->n_rows; a.n_cols = desc->n_cols;
   a.row_tiles = p.row_tiles; a.col_tiles = p.col_tiles; a.splits = p.splits;
   a.tiles_per_split = p.tiles_per_split; a.nstages = p.nstages; a.fam = desc->family; a.t = t;
   a.s2 = (float)desc->outputscale; a.noise = (float)desc->noise; a.diag_offset = desc->diag_offset;
   a.self_offset = desc->self_offset;
   a.V = V; a.ldv = ldv;
-  // large d: row image TMEM-resident (TS distance MMA, 2 S buffers, look-ahead 1)
-  const bool ts = KV_F16 && p.DK >= 48;
-  a.lookahead = ts ? 1 : std::min(2, p.nstages - 1);
+  // large d: row image TMEM-resident (TS distance MMA on fp16 images, 3 S buffers, look-ahead 2)
+  a.lookahead = std::min(2, p.nstages - 1);   // 3 S buffers in both modes
   a.chunk = CHUNK;
   if (p.splits > 1) {
     a.out = split_ws; a.ldo = t; a.split_stride = desc->n_rows * (int64_t)t;
