@@ -36,6 +36,7 @@ struct Args {
   const float* col_img;   // [col tiles][2][BN*DK]
   const __half* v_img;    // [col tiles][2*NW x 64] fp16 [V1 | V2]
   const float* inv_vscale;  // [t] 2^-s_c
+  const float* dscale;    // large d: fp16 distance images, S = S' dscale (null: tf32 images)
   int DK, NW;             // NW = t rounded up to 16
   int64_t n_rows, n_cols;
   int row_tiles, col_tiles, splits, tiles_per_split;
@@ -81,8 +82,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
   constexpr int BN = BNT;
   constexpr int CW = BNT / 2;
   const int DK = a.DK, NW = a.NW;
-  const uint32_t row_bytes = 2u * BM * DK * 4u;
-  const uint32_t col_bytes = 2u * BN * DK * 4u;
+  const bool F16I = a.dscale != nullptr;   // fp16 hi | lo distance images (large d)
+  const uint32_t EB = F16I ? 2u : 4u;
+  const uint32_t row_bytes = 2u * BM * DK * EB;
+  const uint32_t col_bytes = 2u * BN * DK * EB;
   const uint32_t v_bytes = 2u * NW * BN * 2u;
   const int NSC = a.nsc, NSV = a.nsv;
   uint8_t* xr_s = smem;
@@ -177,12 +180,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    const uint32_t idesc_d = make_idesc(BM, BN);
+    const uint32_t idesc_d = F16I ? idesc_f16(BM, BN) : make_idesc(BM, BN);
     const uint32_t idesc_c = idesc_f16(BM, NW);
     const uint32_t lbo_a = (BM / 8) * 128, lbo_b = (BN / 8) * 128, lbo_v = (2 * NW / 8) * 128;
-    const uint32_t a_half16 = (BM * DK * 4) >> 4, b_half16 = (BN * DK * 4) >> 4;
+    const uint32_t a_half16 = (BM * DK * EB) >> 4, b_half16 = (BN * DK * EB) >> 4;
     const uint32_t v2_16 = ((NW / 8) * 128) >> 4;   // V2 rows start NW/8 core rows down
-    const int ksteps = DK / 8;
+    const int ksteps = F16I ? DK / 16 : DK / 8;   // 32 B of K per row and MMA either way
     const uint64_t da0 = make_desc(smem_u32(xr_s), lbo_a, 128);
     const uint64_t db0 = make_desc(smem_u32(cring), lbo_b, 128);
     const uint64_t dv0 = make_desc(smem_u32(vring), lbo_v, 128);
@@ -208,9 +211,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
           for (int pass = 0; pass < 3; ++pass) {
             const uint64_t a_p = da0 + (pass == 0 ? a_half16 : 0u);
             const uint64_t b_p = db + (pass == 1 ? b_half16 : 0u);
-            for (int ks = 0; ks < ksteps; ++ks)
-              mma_ss(d_tm, a_p + (uint64_t)(ks * kstep_a16), b_p + (uint64_t)(ks * kstep_b16), idesc_d,
-                     (pass | ks) != 0);
+            for (int ks = 0; ks < ksteps; ++ks) {
+              if (F16I)
+                mma16_ss(d_tm, a_p + (uint64_t)(ks * kstep_a16), b_p + (uint64_t)(ks * kstep_b16), idesc_d,
+                         (pass | ks) != 0);
+              else
+                mma_ss(d_tm, a_p + (uint64_t)(ks * kstep_a16), b_p + (uint64_t)(ks * kstep_b16), idesc_d,
+                       (pass | ks) != 0);
+            }
           }
           tc_commit(smem_u32(&s_full[sbn]));
           tc_commit(smem_u32(&cempty[ds]));
@@ -286,10 +294,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_wide_kernel(const Args a) {
           for (int e = 0; e < CW; ++e)
             if (e == e_diag) v[e] = 0u;   // same point on both sides: r2 = 0 exactly
         }
+        const float dsc = F16I ? *a.dscale : 1.f;
 #pragma unroll
         for (int e = 0; e < CW; ++e) {
           // x 2^12 for the fp16 split; the finalize's inv_vscale divides it out
-          v[e] = __float_as_uint(kappa_split_scaled<FAM>(__uint_as_float(v[e])));
+          v[e] = __float_as_uint(kappa_split_scaled<FAM>(__uint_as_float(v[e]) * dsc));
         }
         mbar_wait(smem_u32(&k_empty[kb]), kph ^ 1);   // K[kb] was read two tiles ago
         tc_fence_after();
@@ -374,6 +383,7 @@ __global__ void kv_wide_finalize(const float* __restrict__ accw, int splits, int
 
 struct Plan {
   int DK, NW, BN, nfold, row_tiles, col_tiles, splits, tiles_per_split, nsc, nsv;
+  int eb;   // bytes per distance-image element: 2 (fp16 hi | lo, DK >= 48) or 4 (tf32)
   int64_t rows_pad;
   size_t row_img_bytes, col_img_bytes, v_img_bytes, split_bytes, smem;
 };
@@ -381,7 +391,7 @@ struct Plan {
 // SMEM rings for column tile width bn with nfold staging buffers per
 // epilogue warp; false when a 2-deep column ring and 2-deep V ring do not fit
 static bool fit_rings(Plan& p, int bn, int nfold, size_t cap) {
-  const size_t row_b = 2u * BM * p.DK * 4, col_b = 2u * bn * p.DK * 4, v_b = 2u * p.NW * bn * 2;
+  const size_t row_b = 2u * BM * p.DK * p.eb, col_b = 2u * bn * p.DK * p.eb, v_b = 2u * p.NW * bn * 2;
   const size_t fold_b = (size_t)NUM_EPI_WARPS * nfold * STAGE_FOLD_BYTES;
   if (row_b + 512 + fold_b + 2 * col_b + 2 * v_b > cap) return false;
   const size_t budget = cap - row_b - 512 - fold_b;
@@ -399,6 +409,7 @@ static Plan make_plan(const gp_kv_desc* d, int t) {
   Plan p;
   p.DK = (d->d + 2 + 7) / 8 * 8;
   p.NW = (t + 15) / 16 * 16;
+  p.eb = p.DK >= 48 ? 2 : 4;
   // 64-point column tiles with double-buffered fold staging (the tuned
   // d <= 30 configuration); for large d (C4: DK = 96, a 96 KB row image)
   // 32-point tiles and single-buffered staging in the full 227 KB
@@ -424,7 +435,8 @@ static Plan make_plan(const gp_kv_desc* d, int t) {
   p.col_img_bytes = (size_t)p.col_tiles * 2 * BN * p.DK * 4;
   p.v_img_bytes = (size_t)p.col_tiles * 2 * p.NW * BN * 2;
   p.rows_pad = (int64_t)p.row_tiles * BM;
-  p.split_bytes = (size_t)p.splits * p.NW * p.rows_pad * 4 + 256 * sizeof(double) + 2 * TMAX * sizeof(float);
+  p.split_bytes = (size_t)p.splits * p.NW * p.rows_pad * 4 + 256 * sizeof(double) + 2 * TMAX * sizeof(float) +
+                  8 * sizeof(float);
   return p;
 }
 
@@ -460,15 +472,24 @@ int kv_wide(const gp_kv_desc* desc, const float* V, int64_t ldv, int t, float* o
   double* mean = reinterpret_cast<double*>(w); w += 256 * sizeof(double);
   float* vscale = reinterpret_cast<float*>(w); w += TMAX * sizeof(float);
   float* inv_vscale = reinterpret_cast<float*>(w); w += TMAX * sizeof(float);
+  unsigned* rng = reinterpret_cast<unsigned*>(w); w += 4 * sizeof(unsigned);
+  float* dscale = reinterpret_cast<float*>(w); w += 4 * sizeof(float);
   float* accw = reinterpret_cast<float*>(w);
   const double c = desc->family == GP_FAMILY_RBF ? 1.4426950408889634 : -6.0;
-  if (int rc = tc::distance_images(desc->Xr, desc->ldr, desc->n_rows, desc->Xc, desc->ldc, desc->n_cols, desc->d,
-                                   p.DK, BM, p.BN, c, mean, row_img, col_img, st))
+  if (p.eb == 2) {
+    if (int rc = tc::distance_images16(desc->Xr, desc->ldr, desc->n_rows, desc->Xc, desc->ldc, desc->n_cols,
+                                       desc->d, p.DK, BM, p.BN, c, mean, rng, reinterpret_cast<__half*>(row_img),
+                                       reinterpret_cast<__half*>(col_img), dscale, st))
+      return rc;
+  } else if (int rc = tc::distance_images(desc->Xr, desc->ldr, desc->n_rows, desc->Xc, desc->ldc, desc->n_cols,
+                                          desc->d, p.DK, BM, p.BN, c, mean, row_img, col_img, st)) {
     return rc;
+  }
   if (int rc = tc::v_colscale(V, ldv, desc->n_cols, t, vscale, inv_vscale, st)) return rc;
   if (int rc = tc::v_images16_wide(V, ldv, t, p.NW, desc->n_cols, vscale, v_img, p.col_tiles, st, p.BN)) return rc;
   Args a;
   a.row_img = row_img; a.col_img = col_img; a.v_img = v_img; a.inv_vscale = inv_vscale;
+  a.dscale = p.eb == 2 ? dscale : nullptr;
   a.DK = p.DK; a.NW = p.NW;
   a.n_rows = desc->n_rows; a.n_cols = desc->n_cols;
   a.row_tiles = p.row_tiles; a.col_tiles = p.col_tiles; a.splits = p.splits;

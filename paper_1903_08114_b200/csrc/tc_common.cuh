@@ -228,6 +228,12 @@ __host__ __device__ __forceinline__ int canon16(int r, int k, int R) {
 int distance_images(const float* Xr, int64_t ldr, int64_t nr, const float* Xc, int64_t ldc, int64_t nc,
                     int d, int DK, int BMr, int BNc, double c, double* mean, float* row_img,
                     float* col_img, cudaStream_t st);
+// fp16 hi | lo images for large d (DK >= 48): one power-of-two scale per side
+// (|value| <= 2^14), *dscale = 2^(e_row + e_col) multiplies S back; rng: 4
+// words of scratch
+int distance_images16(const float* Xr, int64_t ldr, int64_t nr, const float* Xc, int64_t ldc, int64_t nc,
+                      int d, int DK, int BMr, int BNc, double c, double* mean, unsigned* rng, __half* row_img,
+                      __half* col_img, float* dscale, cudaStream_t st);
 // fp16 V image for the contraction: per 64-point tile a 32-row K-major operand,
 // rows 0-15 V1 = fp16(2^s_c V), rows 16-31 V2 = fp16(2^s_c V - V1)
 int v_images16(const float* V, int64_t ldv, int t, int64_t ncols, const float* vscale, __half* img,
