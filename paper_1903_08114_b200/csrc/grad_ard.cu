@@ -44,6 +44,7 @@ struct Args {
   const uint32_t* y_rows;       // [rows][2*WP] bf16 pairs: Y1 then Y2
   const float* Xr; int64_t ldr;
   const double* mean;
+  const float* dscale;    // large d: fp16 hi | lo distance images, S = S' dscale (null: tf32)
   int DK, WK, WP, GN, d, p0, nl;
   int64_t n_rows, n_cols;
   int row_tiles, col_tiles, splits, tiles_per_split, nstages;
@@ -82,8 +83,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_ard_kernel(const Args a) {
   constexpr int CW = BN / 2;   // columns of a tile per epilogue warp
   extern __shared__ __align__(1024) uint8_t smem[];
   const int DK = a.DK, WK = a.WK, GN = a.GN;
-  const uint32_t row_bytes = 2u * BM * DK * 4u;
-  const uint32_t col_bytes = 2u * BN * DK * 4u;
+  const bool F16I = a.dscale != nullptr;   // fp16 hi | lo distance images (large d)
+  const uint32_t EB = F16I ? 2u : 4u;
+  const uint32_t row_bytes = 2u * BM * DK * EB;
+  const uint32_t col_bytes = 2u * BN * DK * EB;
   const uint32_t r_bytes = 2u * BN * WK * 2u;
   const uint32_t xx_bytes = 2u * GN * BN * 2u;
   const uint32_t stage_bytes = col_bytes + r_bytes + xx_bytes;
@@ -165,7 +168,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_ard_kernel(const Args a) {
     // ===================== MMA issuer (warp-uniform) =====================
     // per tile T: S and H of T, then G of T - 1 (its W is being written by
     // the epilogue while S, H of T run)
-    const uint32_t idesc_d = make_idesc(BM, BN);
+    const uint32_t idesc_d = F16I ? idesc_f16(BM, BN) : make_idesc(BM, BN);
     const uint32_t idesc_h = idesc_bf16(BM, BN), idesc_g = idesc_bf16(BM, GN);
     const uint32_t lbo_a = (BM / 8) * 128, lbo_b = (BN / 8) * 128;
     const uint32_t lbo_r = (BN / 8) * 128, lbo_x = (GN / 8) * 128;
@@ -173,12 +176,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_ard_kernel(const Args a) {
     const uint64_t db0 = make_desc(smem_u32(stages), lbo_b, 128);
     const uint64_t dr0 = make_desc(smem_u32(stages + col_bytes), lbo_r, 128);
     const uint64_t dx0 = make_desc(smem_u32(stages + col_bytes + r_bytes), lbo_x, 128);
-    const uint32_t a_half16 = (BM * DK * 4) >> 4, b_half16 = (BN * DK * 4) >> 4;
+    const uint32_t a_half16 = (BM * DK * EB) >> 4, b_half16 = (BN * DK * EB) >> 4;
     const uint32_t r_half16 = (BN * WK * 2) >> 4, x_half16 = (GN * BN * 2) >> 4;
     const uint32_t stage16 = stage_bytes >> 4;
     const uint32_t ka16 = (2 * lbo_a) >> 4, kb16 = (2 * lbo_b) >> 4;
     const uint32_t kr16 = (2 * lbo_r) >> 4, kx16 = (2 * lbo_x) >> 4;
-    const int dsteps = DK / 8, hsteps = WK / 16;
+    const int dsteps = F16I ? DK / 16 : DK / 8, hsteps = WK / 16;   // 32 B of K per row and MMA
     const uint32_t ty1 = tmem + TM::Y, ty2 = tmem + TM::Y + (uint32_t)a.WP;
     const bool leader = elect_one();
     uint32_t s = 0, ph = 0, T = 0, itc = 0;
@@ -224,8 +227,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_ard_kernel(const Args a) {
           for (int pass = 0; pass < 3; ++pass) {
             const uint64_t ap = da0 + (pass == 0 ? a_half16 : 0u);
             const uint64_t bp = db + (pass == 1 ? b_half16 : 0u);
-            for (int ks = 0; ks < dsteps; ++ks)
-              mma_ss(d_s, ap + (uint64_t)(ks * ka16), bp + (uint64_t)(ks * kb16), idesc_d, (pass | ks) != 0);
+            for (int ks = 0; ks < dsteps; ++ks) {
+              if (F16I)
+                mma16_ss(d_s, ap + (uint64_t)(ks * ka16), bp + (uint64_t)(ks * kb16), idesc_d, (pass | ks) != 0);
+              else
+                mma_ss(d_s, ap + (uint64_t)(ks * ka16), bp + (uint64_t)(ks * kb16), idesc_d, (pass | ks) != 0);
+            }
           }
 #pragma unroll
           for (int pass = 0; pass < 3; ++pass) {   // Y1.R1 + Y1.R2 + Y2.R1
@@ -307,9 +314,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) grad_ard_kernel(const Args a) {
             if (e == e_diag) sv[e] = 0u;
         }
         float a0 = 0.f;
+        const float dsc = F16I ? *a.dscale : 1.f;
 #pragma unroll
         for (int e = 0; e < CW; ++e) {
-          const float S = __uint_as_float(sv[e]);
+          const float S = __uint_as_float(sv[e]) * dsc;
           const float h = __uint_as_float(hv[e]);
           float kap, eps;
           if (FAM == GP_FAMILY_RBF) {
@@ -460,6 +468,7 @@ __global__ void grad_ard_finalize(const double* __restrict__ partials, int nbloc
 
 struct Plan {
   int BN, DK, WK, WP, row_tiles, col_tiles, splits, tiles_per_split, nstages, grid;
+  int eb;   // distance-image element bytes: 2 (fp16 hi | lo, DK >= 48) or 4 (tf32)
   size_t row_img, col_img, r_img, xx_img, y_rows, partials, smem;
 };
 
@@ -468,6 +477,7 @@ static int gn_for(int nl) { return std::max(16, (2 * nl + 15) / 16 * 16); }
 static Plan make_plan(int64_t nr, int64_t nc, int d, int w) {
   Plan p;
   p.DK = (d + 2 + 7) / 8 * 8;
+  p.eb = p.DK >= 48 ? 2 : 4;
   const int BN = p.DK <= 32 ? 64 : 32;   // large d: narrower tiles keep two SMEM stages
   p.BN = BN;
   p.WK = (w + 15) / 16 * 16;
@@ -487,8 +497,8 @@ static Plan make_plan(int64_t nr, int64_t nc, int d, int w) {
   p.xx_img = (size_t)p.col_tiles * 2 * GNmax * BN * 2;
   p.y_rows = (size_t)p.row_tiles * BM * 2 * p.WP * 4;
   p.partials = (size_t)num_sms() * (1 + MAXNL) * 8;
-  const size_t row_b = 2u * BM * p.DK * 4;
-  const size_t stage_b = 2u * BN * p.DK * 4 + 2u * BN * p.WK * 2 + 2u * GNmax * BN * 2;
+  const size_t row_b = 2u * BM * p.DK * p.eb;
+  const size_t stage_b = 2u * BN * p.DK * p.eb + 2u * BN * p.WK * 2 + 2u * GNmax * BN * 2;
   const size_t budget = 225 * 1024 - row_b - 512;
   p.nstages = (int)std::min<size_t>(3, budget / stage_b);
   p.smem = row_b + p.nstages * stage_b + 256;
@@ -511,7 +521,7 @@ size_t grad_ard_workspace(int64_t nr, int64_t nc, int d, int w) {
   ga::Plan p = ga::make_plan(nr, nc, d, w);
   using ga::al256;
   return al256(p.row_img) + al256(p.col_img) + al256(p.r_img) + al256(p.xx_img) + al256(p.y_rows) +
-         al256(p.partials) + 256 * sizeof(double);
+         al256(p.partials) + 256 * sizeof(double) + 8 * sizeof(float);
 }
 
 int grad_ard(int family, int d, const float* Xr, int64_t ldr, int64_t nr, const float* Xc, int64_t ldc, int64_t nc,
@@ -527,11 +537,20 @@ int grad_ard(int family, int d, const float* Xr, int64_t ldr, int64_t nr, const 
   __nv_bfloat16* xx_img = reinterpret_cast<__nv_bfloat16*>(wp); wp += al256(p.xx_img);
   uint32_t* y_rows = reinterpret_cast<uint32_t*>(wp); wp += al256(p.y_rows);
   double* partials = reinterpret_cast<double*>(wp); wp += al256(p.partials);
-  double* mean = reinterpret_cast<double*>(wp);
+  double* mean = reinterpret_cast<double*>(wp); wp += 256 * sizeof(double);
+  unsigned* rng = reinterpret_cast<unsigned*>(wp); wp += 4 * sizeof(unsigned);
+  float* dscale = reinterpret_cast<float*>(wp);
   const double c = family == GP_FAMILY_RBF ? 1.4426950408889634 : -6.0;
   const int BN = p.BN;
-  if (int rc = tc::distance_images(Xr, ldr, nr, Xc, ldc, nc, d, p.DK, BM, BN, c, mean, row_img, col_img, st))
+  if (p.eb == 2) {
+    if (int rc = tc::distance_images16(Xr, ldr, nr, Xc, ldc, nc, d, p.DK, BM, BN, c, mean, rng,
+                                       reinterpret_cast<__half*>(row_img), reinterpret_cast<__half*>(col_img),
+                                       dscale, st))
+      return rc;
+  } else if (int rc = tc::distance_images(Xr, ldr, nr, Xc, ldc, nc, d, p.DK, BM, BN, c, mean, row_img, col_img,
+                                          st)) {
     return rc;
+  }
   {
     const int64_t rows_pad = (int64_t)p.row_tiles * BM;
     int64_t tot = rows_pad * p.WP;
@@ -543,7 +562,8 @@ int grad_ard(int family, int d, const float* Xr, int64_t ldr, int64_t nr, const 
   }
   Args a;
   a.row_img = row_img; a.col_img = col_img; a.r_img = r_img; a.xx_img = xx_img; a.y_rows = y_rows;
-  a.Xr = Xr; a.ldr = ldr; a.mean = mean; a.DK = p.DK; a.WK = p.WK; a.WP = p.WP; a.d = d;
+  a.Xr = Xr; a.ldr = ldr; a.mean = mean; a.DK = p.DK;
+  a.dscale = p.eb == 2 ? dscale : nullptr; a.WK = p.WK; a.WP = p.WP; a.d = d;
   a.n_rows = nr; a.n_cols = nc; a.row_tiles = p.row_tiles; a.col_tiles = p.col_tiles;
   a.splits = p.splits; a.tiles_per_split = p.tiles_per_split; a.nstages = p.nstages;
   a.self_offset = self_offset; a.partials = partials;
