@@ -66,6 +66,11 @@ def test_compute_sanitizer_clean(tool):
            sys.executable, os.path.join(REPO, "scripts", "sanitize_small.py")]
     r = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=1500)
     out = r.stdout + r.stderr
+    if "compute-sanitizer is closed" in out:
+        # the GPU pool disables the sanitizer (runs under it left GPUs needing
+        # a reset); out-of-bounds writes are then covered by the canary tests
+        # in test_gpu_bounds.py
+        pytest.skip("compute-sanitizer closed on this GPU pool")
     assert r.returncode == 0, out[-4000:]
     assert "sanitize workload ok" in out, out[-4000:]
     clean = "RACECHECK SUMMARY: 0 hazards displayed (0 errors, 0 warnings)" if tool == "racecheck" \
