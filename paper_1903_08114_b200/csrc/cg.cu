@@ -451,10 +451,14 @@ __global__ void __launch_bounds__(kZT) cg_precond_z_narrow(CgK s) {
 // The same with whole chunks moved by the TMA: when L is contiguous (ld = k)
 // and k is even (16-byte aligned chunk starts and sizes), thread 0 copies each
 // 32-row chunk of L (25.6 KB at k = 100) with one cp.async.bulk into a
-// double-buffered row-major tile; the R rows follow by cp.async. A warp owns 8
-// rows x 4 column quads, so the stride-k row reads are at most 2-way bank
-// conflicted. Even / odd kk accumulate separately (z differs from the forms
-// above in the last bits).
+// double-buffered row-major tile; the R rows follow by cp.async. A lane owns
+// 2 rows x 4 columns (one C load serves both rows: the one-row form was bound
+// by SMEM wavefronts, 5 LDS per 8 DFMA; 0.49 -> 0.35 ms at n = 10^6, k = 100)
+// and the k range is split between warp pairs (warps 0-1 kk < k/2, warps 2-3
+// the rest, partials added through SMEM), so every warp still covers 16 rows
+// of the 32-row chunk. (Three k ranges over 6 warps with R read from global
+// memory in the epilogue measured slower: 0.42 ms.) Even / odd kk accumulate
+// separately (z differs from the forms above in the last bits).
 constexpr int kZB = 32;           // rows per chunk
 static size_t pz_bulk_smem(int k) {
   return ((size_t)k * 16 + 2 * ((size_t)kZB * k + kZB * 16) + 16 * kZB) * sizeof(double) + 64;
@@ -481,7 +485,12 @@ __global__ void __launch_bounds__(128) cg_precond_z_bulk(CgK s) {
   int64_t r0, r1;
   row_range(s.n, r0, r1);
   const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-  const int rl = 8 * w + (ln >> 2), tq = ln & 3;  // row of the chunk, column quad
+  const int rl = 8 * w + (ln >> 2), tq = ln & 3;  // reduction slot, column quad
+  const int kh = w >> 1;                           // k half of this warp
+  const int ra = 16 * (w & 1) + (ln >> 2), rb = ra + 8;   // the lane's two rows of the chunk
+  const int khalf = ((k >> 1) + 1) & ~1;           // even split point
+  const int k0 = kh ? khalf : 0, k1 = kh ? k : khalf;
+  double* xch = sred;                              // [kZB][16] k-half partials (sred is free in the loop)
   const bool worker = tq < TQ;
   bool live[4];
 #pragma unroll
@@ -522,46 +531,79 @@ __global__ void __launch_bounds__(128) cg_precond_z_bulk(CgK s) {
     __syncthreads();
     const double* sL = sB + (size_t)b * bstride;
     const double* sR = sL + (size_t)kZB * k;
-    if (worker && rl < nr) {
+    const bool va = worker && ra < nr, vb = worker && rb < nr;
+    double sa[4] = {0.0, 0.0, 0.0, 0.0}, sb[4] = {0.0, 0.0, 0.0, 0.0};
+    if (va) {
       // even and odd kk in separate accumulators (k is even here): twice
       // the independent DFMA chains, the loop is latency-bound otherwise
-      double lc[4] = {0.0, 0.0, 0.0, 0.0}, lo[4] = {0.0, 0.0, 0.0, 0.0};
-      const double* lr = sL + (size_t)rl * k;
+      double ea[4] = {0.0, 0.0, 0.0, 0.0}, oa[4] = {0.0, 0.0, 0.0, 0.0};
+      double eb[4] = {0.0, 0.0, 0.0, 0.0}, ob[4] = {0.0, 0.0, 0.0, 0.0};
+      const double* pa = sL + (size_t)ra * k;
+      const double* pb = sL + (size_t)(vb ? rb : ra) * k;
       const double* cq = sC + 4 * tq;
-      for (int kk = 0; kk < k; kk += 2) {
-        const double2 lv = *reinterpret_cast<const double2*>(lr + kk);
+      for (int kk = k0; kk < k1; kk += 2) {
+        const double2 la = *reinterpret_cast<const double2*>(pa + kk);
+        const double2 lb = *reinterpret_cast<const double2*>(pb + kk);
         const double2 ca = *reinterpret_cast<const double2*>(cq + kk * TP);
         const double2 cb = *reinterpret_cast<const double2*>(cq + kk * TP + 2);
         const double2 da = *reinterpret_cast<const double2*>(cq + (kk + 1) * TP);
         const double2 db = *reinterpret_cast<const double2*>(cq + (kk + 1) * TP + 2);
-        lc[0] = fma(lv.x, ca.x, lc[0]);
-        lc[1] = fma(lv.x, ca.y, lc[1]);
-        lc[2] = fma(lv.x, cb.x, lc[2]);
-        lc[3] = fma(lv.x, cb.y, lc[3]);
-        lo[0] = fma(lv.y, da.x, lo[0]);
-        lo[1] = fma(lv.y, da.y, lo[1]);
-        lo[2] = fma(lv.y, db.x, lo[2]);
-        lo[3] = fma(lv.y, db.y, lo[3]);
+        ea[0] = fma(la.x, ca.x, ea[0]);
+        ea[1] = fma(la.x, ca.y, ea[1]);
+        ea[2] = fma(la.x, cb.x, ea[2]);
+        ea[3] = fma(la.x, cb.y, ea[3]);
+        oa[0] = fma(la.y, da.x, oa[0]);
+        oa[1] = fma(la.y, da.y, oa[1]);
+        oa[2] = fma(la.y, db.x, oa[2]);
+        oa[3] = fma(la.y, db.y, oa[3]);
+        eb[0] = fma(lb.x, ca.x, eb[0]);
+        eb[1] = fma(lb.x, ca.y, eb[1]);
+        eb[2] = fma(lb.x, cb.x, eb[2]);
+        eb[3] = fma(lb.x, cb.y, eb[3]);
+        ob[0] = fma(lb.y, da.x, ob[0]);
+        ob[1] = fma(lb.y, da.y, ob[1]);
+        ob[2] = fma(lb.y, db.x, ob[2]);
+        ob[3] = fma(lb.y, db.y, ob[3]);
       }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) lc[j] += lo[j];
-      const int64_t r = rc + rl;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        if (!live[j]) continue;
-        const int c = 4 * tq + j;
-        const double rv = sR[rl * 16 + c];
-        const double z = (rv - lc[j]) / s.pc_noise;
-        s.Z[r * s.ld + c] = z;
-        if (INIT) {
-          s.P[r * s.ld + c] = z;
-          s.P32[r * s.ld32 + c] = (float)z;
+        sa[j] = ea[j] + oa[j];
+        sb[j] = eb[j] + ob[j];
+      }
+      if (kh == 1) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          xch[ra * 16 + 4 * tq + j] = sa[j];
+          if (vb) xch[rb * 16 + 4 * tq + j] = sb[j];
         }
-        gam[j] += rv * z;
       }
     }
-    __syncthreads();   // buffer b is refilled by the issue two chunks on
+    __syncthreads();   // the second k half's partials are in xch
+    if (kh == 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rr = h ? rb : ra;
+        if (!(h ? vb : va)) continue;
+        const int64_t r = rc + rr;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (!live[j]) continue;
+          const int c = 4 * tq + j;
+          const double lc = (h ? sb[j] : sa[j]) + xch[rr * 16 + c];
+          const double rv = sR[rr * 16 + c];
+          const double z = (rv - lc) / s.pc_noise;
+          s.Z[r * s.ld + c] = z;
+          if (INIT) {
+            s.P[r * s.ld + c] = z;
+            s.P32[r * s.ld32 + c] = (float)z;
+          }
+          gam[j] += rv * z;
+        }
+      }
+    }
+    __syncthreads();   // xch is rewritten and buffer b refilled by the next chunks
   }
+  // warps 2-3 hold zero gam: their slots (16-31) add nothing
   if (worker) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) sred[(4 * tq + j) * kZB + rl] = gam[j];
