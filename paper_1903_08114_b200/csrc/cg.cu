@@ -76,7 +76,7 @@ __host__ __device__ inline int ltmul_scratch(int k, int t) {
   if (ltmul_tiled(k, t)) {
     const int KP = (k + 3) / 4 * 4, TP = (t + 3) / 4 * 4;
     const int stage = 2 * kLtCR * (KP + TP), red = 256 * 16;
-    return stage > red ? stage : red;
+    return (stage > red ? stage : red) + 2;   // + the two chunk mbarriers
   }
   return 16 * (k > 1 ? k : 1) + 16 * t;
 }
@@ -96,15 +96,36 @@ __device__ void block_ltmul(int64_t r0, int64_t r1, int k, int t, const double* 
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31, nw = kRT >> 5;
     // chunk copies (8-byte cp.async, zero-filled outside the rows / columns),
     // double buffered so the next chunk streams in during this one's FMAs
+    // contiguous L with k % 4 == 0 (rows of KP = k doubles, 32-byte aligned
+    // chunks): each chunk of L rows is ONE cp.async.bulk (TMA) issued by
+    // thread 0 and completed on an mbarrier, instead of 8-byte copies by
+    // every thread; rows past the end are never read, so no zero fill
+    const bool bulk = ldl == k && KP == k;
+    const int mb_off = 2 * stage > 256 * 16 ? 2 * stage : 256 * 16;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + mb_off);
+    if (bulk && threadIdx.x == 0) {
+      tc::mbar_init(tc::smem_u32(&bar[0]), 1);
+      tc::mbar_init(tc::smem_u32(&bar[1]), 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     auto issue = [&](int64_t rc, int b) {
       const int nr = (int)min((int64_t)kLtCR, r1 - rc);
       const uint32_t bl = (uint32_t)__cvta_generic_to_shared(sm + (size_t)b * stage);
       const uint32_t ba = bl + (uint32_t)(kLtCR * KP * 8);
+      if (bulk) {
+        if (threadIdx.x == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          const uint32_t bytes = (uint32_t)(nr * k * 8);
+          tc::mbar_expect_tx(tc::smem_u32(&bar[b]), bytes);
+          tc::bulk_g2s(bl, L + rc * k, bytes, tc::smem_u32(&bar[b]));
+        }
+      }
       for (int r = w; r < kLtCR; r += nw) {
         const bool rin = r < nr;
         const double* lr = L + (rin ? (rc + r) * ldl : 0);
         const double* ar = A + (rin ? (rc + r) * lda : 0);
-        for (int c = ln; c < KP; c += 32) cp_async8z(bl + (uint32_t)((r * KP + c) * 8), lr + (rin && c < k ? c : 0), rin && c < k);
+        if (!bulk)
+          for (int c = ln; c < KP; c += 32) cp_async8z(bl + (uint32_t)((r * KP + c) * 8), lr + (rin && c < k ? c : 0), rin && c < k);
         for (int c = ln; c < TP; c += 32) cp_async8z(ba + (uint32_t)((r * TP + c) * 8), ar + (rin && c < t ? c : 0), rin && c < t);
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
@@ -115,9 +136,10 @@ __device__ void block_ltmul(int64_t r0, int64_t r1, int k, int t, const double* 
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
     __syncthreads();   // the caller's writes of A (and prior use of sm) are complete
-    int b = 0;
+    int b = 0, ci = 0;
+    if (bulk) __syncthreads();   // barriers initialised before the first copy completes on them
     if (r0 < r1) issue(r0, 0);
-    for (int64_t rc = r0; rc < r1; rc += kLtCR, b ^= 1) {
+    for (int64_t rc = r0; rc < r1; rc += kLtCR, b ^= 1, ++ci) {
       const int nr = (int)min((int64_t)kLtCR, r1 - rc);
       if (rc + kLtCR < r1) {
         issue(rc + kLtCR, b ^ 1);
@@ -125,6 +147,7 @@ __device__ void block_ltmul(int64_t r0, int64_t r1, int k, int t, const double* 
       } else {
         asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
+      if (bulk) tc::mbar_wait(tc::smem_u32(&bar[b]), (ci >> 1) & 1);
       __syncthreads();
       const double* sLc = sm + (size_t)b * stage;
       const double* sAc = sLc + kLtCR * KP;
