@@ -1054,27 +1054,42 @@ __global__ void __launch_bounds__(1024) precond_factor_kernel(int k, double nois
   }
   __syncthreads();
   // right-looking Cholesky with one barrier per column: step j updates the
-  // trailing lower triangle with the unscaled column j over d_jj and scales
-  // column j - 1 (which no thread reads in step j)
-  double dprev = 1.0;
+  // trailing square (both triangles, so the column j a thread needs is read
+  // as row j: contiguous, conflict-free) with the unscaled column j over
+  // d_jj and scales column j - 1 (which no thread reads in step j). Threads
+  // form a 32 x 32 grid over (row i, column l): no index division.
+  // The pivot's 1 / d_jj, sqrt(d_jj) and 1 / sqrt(d_jj) are formed ONCE, by
+  // the thread that wrote d_jj last (thread 0 updates (j, j) in step j - 1),
+  // into per-column slots: fp64 division and square root in all 1024 threads
+  // every step cost more than the update itself.
+  double* s_inv = Cs + (size_t)k * k;   // [k]
+  double* s_sq = s_inv + k;             // [k]
+  double* s_rs = s_sq + k;              // [k]
+  const int tx = tid & 31, ty = tid >> 5, nty = nt >> 5;
+  auto pivot_terms = [&](int j) {
+    const double d = Cs[j * k + j];
+    if (!(d > 0.0) || !isfinite(d)) fail = 1;
+    s_inv[j] = 1.0 / d;
+    s_sq[j] = sqrt(d);
+    s_rs[j] = 1.0 / sqrt(d);
+  };
+  if (tid == 0) pivot_terms(0);
+  __syncthreads();
   for (int j = 0; j < k; ++j) {
-    const double djj = Cs[j * k + j];
-    if (tid == 0 && (!(djj > 0.0) || !isfinite(djj))) fail = 1;
     if (j >= 1) {
-      const double rs = 1.0 / sqrt(dprev);
+      const double rs = s_rs[j - 1];
       for (int i = j + tid; i < k; i += nt) Cs[i * k + j - 1] *= rs;
-      if (tid == 0) Cs[(j - 1) * k + j - 1] = sqrt(dprev);
+      if (tid == 0) Cs[(j - 1) * k + j - 1] = s_sq[j - 1];
     }
-    const double inv = 1.0 / djj;
-    const int m = k - j - 1;
-    for (int p = tid; p < m * m; p += nt) {
-      const int i = j + 1 + p / m, l = j + 1 + p % m;
-      if (l <= i) Cs[i * k + l] -= Cs[i * k + j] * Cs[l * k + j] * inv;
+    const double inv = s_inv[j];
+    for (int i = j + 1 + ty; i < k; i += nty) {
+      const double a = Cs[i * k + j];
+      for (int l = j + 1 + tx; l < k; l += 32) Cs[i * k + l] -= a * Cs[j * k + l] * inv;
     }
-    dprev = djj;
+    if (tid == 0 && j + 1 < k) pivot_terms(j + 1);   // (j + 1, j + 1) was this thread's first update
     __syncthreads();
   }
-  if (tid == 0) Cs[(k - 1) * k + k - 1] = sqrt(dprev);
+  if (tid == 0) Cs[(k - 1) * k + k - 1] = s_sq[k - 1];
   __syncthreads();
   if (fail) {
     if (tid == 0) info[0] = 1;
@@ -1090,12 +1105,10 @@ __global__ void __launch_bounds__(1024) precond_factor_kernel(int k, double nois
   }
   __syncthreads();
   for (int i = 0; i + 1 < k; ++i) {
-    const double rinv = 1.0 / Cs[i * k + i];
-    const int m = k - 1 - i;
-    for (int p = tid; p < m * (i + 1); p += nt) {
-      const int c = p / m, r = i + 1 + (p - c * m);
+    const double rinv = s_rs[i];   // 1 / C_ii
+    for (int c = ty; c <= i; c += nty) {
       const double xic = (c == i ? 1.0 : Cs[c * k + i]) * rinv;
-      Cs[c * k + r] -= Cs[r * k + i] * xic;
+      for (int r = i + 1 + tx; r < k; r += 32) Cs[c * k + r] -= Cs[r * k + i] * xic;
     }
     __syncthreads();
   }
@@ -1553,7 +1566,7 @@ int gp_precond_factor(int64_t n, int k, const double* L, int64_t ldl, double noi
   GP_REQUIRE(k >= 1 && noise > 0.0, "gp_precond_factor: k=%d noise=%g", k, noise);
   // chol <- L^T L
   if (int rc = gp_lt_mul(n, k, L, ldl, L, ldl, k, chol, partials, partials_len, stream)) return rc;
-  const size_t fsm = (size_t)k * k * sizeof(double);
+  const size_t fsm = ((size_t)k * k + 3 * (size_t)k) * sizeof(double);   // matrix + pivot terms
   if (k <= 160) {
     if (int rc = set_smem(precond_factor_kernel, fsm)) return rc;
     precond_factor_kernel<<<1, 1024, fsm, st>>>(k, noise, chol, Binv, logdet_tr_dev, info_dev);
