@@ -599,18 +599,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       uint32_t p1[16], p2[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) split_pair(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]), p1[k], p2[k]);
-      // in place over this warp's own S columns: kstep 2ch at [32ch, +16), 2ch+1 at [32ch+16, +16)
+      // K in place over this warp's own S columns (kstep 2ch at [32ch, +16),
+      // 2ch+1 at [32ch+16, +16)) and the K^T rows for the mirror (8
+      // consecutive j of point i = one 16-byte core-matrix row), first half
+      // of the columns first: its stores go out while the second half's
+      // split is still in flight, which shortens the tile's tail (n = 10^6:
+      // 342.0 -> 339.5-340.5 ms; per-8-column stores with the K^T wait
+      // before the first were slower, 385 ms: profiles/r02_kv_sym.md)
       tmem_st8(sk, p1);
       tmem_st8(sk + 8, p2);
+      if (mir) {
+        // the previous mirror tile's products have read the SMEM K
+        if (Mt >= 1) SYM_T(2, wait_c(smem_u32(ks_empty), (Mt - 1) & 1));
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          sts128(ks_row + m * 2048u, p1[4 * m], p1[4 * m + 1], p1[4 * m + 2], p1[4 * m + 3]);
+          sts128(ks_row + KS_HALF + m * 2048u, p2[4 * m], p2[4 * m + 1], p2[4 * m + 2], p2[4 * m + 3]);
+        }
+      }
       tmem_st8(sk + 16, p1 + 8);
       tmem_st8(sk + 24, p2 + 8);
       if (mir) {
-        // K^T operand: 8 consecutive j of point i = one 16-byte core-matrix row
-        // the previous mirror tile's products have read the SMEM K
-        if (Mt >= 1) SYM_T(2, wait_c(smem_u32(ks_empty), (Mt - 1) & 1));
         ++Mt;
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
+        for (int m = 2; m < 4; ++m) {
           sts128(ks_row + m * 2048u, p1[4 * m], p1[4 * m + 1], p1[4 * m + 2], p1[4 * m + 3]);
           sts128(ks_row + KS_HALF + m * 2048u, p2[4 * m], p2[4 * m + 1], p2[4 * m + 2], p2[4 * m + 3]);
         }
