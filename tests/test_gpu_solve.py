@@ -375,3 +375,26 @@ def test_large_d_gradient_uses_the_narrow_operands():
     ref = LK.assemble_gradients(m, LK._grad_forms_sym_raw(m, d, Xs32, Ys, Rs), a, S, W, pc, n)
     g = np.array([got[k] for k in ref]), np.array(list(ref.values()))
     assert np.abs(g[0] - g[1]).max() <= 1e-3 * np.abs(g[1]).max()
+
+
+@pytest.mark.parametrize("n,k,t,strided", [(1000, 100, 11, False), (999, 4, 3, False), (4097, 6, 11, False),
+                                           (3333, 128, 16, False), (2000, 100, 11, True), (70, 2, 1, False)])
+def test_lt_mul_and_woodbury_shapes(n, k, t, strided):
+    """L^T V (gp_lt_mul: TMA-bulk chunks of L when L is contiguous with
+    k % 4 == 0, 8-byte copies otherwise; ragged last chunks) and one
+    preconditioned CG solve on the same factor against numpy, fp64."""
+    import torch
+    from paper_1903_08114_b200 import _ops
+    rng = np.random.default_rng(n + k + t)
+    Lh = rng.standard_normal((n, k + 3 if strided else k))
+    V = rng.standard_normal((n, t))
+    L = torch.from_numpy(Lh).cuda()[:, :k] if strided else torch.from_numpy(Lh).cuda()
+    got = _ops.lt_mul(L, torch.from_numpy(V).cuda()).cpu().numpy()
+    np.testing.assert_allclose(got, Lh[:, :k].T @ V, rtol=1e-12, atol=1e-10 * np.sqrt(n))
+    # P^{-1} applied through the device mBCG's Woodbury kernels on an SPD
+    # system whose preconditioner is exact (A = noise I + L L^T): one iteration
+    noise = 0.5
+    pc = precond.build_preconditioner(L.contiguous(), noise)
+    A = noise * np.eye(n) + Lh[:, :k] @ Lh[:, :k].T
+    sol = cg.mbcg_device(lambda X: torch.from_numpy(A).cuda() @ X, torch.from_numpy(V).cuda(), 1e-10, 50, pc)
+    np.testing.assert_allclose(sol.U.cpu().numpy(), np.linalg.solve(A, V), rtol=0, atol=1e-8)
