@@ -72,9 +72,10 @@ constexpr uint32_t STAGE_BYTES = TN * BT * 8u;       // fixed-point sums of one 
 // function of the item index, so the fixed-point result does not depend on
 // the grid size or on how the chunks are split across devices. Longer chunks
 // carry O_I across more items (fewer flushes; n = 10^6: 4 -> 16 items is
-// 360 -> 354 ms) but leave fewer chunks than CTAs at small n.
+// 360 -> 354 ms, 16 -> 32 is 339.4 -> 337.8 ms, 64 no better) but leave
+// fewer chunks than CTAs at small n.
 static int item_chunk(int n_items) {
-  for (int c = 16; c > 4; c >>= 1)
+  for (int c = 32; c > 4; c >>= 1)
     if (n_items >= 4 * 148 * c) return c;   // at least 4 chunks per SM of a full B200
   return 4;
 }
