@@ -655,8 +655,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       const bool in = row < a.n;
 #pragma unroll
       for (int c = 0; c < TN; ++c) {
+        if (c >= a.t) break;   // only the t live columns are staged and reduced
         long long x = 0;
-        if (c < a.t && in) {
+        if (in) {
           // v 2^E_c truncated toward zero (exact scaling: |v| 2^E_c <= 2^61 by
           // the choice of E_c); one F2I on the XU pipe, which has headroom
           if (fabsf(v[c]) < INFINITY) x = __float2ll_rz(v[c] * scale_s[c]);
@@ -667,8 +668,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       drain_bar();
       if (issuer) {
-        for (int c = 0; c < a.t; ++c)
-          bulk_red_u64(a.acc + row0 * a.t + (int64_t)c * BT, smem_u32(sb + c * BT), BT * 8u);
+        // the t columns of a 128-row block are contiguous in both the staging
+        // buffer and the row-block-major sums: ONE reduce-add of t x 1 KB
+        // (t separate 1 KB reduce-adds kept the drain's issuer on the
+        // critical path: n = 10^6 337.9 -> 328.5 ms)
+        bulk_red_u64(a.acc + row0 * a.t, smem_u32(sb), (uint32_t)a.t * BT * 8u);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
       ++nflush;
