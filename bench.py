@@ -390,7 +390,7 @@ def e2e_run(args, w, n, X, y, model, comm, r0, r1):
     import torch.distributed as dist
     from paper_1903_08114_b200 import _device as D, _ops
     from paper_1903_08114_b200.cg import FusedOperator, MbcgRun
-    from paper_1903_08114_b200.likelihood import build_kernel_preconditioner, draw_probes_device
+    from paper_1903_08114_b200.likelihood import ProbeDraws, build_kernel_preconditioner, draw_probes_device
 
     steps = args.steps
 
@@ -401,21 +401,15 @@ def e2e_run(args, w, n, X, y, model, comm, r0, r1):
         if comm:
             dist.barrier()
         t0 = time.perf_counter()
-        ps = D.PointSet(Xh)
         # the solve's setup is inside the timed region too: pivoted-Cholesky
         # preconditioner and the seeded N(0, P) probes (host PCG64 normals
         # uploaded, L z1 on the device), as mll_value_and_grad does per call
-        # (the host normals are drawn while the device factorises, as in
-        # mll_value_and_grad)
-        draws = []
-
-        def host_draws():
-            rng = np.random.default_rng(0)
-            draws.append(rng.standard_normal((w.rank, T_RHS - 1)))
-            draws.append(rng.standard_normal((n, T_RHS - 1)))
-
-        precond = build_kernel_preconditioner(model, ps, w.rank, overlap=host_draws)
-        Z = draw_probes_device(n, T_RHS - 1, 0, precond, tuple(draws) if draws else None)
+        # (ProbeDraws: the host normals are drawn on a helper thread that
+        # overlaps the upload and the factorisation)
+        draws = ProbeDraws(0, w.rank, n, T_RHS - 1)
+        ps = D.PointSet(Xh)
+        precond = build_kernel_preconditioner(model, ps, w.rank, overlap=draws.overlap)
+        Z = draw_probes_device(n, T_RHS - 1, 0, precond, draws.result())
         B = torch.cat([D.to_device(yh)[:, None], Z], dim=1)[r0:r1].contiguous()
         Xs32, _ = ps.scaled(model.lengthscales)
         kv = _ops.training_operator(model.family_code, w.d, Xs32, 1.0, 0.0, -1, comm, algo=args.algo)

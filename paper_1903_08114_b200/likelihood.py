@@ -91,11 +91,50 @@ def draw_probes_device(n: int, t: int, seed: int, cache, draws=None):
     """`draws`: the (z1, z2) normals already taken from default_rng(seed) for
     a rank-`cache.rank` preconditioner (drawn while the factor was built)."""
     rng = np.random.default_rng(seed)
-    if cache is None:
-        return D.to_device(rng.standard_normal((n, t)))
+    if cache is None:   # z1 is empty: z2 is the stream's first n x t normals
+        return D.to_device(draws[1] if draws is not None else rng.standard_normal((n, t)))
     if draws is not None and draws[0].shape[0] != cache.rank:
         draws = None   # the factorisation stopped early: the z2 stream position differs
     return _pc.precond_sample_device(cache, rng, t, draws)
+
+
+class ProbeDraws:
+    """The seeded probes' host normals (likelihood.py:94-101: z1 = k x t,
+    then z2 = n x t, from default_rng(seed)), bit-identical to the reference.
+    Large blocks (>= 2^20 normals) are drawn on a helper thread started
+    before the inputs are uploaded, so the draw overlaps the upload, the
+    prescale and the pivoted Cholesky (numpy's generator fills without the
+    GIL); small ones are drawn inline while the device factorises."""
+
+    THREAD_MIN = 1 << 20
+
+    def __init__(self, seed: int, k: int, n: int, t: int):
+        self.args = (seed, k, n, t)
+        self.out = None
+        self.thread = None
+        if n * t >= self.THREAD_MIN:
+            import threading
+            self.thread = threading.Thread(target=self._run, daemon=True)
+            self.thread.start()
+
+    def _run(self):
+        seed, k, n, t = self.args
+        rng = np.random.default_rng(seed)
+        z1 = rng.standard_normal((k, t))
+        self.out = (z1, rng.standard_normal((n, t)))
+
+    def overlap(self):
+        """Host work to run while the device factorises (the inline case)."""
+        if self.thread is None and self.out is None:
+            self._run()
+
+    def result(self):
+        """(z1, z2), or None if the draw failed (the caller then draws)."""
+        if self.thread is not None:
+            self.thread.join()
+        elif self.out is None:
+            self._run()
+        return self.out
 
 
 def draw_probes(n: int, t: int, seed: int, cache) -> np.ndarray:
@@ -125,6 +164,10 @@ def mll_value_and_grad(model: KernelModel, X, y, plan: PartitionPlan, pool: Work
     """log p(y) and d/dtheta for every trainable hyperparameter
     (likelihood.py:104-163), computed on the GPU."""
     T = D.torch()
+    n0 = X.n if isinstance(X, D.PointSet) else len(X)
+    k0 = min(cg_config.precond_rank, n0) if cg_config.precond_rank > 0 else 0
+    # started before the upload; the sharded path below draws its own
+    draws = ProbeDraws(probe_seed, k0, n0, cg_config.probes) if active_comm(n0) is None else None
     ps = D.points(X)
     n = ps.n
     yd = D.to_device(y)
@@ -139,18 +182,10 @@ def mll_value_and_grad(model: KernelModel, X, y, plan: PartitionPlan, pool: Work
         return mll_value_and_grad_sharded(model, ps, yd, cg_config, probe_seed, comm)
     t = cg_config.probes
     yc = yd - model.mean
-    # the probes' host normals (likelihood.py:94-101: z1 = k x t before
-    # z2 = n x t) are drawn while the device runs the pivoted Cholesky
-    k_req = min(cg_config.precond_rank, n) if cg_config.precond_rank > 0 else 0
-    draws = []
-
-    def host_draws():
-        rng = np.random.default_rng(probe_seed)
-        draws.append(rng.standard_normal((k_req, t)))
-        draws.append(rng.standard_normal((n, t)))
-
-    cache = build_kernel_preconditioner(model, ps, cg_config.precond_rank, overlap=host_draws)
-    Z = draw_probes_device(n, t, probe_seed, cache, tuple(draws) if draws else None)
+    # the probes' host normals (likelihood.py:94-101) come from ProbeDraws:
+    # a helper thread for large n, else drawn while the device factorises
+    cache = build_kernel_preconditioner(model, ps, cg_config.precond_rank, overlap=draws.overlap)
+    Z = draw_probes_device(n, t, probe_seed, cache, draws.result())
     op = training_operator(model, ps, precision=cg_config.precision, workers=pool.workers, t=t + 1)
     B = T.cat([yc[:, None], Z], dim=1).contiguous()
     sol = mbcg_device(op, B, cg_config.tolerance, cg_config.max_iters, cache)
