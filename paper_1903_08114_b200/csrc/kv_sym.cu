@@ -643,7 +643,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kv_sym_kernel(const Args a) {
     const int i_loc = q * 32 + lane;
     uint32_t K = 0;
     // 128 output rows x t columns -> fixed point -> SMEM staging (column-major,
-    // the global layout) -> one TMA bulk reduce-add per column, issued by one
+    // the global layout) -> one TMA bulk reduce-add per 128-row block, issued by one
     // thread; the L2 does the 64-bit integer adds at line granularity
     const bool issuer = warp == DRAIN_WARP0 && lane == 0;
     uint32_t nflush = 0;
